@@ -1,0 +1,188 @@
+/*
+ * pushpull.h — C ABI of the B200-native push-pull library (libpushpull.so).
+ *
+ * Hot path of Yang, Buluç, Owens, "Implementing Push-Pull Efficiently in
+ * GraphBLAS" (ICPP'18, arXiv 1804.03327): the masked Boolean-semiring matvec
+ * GrB_mxv that drives direction-optimised BFS.  Citations: P:n = PAPER.md line n
+ * (Sec./Eq./Alg. given beside it); DESIGN.md Rn = the reading DESIGN.md fixes
+ * where the paper is silent or ambiguous.
+ *
+ * Conventions (apply to every call):
+ *  - Every function returns pp_status and never throws across the ABI.  On error
+ *    pp_last_error() returns a thread-local message naming the offending
+ *    argument / row / edge; outputs are then unspecified.
+ *  - Ownership: the caller owns every buffer it passes.  pp_graph_upload COPIES
+ *    the graph to device memory the returned handle owns (freed by
+ *    pp_graph_free).  Output vectors/arrays are caller-allocated; a torch
+ *    tensor's data_ptr() is fine.
+ *  - Streams: all device work is stream-ordered on the ctx stream (a
+ *    cudaStream_t, NULL = legacy default stream).  Calls that return a host
+ *    value (pp_mxv's w->nnz when requested, pp_bfs with stats or with a host
+ *    depth/parent pointer) synchronise that stream before returning.
+ *  - Threading: one ctx per host thread; the library starts no host threads.
+ *  - Vertex ids are uint32 (n < 2^32).  Graph offsets are accepted as int64.
+ *  - There is no CPU fallback: without a usable CUDA device every call that needs
+ *    one fails with PP_ERR_CUDA.
+ */
+#ifndef PUSHPULL_H
+#define PUSHPULL_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PP_OK = 0,
+  PP_ERR_ARG = 1,          /* NULL / inconsistent argument                          */
+  PP_ERR_RANGE = 2,        /* source or vertex id out of range         */
+  PP_ERR_DIM = 3,          /* dimension / vector-format mismatch     */
+  PP_ERR_GRAPH = 4,        /* malformed CSR/CSC under PP_GRAPH_VALIDATE     */
+  PP_ERR_UNSUPPORTED = 5,  /* semiring other than Boolean, or a size limit          */
+  PP_ERR_CUDA = 6,         /* CUDA runtime error (incl. no device)                  */
+  PP_ERR_NCCL = 7,         /* reserved for the distributed context                  */
+  PP_ERR_OOM = 8,          /* device allocation failed                              */
+  PP_ERR_TIMEOUT = 9       /* device-side watchdog fired (persistent BFS barrier)   */
+} pp_status;
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char* pp_last_error(void);
+/* Library version string. */
+const char* pp_version(void);
+
+typedef struct pp_ctx_s* pp_ctx;     /* device + stream                                  */
+typedef struct pp_graph_s* pp_graph; /* device-resident CSR + CSC, owned by the library */
+
+/* Bind a context to CUDA `device` and `cuda_stream` (a cudaStream_t or NULL).
+ * The stream must outlive the context.  Fails with PP_ERR_CUDA without a GPU. */
+pp_status pp_ctx_create(int device, void* cuda_stream, pp_ctx* out);
+pp_status pp_ctx_destroy(pp_ctx ctx);
+/* Number of kernels this library has launched on `ctx` so far (bench evidence). */
+pp_status pp_ctx_launch_count(pp_ctx ctx, uint64_t* out);
+
+/* ---- graph residency (P:358 CSR for push, P:318 A^T rows for pull) ----
+ * A is n x n.  CSR row u lists the out-neighbours w, (u,w) in E: push expands
+ * rows of CSR (= columns of A^T, Alg. 3).  CSC row v lists the in-neighbours u:
+ * pull scans rows of A^T (Alg. 2).  Column ids must be < n; with
+ * PP_GRAPH_VALIDATE offsets must be monotone with off[0]=0, off[n]=nnz, and each
+ * row strictly increasing (sorted, no duplicates; PAPER.md:467 preprocessing).
+ * Sorted rows are what make pull's early exit return the min-id parent.
+ * PP_GRAPH_SYMMETRIC: csc_off/csc_idx may be NULL and then alias CSR (every
+ * configuration here is undirected).  Host pointers unless
+ * PP_GRAPH_DEVICE.  Offsets are stored on device as uint32 when nnz < 2^32,
+ * else uint64.  Returns PP_ERR_GRAPH (message names the row) on a malformed
+ * graph under VALIDATE, PP_ERR_OOM if it does not fit. */
+#define PP_GRAPH_SYMMETRIC 1u
+#define PP_GRAPH_DEVICE 2u
+#define PP_GRAPH_VALIDATE 4u
+pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr_off,
+                          const uint32_t* csr_idx, const int64_t* csc_off,
+                          const uint32_t* csc_idx, uint32_t flags, pp_graph* out);
+pp_status pp_graph_free(pp_graph g);
+/* n, nnz, device bytes held by the handle (graph + BFS work buffers). */
+pp_status pp_graph_info(pp_graph g, int64_t* n, int64_t* nnz, int64_t* device_bytes);
+
+/* ---- vectors (P:83 sparse = sorted index list; P:435 DenseVector) ----------------------
+ * LIST:   data = device uint32[capacity], ids sorted ascending and unique, nnz
+ *         entries valid (outputs are produced sorted).
+ * BITMAP: data = device uint32[ceil(n/32)], bit i of word i/32 = element i; bits
+ *         >= n are zero on output.  nnz = popcount, or -1 = unknown on input. */
+typedef enum { PP_VEC_LIST = 0, PP_VEC_BITMAP = 1 } pp_vec_format;
+typedef struct {
+  int32_t format;
+  int64_t n;
+  int64_t nnz;
+  void* data;
+  int64_t capacity; /* LIST: entries allocated in data; BITMAP: ignored */
+} pp_vector;
+
+/* ---- masked matvec GrB_mxv(w, mask, accum, semiring, A, u, desc) -------
+ * Boolean semiring ({0,1}, AND, OR, 0) (Alg. 1 caption P:204; R3):
+ *   t(i)    = OR_j  Op(i,j) AND u(j),  Op = A^T if transpose else A      Eq. 2, Eq. 3
+ *   pass(i) = mask ? (mask(i) != 0) XOR complement : 1                  P:152, Alg. 2 line 3
+ *   z(i)    = accum ? w_in(i) OR t(i) : t(i)                            Alg. 2 line 10 (R6)
+ *   w(i)    = pass(i) ? z(i) : (replace ? 0 : w_in(i))                  Eq. 4, R5
+ * direction PULL = row-based (Alg. 2, rows of Op, early exit on OR);
+ * PUSH = column-based (Alg. 3, columns of Op, mask filter before the OR-merge);
+ * AUTO = the Convert hysteresis of P:368/433 on nnz(u)/n vs switchpoint with
+ * prev_nnz as its state (R25).  The result never depends on the
+ * direction, only the time.  u / mask may be LIST or BITMAP (converted as
+ * needed); w's format is the caller's choice; with accum or replace == 0, w
+ * holds w_in on entry in that same format.  Errors: PP_ERR_ARG for complement
+ * without a mask (R9) or a NULL vector; PP_ERR_DIM for length/format mismatch
+ * or a LIST output whose capacity is too small (w->nnz then holds the needed
+ * size); PP_ERR_UNSUPPORTED for a semiring other than PP_SR_LOR_LAND.
+ * w->nnz is set when want_nnz (synchronises), else -1 for BITMAP output. */
+typedef enum { PP_SR_LOR_LAND = 0 } pp_semiring;
+typedef enum { PP_DIR_AUTO = 0, PP_DIR_PUSH = 1, PP_DIR_PULL = 2 } pp_direction;
+typedef struct {
+  const pp_vector* mask; /* NULL: no mask                                          */
+  int32_t complement;    /* structural complement scmp                     */
+  int32_t semiring;      /* PP_SR_LOR_LAND only                                    */
+  int32_t accum;         /* 0: w = t ; 1: w = w_in OR t                            */
+  int32_t replace;       /* 1: masked-out outputs are 0 (Eq. 4); 0: keep w_in      */
+  int32_t direction;     /* pp_direction                                           */
+  int32_t early_exit;    /* 1: stop a row at its first true term (only legal for OR) */
+  int32_t transpose;     /* 1: w = A^T u (traversal, f' = A^T f); 0: w = A u       */
+  int32_t want_nnz;      /* 1: compute w->nnz (synchronises)                       */
+  double switchpoint;    /* AUTO threshold on nnz(u)/n, default 0.01       */
+  int64_t prev_nnz;      /* Convert hysteresis state, -1 = none                    */
+} pp_descriptor;
+/* Fill *d with the defaults: no mask, replace=1, early_exit=1, transpose=1,
+ * direction AUTO, switchpoint 0.01, prev_nnz -1, want_nnz 1. */
+pp_status pp_descriptor_default(pp_descriptor* d);
+pp_status pp_mxv(pp_graph g, pp_vector* w, const pp_descriptor* desc, const pp_vector* u);
+
+/* ---- direction-optimised BFS, Algorithm 1 --------------------------------------
+ * depth: int32[n], device or host memory (detected); 0 = unreached, source = 1,
+ *   level-k vertices = k (Alg. 1 convention, R1).  Host memory means the
+ *   result is copied back inside the call (end-to-end path).
+ * parent: int32[n] or NULL; canonical min-id parent at depth-1 (R14),
+ *   parent[source] = source, unreached = -1.
+ * Direction per level (Opt. 1): mode DO uses `heuristic`:
+ *   PP_HEUR_EDGES   Beamer edge-count rule (P:366 first sentence; R11), alpha=15, beta=18;
+ *   PP_HEUR_PAPER_R the paper's r = nnz(f)/M rule (R10), alpha=beta=0.01;
+ *   alpha/beta <= 0 select those defaults.  Level 1 is push (pull in PULL_ONLY).
+ * Pull levels compute A^T v .* !v (operand reuse P:284, masking P:270, early
+ * exit P:278); push levels compute A^T f .* !v column-wise (Alg. 3).
+ * toggles (ablation) never change depths or parents.
+ * stats (host, nullable): per-level direction / counters, synchronises.
+ * Errors: PP_ERR_RANGE for a bad source, PP_ERR_TIMEOUT if the device watchdog
+ * fired (never expected; depth is then invalid). */
+typedef enum { PP_HEUR_EDGES = 0, PP_HEUR_PAPER_R = 1 } pp_heuristic;
+typedef enum { PP_MODE_DO = 0, PP_MODE_PUSH_ONLY = 1, PP_MODE_PULL_ONLY = 2 } pp_mode;
+#define PP_OPT_NO_MASKING 1u   /* pull scans every row, then filters by !v (Opt. 2 off) */
+#define PP_OPT_NO_EARLYEXIT 2u /* pull scans whole rows (Opt. 3 off)                     */
+#define PP_OPT_NO_REUSE 4u     /* pull tests the frontier f instead of v (Opt. 4 off)    */
+typedef struct {
+  int32_t heuristic;    /* pp_heuristic                                   */
+  int32_t mode;         /* pp_mode                                        */
+  double alpha, beta;   /* <= 0: defaults of the chosen heuristic          */
+  int32_t want_parents; /* ignored if parent == NULL                       */
+  uint32_t toggles;     /* PP_OPT_* (0 = all of the paper's optimisations) */
+} pp_bfs_options;
+pp_status pp_bfs_options_default(pp_bfs_options* o);
+
+/* Per-level record of level k (1-based) at index k-1: dir (0 push, 1 pull),
+ * c = |frontier discovered by level k|, m_f = sum of its out-degrees (Eq. 1),
+ * m_u = sum of in-degrees still unvisited after level k.  Arrays are
+ * caller-owned host memory of `capacity` entries (any may be NULL).  levels =
+ * number of levels executed (= max depth); reached = #vertices with depth > 0. */
+typedef struct {
+  int32_t levels;
+  int64_t reached;
+  int32_t capacity;
+  int8_t* dir;
+  int64_t* c;
+  int64_t* m_f;
+  int64_t* m_u;
+} pp_bfs_stats;
+
+pp_status pp_bfs(pp_graph g, int64_t source, const pp_bfs_options* opts, int32_t* depth,
+                 int32_t* parent, pp_bfs_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PUSHPULL_H */

@@ -1,0 +1,517 @@
+// capi.cpp — the C ABI of include/pushpull.h: argument validation, ownership, device
+// residency and the host side of pp_mxv / pp_bfs.  Every compute step runs in the
+// CUDA kernels of bfs.cu / mxv.cu / graph.cu; there is no CPU path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "pp_internal.h"
+
+namespace pp {
+static thread_local std::string g_err;
+
+void set_error(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+}
+
+pp_status cuda_fail(cudaError_t e, const char* what) {
+  set_error("%s: %s", what, cudaGetErrorString(e));
+  cudaGetLastError();  // clear sticky-free errors
+  return e == cudaErrorMemoryAllocation ? PP_ERR_OOM : PP_ERR_CUDA;
+}
+}  // namespace pp
+
+using namespace pp;
+
+#define PP_CK(call, what)                                 \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) return pp::cuda_fail(_e, what); \
+  } while (0)
+
+#define PP_FAIL(code, ...)  \
+  do {                      \
+    set_error(__VA_ARGS__); \
+    return code;            \
+  } while (0)
+
+namespace {
+
+template <typename T>
+pp_status dalloc(T** p, size_t count, int64_t* bytes, const char* what) {
+  size_t b = sizeof(T) * std::max<size_t>(count, 1);
+  cudaError_t e = cudaMalloc((void**)p, b);
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    return cuda_fail(e, what);
+  }
+  *bytes += (int64_t)b;
+  return PP_OK;
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+void free_graph(pp_graph g) {
+  if (!g) return;
+  void* ptrs[] = {g->off, g->idx, g->symmetric ? nullptr : g->coff,
+                  g->symmetric ? nullptr : (void*)g->cidx, g->isolated, g->vis[0], g->vis[1],
+                  g->L[0], g->L[1], g->H[0], g->H[1], g->ctr, g->stats, g->bar,
+                  g->sbits[0], g->sbits[1], g->sbits[2], g->sbits[3], g->sblock, g->scount,
+                  g->dtmp[0], g->dtmp[1]};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (g->status_host) cudaFreeHost(g->status_host);
+  if (g->scount_host) cudaFreeHost(g->scount_host);
+  delete g;
+}
+
+struct Guard {  // frees a half-built graph on early return
+  pp_graph g;
+  ~Guard() { free_graph(g); }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* pp_last_error(void) { return g_err.c_str(); }
+const char* pp_version(void) { return "pushpull-b200 0.1 (sm_100a)"; }
+
+pp_status pp_ctx_create(int device, void* cuda_stream, pp_ctx* out) {
+  if (!out) PP_FAIL(PP_ERR_ARG, "pp_ctx_create: out is NULL");
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    PP_FAIL(PP_ERR_CUDA, "pp_ctx_create: no CUDA device (%s); there is no CPU fallback",
+            e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+  }
+  if (device < 0 || device >= count) PP_FAIL(PP_ERR_ARG, "pp_ctx_create: device %d of %d", device, count);
+  PP_CK(cudaSetDevice(device), "cudaSetDevice");
+  cudaDeviceProp prop;
+  PP_CK(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  if (prop.major != 10 || prop.minor != 0)
+    PP_FAIL(PP_ERR_UNSUPPORTED, "pp_ctx_create: built for sm_100a (B200), device is sm_%d%d",
+            prop.major, prop.minor);
+  int coop = 0;
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+  if (!coop) PP_FAIL(PP_ERR_UNSUPPORTED, "pp_ctx_create: device lacks cooperative launch");
+  pp_ctx c = new pp_ctx_s;
+  c->device = device;
+  c->stream = (cudaStream_t)cuda_stream;
+  c->num_sms = prop.multiProcessorCount;
+  *out = c;
+  return PP_OK;
+}
+
+static void ctx_release(pp_ctx ctx) {
+  if (--ctx->refs == 0) delete ctx;
+}
+
+pp_status pp_ctx_destroy(pp_ctx ctx) {
+  if (!ctx) PP_FAIL(PP_ERR_ARG, "pp_ctx_destroy: NULL ctx");
+  ctx_release(ctx);  // graphs still alive keep the context until they are freed
+  return PP_OK;
+}
+
+pp_status pp_ctx_launch_count(pp_ctx ctx, uint64_t* out) {
+  if (!ctx || !out) PP_FAIL(PP_ERR_ARG, "pp_ctx_launch_count: NULL argument");
+  *out = ctx->launches;
+  return PP_OK;
+}
+
+pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr_off,
+                          const uint32_t* csr_idx, const int64_t* csc_off,
+                          const uint32_t* csc_idx, uint32_t flags, pp_graph* out) {
+  if (!ctx || !out || !csr_off || (nnz > 0 && !csr_idx))
+    PP_FAIL(PP_ERR_ARG, "pp_graph_upload: NULL argument");
+  *out = nullptr;
+  const bool symmetric = (flags & PP_GRAPH_SYMMETRIC) != 0;
+  if (!symmetric && (!csc_off || (nnz > 0 && !csc_idx)))
+    PP_FAIL(PP_ERR_ARG, "pp_graph_upload: CSC required unless PP_GRAPH_SYMMETRIC");
+  if (symmetric) {
+    csc_off = csr_off;
+    csc_idx = csr_idx;
+  }
+  if (n < 1 || n >= (int64_t)0xFFFFFFFFll)
+    PP_FAIL(PP_ERR_UNSUPPORTED, "pp_graph_upload: n=%lld outside [1, 2^32-1)", (long long)n);
+  if (nnz < 0) PP_FAIL(PP_ERR_ARG, "pp_graph_upload: nnz < 0");
+  PP_CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaStream_t st = ctx->stream;
+
+  pp_graph g = new pp_graph_s;
+  Guard guard{g};
+  g->ctx = ctx;
+  g->n = n;
+  g->nnz = nnz;
+  g->symmetric = symmetric;
+  g->off64 = nnz >= (int64_t)0xFFFFFFFFll;
+  const int64_t words = (n + 31) / 32;
+  g->nwords = (uint32_t)(((words + 31) / 32) * 32);
+  int64_t& bytes = g->device_bytes;
+  pp_status s;
+
+  // int64 offsets staged on device (host input copied, device input used in place)
+  const bool dev = (flags & PP_GRAPH_DEVICE) != 0;
+  const int64_t* d_off64 = csr_off;
+  const int64_t* d_coff64 = csc_off;
+  if (!dev) {
+    int64_t junk = 0;
+    if ((s = dalloc(&g->dtmp[0], (size_t)(n + 1) * 2, &junk, "offset staging")) != PP_OK) return s;
+    PP_CK(cudaMemcpyAsync(g->dtmp[0], csr_off, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, st),
+          "copy offsets");
+    d_off64 = (const int64_t*)g->dtmp[0];
+    if (symmetric) {
+      d_coff64 = d_off64;
+    } else {
+      PP_CK(cudaMemcpyAsync((int64_t*)g->dtmp[0] + (n + 1), csc_off, sizeof(int64_t) * (n + 1),
+                            cudaMemcpyHostToDevice, st),
+            "copy csc offsets");
+      d_coff64 = (const int64_t*)g->dtmp[0] + (n + 1);
+    }
+  }
+  // offsets boundary values
+  int64_t ends[4];
+  PP_CK(cudaMemcpyAsync(&ends[0], d_off64, 8, cudaMemcpyDefault, st), "read off[0]");
+  PP_CK(cudaMemcpyAsync(&ends[1], d_off64 + n, 8, cudaMemcpyDefault, st), "read off[n]");
+  PP_CK(cudaMemcpyAsync(&ends[2], d_coff64, 8, cudaMemcpyDefault, st), "read coff[0]");
+  PP_CK(cudaMemcpyAsync(&ends[3], d_coff64 + n, 8, cudaMemcpyDefault, st), "read coff[n]");
+  PP_CK(cudaStreamSynchronize(st), "sync");
+  if (ends[0] != 0 || ends[1] != nnz)
+    PP_FAIL(PP_ERR_GRAPH, "pp_graph_upload: CSR off[0]=%lld off[n]=%lld, expected 0 and nnz=%lld",
+            (long long)ends[0], (long long)ends[1], (long long)nnz);
+  if (ends[2] != 0 || ends[3] != nnz)
+    PP_FAIL(PP_ERR_GRAPH, "pp_graph_upload: CSC off[0]=%lld off[n]=%lld, expected 0 and nnz=%lld",
+            (long long)ends[2], (long long)ends[3], (long long)nnz);
+
+  // column ids
+  if ((s = dalloc(&g->idx, (size_t)nnz, &bytes, "csr idx")) != PP_OK) return s;
+  if (nnz) PP_CK(cudaMemcpyAsync(g->idx, csr_idx, sizeof(uint32_t) * nnz, cudaMemcpyDefault, st), "copy idx");
+  if (symmetric) {
+    g->cidx = g->idx;
+  } else {
+    if ((s = dalloc(&g->cidx, (size_t)nnz, &bytes, "csc idx")) != PP_OK) return s;
+    if (nnz)
+      PP_CK(cudaMemcpyAsync(g->cidx, csc_idx, sizeof(uint32_t) * nnz, cudaMemcpyDefault, st),
+            "copy csc idx");
+  }
+  // small control buffers
+  if ((s = dalloc(&g->scount, 8, &bytes, "counters")) != PP_OK) return s;
+  PP_CK(cudaMallocHost((void**)&g->scount_host, 8 * sizeof(unsigned long long)), "pinned counters");
+  PP_CK(cudaMallocHost((void**)&g->status_host, sizeof(BfsStatus)), "pinned status");
+
+  if (flags & PP_GRAPH_VALIDATE) {
+    for (int side = 0; side < (symmetric ? 1 : 2); ++side) {
+      PP_CK(cudaMemsetAsync(g->scount, 0xFF, sizeof(unsigned long long), st), "memset");
+      PP_CK(launch_graph_validate(g, side ? d_coff64 : d_off64, side ? g->cidx : g->idx, g->scount,
+                                  &ctx->launches),
+            "validate kernel");
+      PP_CK(cudaMemcpyAsync(g->scount_host, g->scount, 8, cudaMemcpyDeviceToHost, st), "copy");
+      PP_CK(cudaStreamSynchronize(st), "sync");
+      if (g->scount_host[0] != ~0ull)
+        PP_FAIL(PP_ERR_GRAPH,
+                "pp_graph_upload: %s row %llu is malformed (offsets decrease, an id >= n, or the "
+                "row is not strictly increasing)",
+                side ? "CSC" : "CSR", (unsigned long long)g->scount_host[0]);
+    }
+  }
+
+  // narrowed offsets, isolated bitmap, heavy-chunk capacities
+  const size_t offb = g->off64 ? 8 : 4;
+  {
+    void* p = nullptr;
+    PP_CK(cudaMalloc(&p, offb * (n + 1)), "offsets");
+    g->off = p;
+    bytes += (int64_t)(offb * (n + 1));
+    if (symmetric) {
+      g->coff = g->off;
+    } else {
+      PP_CK(cudaMalloc(&p, offb * (n + 1)), "csc offsets");
+      g->coff = p;
+      bytes += (int64_t)(offb * (n + 1));
+    }
+  }
+  if ((s = dalloc(&g->isolated, g->nwords, &bytes, "isolated")) != PP_OK) return s;
+  PP_CK(cudaMemsetAsync(g->scount, 0, 2 * sizeof(unsigned long long), st), "memset");
+  PP_CK(launch_graph_prepare(g, d_off64, d_coff64, g->scount, &ctx->launches), "prepare kernels");
+  PP_CK(cudaMemcpyAsync(g->scount_host, g->scount, 16, cudaMemcpyDeviceToHost, st), "copy");
+  PP_CK(cudaStreamSynchronize(st), "sync");
+  g->hcap = (int64_t)std::max(g->scount_host[0], g->scount_host[1]);
+
+  // BFS / mxv working set
+  for (int k = 0; k < 2; ++k) {
+    if ((s = dalloc(&g->vis[k], g->nwords, &bytes, "visited")) != PP_OK) return s;
+    if ((s = dalloc(&g->L[k], (size_t)n, &bytes, "frontier list")) != PP_OK) return s;
+    if ((s = dalloc(&g->H[k], (size_t)g->hcap, &bytes, "heavy chunks")) != PP_OK) return s;
+  }
+  if ((s = dalloc(&g->ctr, kRing, &bytes, "level counters")) != PP_OK) return s;
+  g->stats_cap = (int)std::min<int64_t>(n + 1, 1 << 16);
+  if ((s = dalloc(&g->stats, (size_t)g->stats_cap, &bytes, "level stats")) != PP_OK) return s;
+  if ((s = dalloc(&g->bar, 2, &bytes, "barrier")) != PP_OK) return s;  // [bar][status]
+  g->status = reinterpret_cast<BfsStatus*>(g->bar + 1);
+  for (int k = 0; k < 4; ++k)
+    if ((s = dalloc(&g->sbits[k], g->nwords, &bytes, "scratch bitmap")) != PP_OK) return s;
+  if ((s = dalloc(&g->sblock, g->nwords / 256 + 1, &bytes, "scan blocks")) != PP_OK) return s;
+  PP_CK(cudaMemsetAsync(g->bar, 0, sizeof(GridBarrier) * 2, st), "memset");
+  PP_CK(cudaStreamSynchronize(st), "sync");
+  if (g->dtmp[0]) {
+    cudaFree(g->dtmp[0]);
+    g->dtmp[0] = nullptr;
+  }
+  g->bfs_grid = bfs_grid_size(g, false);
+  guard.g = nullptr;
+  ctx->refs += 1;
+  *out = g;
+  return PP_OK;
+}
+
+pp_status pp_graph_free(pp_graph g) {
+  if (!g) PP_FAIL(PP_ERR_ARG, "pp_graph_free: NULL graph");
+  pp_ctx ctx = g->ctx;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  free_graph(g);
+  ctx_release(ctx);
+  return PP_OK;
+}
+
+pp_status pp_graph_info(pp_graph g, int64_t* n, int64_t* nnz, int64_t* device_bytes) {
+  if (!g) PP_FAIL(PP_ERR_ARG, "pp_graph_info: NULL graph");
+  if (n) *n = g->n;
+  if (nnz) *nnz = g->nnz;
+  if (device_bytes) *device_bytes = g->device_bytes;
+  return PP_OK;
+}
+
+pp_status pp_descriptor_default(pp_descriptor* d) {
+  if (!d) PP_FAIL(PP_ERR_ARG, "pp_descriptor_default: NULL");
+  memset(d, 0, sizeof(*d));
+  d->mask = nullptr;
+  d->semiring = PP_SR_LOR_LAND;
+  d->replace = 1;
+  d->direction = PP_DIR_AUTO;
+  d->early_exit = 1;
+  d->transpose = 1;
+  d->want_nnz = 1;
+  d->switchpoint = 0.01;
+  d->prev_nnz = -1;
+  return PP_OK;
+}
+
+pp_status pp_bfs_options_default(pp_bfs_options* o) {
+  if (!o) PP_FAIL(PP_ERR_ARG, "pp_bfs_options_default: NULL");
+  memset(o, 0, sizeof(*o));
+  o->heuristic = PP_HEUR_EDGES;
+  o->mode = PP_MODE_DO;
+  o->alpha = 0;
+  o->beta = 0;
+  o->want_parents = 0;
+  o->toggles = 0;
+  return PP_OK;
+}
+
+static pp_status check_vec(const pp_vector* v, int64_t n, const char* name) {
+  if (!v) PP_FAIL(PP_ERR_ARG, "pp_mxv: %s is NULL", name);
+  if (v->n != n) PP_FAIL(PP_ERR_DIM, "pp_mxv: %s has length %lld, graph has n=%lld", name, (long long)v->n, (long long)n);
+  if (v->format != PP_VEC_LIST && v->format != PP_VEC_BITMAP)
+    PP_FAIL(PP_ERR_DIM, "pp_mxv: %s has unknown format %d", name, v->format);
+  if (!v->data && !(v->format == PP_VEC_LIST && v->nnz == 0 && v->capacity == 0))
+    PP_FAIL(PP_ERR_ARG, "pp_mxv: %s data is NULL", name);
+  if (v->format == PP_VEC_LIST && (v->nnz < 0 || v->nnz > std::max<int64_t>(v->capacity, v->nnz)))
+    PP_FAIL(PP_ERR_DIM, "pp_mxv: %s list nnz=%lld invalid", name, (long long)v->nnz);
+  return PP_OK;
+}
+
+pp_status pp_mxv(pp_graph g, pp_vector* w, const pp_descriptor* desc, const pp_vector* u) {
+  if (!g || !desc) PP_FAIL(PP_ERR_ARG, "pp_mxv: NULL graph or descriptor");
+  pp_status s;
+  if ((s = check_vec(u, g->n, "u")) != PP_OK) return s;
+  if ((s = check_vec(w, g->n, "w")) != PP_OK) return s;
+  if (desc->semiring != PP_SR_LOR_LAND)
+    PP_FAIL(PP_ERR_UNSUPPORTED, "pp_mxv: semiring %d unsupported (Boolean LOR.LAND only)", desc->semiring);
+  if (!desc->mask && desc->complement)
+    PP_FAIL(PP_ERR_ARG, "pp_mxv: structural complement without a mask");
+  if (desc->mask && (s = check_vec(desc->mask, g->n, "mask")) != PP_OK) return s;
+  if (desc->direction < PP_DIR_AUTO || desc->direction > PP_DIR_PULL)
+    PP_FAIL(PP_ERR_ARG, "pp_mxv: direction %d", desc->direction);
+  PP_CK(cudaSetDevice(g->ctx->device), "cudaSetDevice");
+  cudaStream_t st = g->ctx->stream;
+  unsigned long long* bad = g->scount + 2;
+  PP_CK(cudaMemsetAsync(bad, 0xFF, sizeof(unsigned long long), st), "memset");
+  const bool need_win = desc->accum || !desc->replace;
+
+  // Convert — AUTO picks the kernel by nnz(u)/n with hysteresis (R25)
+  int64_t unnz = u->nnz;
+  int pull;
+  if (desc->direction == PP_DIR_AUTO) {
+    if (unnz < 0) {  // bitmap of unknown count
+      PP_CK(launch_popcount(g, (const uint32_t*)u->data, g->scount), "popcount");
+      PP_CK(cudaMemcpyAsync(g->scount_host, g->scount, 8, cudaMemcpyDeviceToHost, st), "copy");
+      PP_CK(cudaStreamSynchronize(st), "sync");
+      unnz = (int64_t)g->scount_host[0];
+    }
+    const double r = (double)unnz / (double)g->n;
+    const int64_t prev = desc->prev_nnz;
+    if (u->format == PP_VEC_LIST) pull = (r > desc->switchpoint && (prev < 0 || unnz > prev)) ? 1 : 0;
+    else pull = (r < desc->switchpoint && (prev < 0 || unnz < prev)) ? 0 : 1;
+  } else {
+    pull = desc->direction == PP_DIR_PULL ? 1 : 0;
+  }
+
+  MxvPlan p;
+  memset(&p, 0, sizeof(p));
+  p.pull = pull;
+  p.transpose = desc->transpose ? 1 : 0;
+  p.complement = desc->complement ? 1 : 0;
+  p.accum = desc->accum ? 1 : 0;
+  p.replace = desc->replace ? 1 : 0;
+  p.early_exit = desc->early_exit ? 1 : 0;
+  if (pull) {
+    if (u->format == PP_VEC_BITMAP) {
+      p.u_bits = (const uint32_t*)u->data;
+    } else {
+      PP_CK(launch_list_to_bitmap(g, (const uint32_t*)u->data, u->nnz, g->sbits[1], bad), "u list->bitmap");
+      p.u_bits = g->sbits[1];
+    }
+  } else {
+    if (u->format == PP_VEC_LIST) {
+      p.u_list = (const uint32_t*)u->data;
+      p.u_nnz = u->nnz;
+    } else {
+      p.u_bits = (const uint32_t*)u->data;
+    }
+  }
+  if (desc->mask) {
+    if (desc->mask->format == PP_VEC_BITMAP) {
+      p.mask_bits = (const uint32_t*)desc->mask->data;
+    } else {
+      PP_CK(launch_list_to_bitmap(g, (const uint32_t*)desc->mask->data, desc->mask->nnz, g->sbits[2], bad),
+            "mask list->bitmap");
+      p.mask_bits = g->sbits[2];
+    }
+  }
+  if (w->format == PP_VEC_BITMAP) {
+    p.out_bits = (uint32_t*)w->data;
+    p.win_bits = (const uint32_t*)w->data;
+  } else {
+    p.out_bits = g->sbits[3];
+    if (need_win) {
+      PP_CK(launch_list_to_bitmap(g, (const uint32_t*)w->data, w->nnz, g->sbits[3], bad), "w list->bitmap");
+    }
+    p.win_bits = g->sbits[3];
+  }
+  PP_CK(launch_mxv(g, p), "mxv kernels");
+
+  if (w->format == PP_VEC_LIST) {
+    PP_CK(launch_bitmap_to_list(g, g->sbits[3], (uint32_t*)w->data, w->capacity, g->scount), "bitmap->list");
+  } else if (desc->want_nnz) {
+    PP_CK(launch_popcount(g, (const uint32_t*)w->data, g->scount), "popcount");
+  }
+  if (w->format == PP_VEC_LIST || desc->want_nnz) {
+    PP_CK(cudaMemcpyAsync(g->scount_host, g->scount, 24, cudaMemcpyDeviceToHost, st), "copy");
+    PP_CK(cudaStreamSynchronize(st), "sync");
+    if (g->scount_host[2] != ~0ull)
+      PP_FAIL(PP_ERR_RANGE, "pp_mxv: input list entry %llu holds an id >= n",
+              (unsigned long long)g->scount_host[2]);
+    w->nnz = (int64_t)g->scount_host[0];
+    if (w->format == PP_VEC_LIST && w->nnz > w->capacity)
+      PP_FAIL(PP_ERR_DIM, "pp_mxv: output list needs %lld entries, capacity %lld", (long long)w->nnz,
+              (long long)w->capacity);
+  } else {
+    w->nnz = -1;
+  }
+  return PP_OK;
+}
+
+pp_status pp_bfs(pp_graph g, int64_t source, const pp_bfs_options* opts, int32_t* depth,
+                 int32_t* parent, pp_bfs_stats* stats) {
+  if (!g || !depth) PP_FAIL(PP_ERR_ARG, "pp_bfs: NULL graph or depth");
+  if (source < 0 || source >= g->n)
+    PP_FAIL(PP_ERR_RANGE, "pp_bfs: source %lld out of range [0, %lld)", (long long)source, (long long)g->n);
+  pp_bfs_options o;
+  if (opts) o = *opts;
+  else pp_bfs_options_default(&o);
+  if (o.heuristic != PP_HEUR_EDGES && o.heuristic != PP_HEUR_PAPER_R)
+    PP_FAIL(PP_ERR_ARG, "pp_bfs: heuristic %d", o.heuristic);
+  if (o.mode < PP_MODE_DO || o.mode > PP_MODE_PULL_ONLY) PP_FAIL(PP_ERR_ARG, "pp_bfs: mode %d", o.mode);
+  if (o.toggles & ~7u) PP_FAIL(PP_ERR_ARG, "pp_bfs: unknown toggles 0x%x", o.toggles);
+  double alpha = o.alpha, beta = o.beta;
+  if (alpha <= 0) alpha = (o.heuristic == PP_HEUR_EDGES) ? 15.0 : 0.01;
+  if (beta <= 0) beta = (o.heuristic == PP_HEUR_EDGES) ? 18.0 : 0.01;
+  if (!o.want_parents) parent = nullptr;
+  PP_CK(cudaSetDevice(g->ctx->device), "cudaSetDevice");
+  cudaStream_t st = g->ctx->stream;
+
+  // Host outputs (end-to-end path): compute into device staging, copy back in the call.
+  const bool host_depth = !is_device_ptr(depth);
+  const bool host_parent = parent && !is_device_ptr(parent);
+  int32_t* d_depth = depth;
+  uint32_t* d_parent = (uint32_t*)parent;
+  pp_status s;
+  if (host_depth) {
+    if (!g->dtmp[0] && (s = dalloc(&g->dtmp[0], (size_t)(g->n + 1) / 2 + 1, &g->device_bytes, "depth staging")) != PP_OK)
+      return s;
+    d_depth = (int32_t*)g->dtmp[0];
+  }
+  if (host_parent) {
+    if (!g->dtmp[1] && (s = dalloc(&g->dtmp[1], (size_t)(g->n + 1) / 2 + 1, &g->device_bytes, "parent staging")) != PP_OK)
+      return s;
+    d_parent = (uint32_t*)g->dtmp[1];
+  }
+  PP_CK(cudaMemsetAsync(g->bar, 0, sizeof(GridBarrier) + sizeof(BfsStatus), st), "memset control");
+  const int max_levels = (int)std::min<int64_t>(g->n + 1, 0x7FFFFFFF);
+  PP_CK(launch_bfs(g, (uint32_t)source, o.mode, o.heuristic, alpha, beta, o.toggles, d_depth, d_parent,
+                   max_levels),
+        "bfs kernel launch");
+  if (host_depth)
+    PP_CK(cudaMemcpyAsync(depth, d_depth, sizeof(int32_t) * g->n, cudaMemcpyDeviceToHost, st), "copy depth");
+  if (host_parent)
+    PP_CK(cudaMemcpyAsync(parent, d_parent, sizeof(int32_t) * g->n, cudaMemcpyDeviceToHost, st), "copy parent");
+  if (stats || host_depth || host_parent) {
+    PP_CK(cudaMemcpyAsync(g->status_host, g->status, sizeof(BfsStatus), cudaMemcpyDeviceToHost, st),
+          "copy status");
+    PP_CK(cudaStreamSynchronize(st), "bfs sync");
+    if (g->status_host->error)
+      PP_FAIL((pp_status)g->status_host->error, "pp_bfs: device watchdog fired (grid barrier wait > 4 s)");
+  }
+  if (stats) {
+    stats->levels = g->status_host->levels;
+    stats->reached = g->status_host->reached;
+    const int m = std::min(std::min(stats->capacity, g->status_host->levels), g->stats_cap);
+    if (m > 0) {
+      LevelStat* hs = new LevelStat[m];
+      cudaError_t e = cudaMemcpy(hs, g->stats, sizeof(LevelStat) * m, cudaMemcpyDeviceToHost);
+      if (e != cudaSuccess) {
+        delete[] hs;
+        return cuda_fail(e, "copy stats");
+      }
+      for (int k = 0; k < m; ++k) {
+        if (stats->dir) stats->dir[k] = (int8_t)hs[k].dir;
+        if (stats->c) stats->c[k] = hs[k].c;
+        if (stats->m_f) stats->m_f[k] = hs[k].m_f;
+        if (stats->m_u) stats->m_u[k] = hs[k].m_u;
+      }
+      delete[] hs;
+    }
+  }
+  return PP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,92 @@
+// graph.cu — graph residency: offset narrowing, the isolated /
+// padding bitmap (vertices no traversal can touch), heavy-chunk capacity, validation.
+#include "pp_device.cuh"
+
+namespace pp {
+
+template <typename Off>
+__global__ void k_off_narrow(const int64_t* __restrict__ in, Off* __restrict__ out, int64_t m) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (Off)in[i];
+}
+
+// bit v of word w: 1 when v >= n (padding) or v has neither in- nor out-edges.
+__global__ void k_isolated(const int64_t* __restrict__ off, const int64_t* __restrict__ coff,
+                           int64_t n, uint32_t nwords, uint32_t* __restrict__ iso) {
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
+       w += gridDim.x * blockDim.x) {
+    uint32_t bits = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int64_t v = (int64_t)w * 32 + b;
+      bool isolated = true;
+      if (v < n) isolated = (off[v + 1] == off[v]) && (coff[v + 1] == coff[v]);
+      bits |= (isolated ? 1u : 0u) << b;
+    }
+    iso[w] = bits;
+  }
+}
+
+// Heavy-chunk capacity: sum over rows with degree >= kHeavy of ceil(deg / kChunk).
+__global__ void k_hcap(const int64_t* __restrict__ off, int64_t n, unsigned long long* out) {
+  unsigned long long c = 0;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = off[v + 1] - off[v];
+    if (d >= (int64_t)kHeavy) c += (unsigned long long)((d + kChunk - 1) / kChunk);
+  }
+  c = warp_sum(c);
+  if (lane_id() == 0 && c) atomicAdd(out, c);
+}
+
+// First offending row (or n+1 if none): non-monotone offsets, id >= n, unsorted / duplicate.
+__global__ void k_validate(const int64_t* __restrict__ off, const uint32_t* __restrict__ idx,
+                           int64_t n, unsigned long long* bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = off[i], e = off[i + 1];
+    bool ok = b <= e;
+    for (int64_t p = b; ok && p < e; ++p) {
+      const uint32_t x = idx[p];
+      if ((int64_t)x >= n) ok = false;
+      if (p > b && idx[p - 1] >= x) ok = false;
+    }
+    if (!ok) atomicMin(bad, (unsigned long long)i);
+  }
+}
+
+cudaError_t launch_graph_validate(pp_graph g, const int64_t* d_off64, const uint32_t* d_idx,
+                                  unsigned long long* d_bad, uint64_t* launches) {
+  const int blocks = g->ctx->num_sms * 8;
+  *launches += 1;
+  k_validate<<<blocks, kBlock, 0, g->ctx->stream>>>(d_off64, d_idx, g->n, d_bad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_graph_prepare(pp_graph g, const int64_t* d_off64, const int64_t* d_coff64,
+                                 unsigned long long* d_scratch, uint64_t* launches) {
+  cudaStream_t st = g->ctx->stream;
+  const int blocks = g->ctx->num_sms * 8;
+  if (g->off64) {
+    *launches += 1;
+    k_off_narrow<uint64_t><<<blocks, kBlock, 0, st>>>(d_off64, (uint64_t*)g->off, g->n + 1);
+    if (!g->symmetric) {
+      *launches += 1;
+      k_off_narrow<uint64_t><<<blocks, kBlock, 0, st>>>(d_coff64, (uint64_t*)g->coff, g->n + 1);
+    }
+  } else {
+    *launches += 1;
+    k_off_narrow<uint32_t><<<blocks, kBlock, 0, st>>>(d_off64, (uint32_t*)g->off, g->n + 1);
+    if (!g->symmetric) {
+      *launches += 1;
+      k_off_narrow<uint32_t><<<blocks, kBlock, 0, st>>>(d_coff64, (uint32_t*)g->coff, g->n + 1);
+    }
+  }
+  *launches += 3;
+  k_isolated<<<blocks, kBlock, 0, st>>>(d_off64, d_coff64, g->n, g->nwords, g->isolated);
+  k_hcap<<<blocks, kBlock, 0, st>>>(d_off64, g->n, d_scratch + 0);
+  k_hcap<<<blocks, kBlock, 0, st>>>(d_coff64, g->n, d_scratch + 1);
+  return cudaGetLastError();
+}
+
+}  // namespace pp

@@ -1,0 +1,122 @@
+// pp_internal.h — host-side internals of libpushpull (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "pushpull.h"
+
+namespace pp {
+
+// ---- tunables ---------------------------------------------------------------
+constexpr int kBlock = 256;        // threads per CTA of every kernel
+constexpr int kWarps = kBlock / 32;
+constexpr unsigned kHeavy = 256;   // out-degree >= kHeavy: expanded as kChunk-edge chunks
+constexpr unsigned kChunk = 256;   // edges per heavy chunk (push load balance)
+constexpr int kRing = 4;           // level-counter ring
+
+// Per-level counters, written with atomics during a level, read after the grid barrier.
+struct LevelCtr {
+  unsigned long long c;      // vertices discovered by the level
+  unsigned long long m_f;    // sum of their out-degrees (Eq. 1)
+  unsigned long long m_fin;  // sum of their in-degrees (m_u update, directed graphs)
+  unsigned int nL, nH;       // next frontier: light-list length, heavy-chunk count
+  unsigned int work, work2;  // dynamic work counters (phase, convert phase)
+  unsigned int pad[6];
+};
+static_assert(sizeof(LevelCtr) == 64, "LevelCtr layout");
+
+struct LevelStat {
+  int dir;
+  int pad;
+  long long c, m_f, m_u;
+};
+
+struct GridBarrier {
+  unsigned int count;
+  unsigned int pad0[31];
+  unsigned int gen;
+  unsigned int pad1[31];
+};
+
+// Device-side BFS status words.
+struct BfsStatus {
+  int error;   // 0 or pp_status
+  int levels;  // levels executed
+  long long reached;
+};
+
+}  // namespace pp
+
+struct pp_ctx_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 0;
+  uint64_t launches = 0;
+  int refs = 1;  // the caller's handle + one per live graph
+};
+
+struct pp_graph_s {
+  pp_ctx ctx = nullptr;
+  int64_t n = 0, nnz = 0;
+  bool symmetric = false;
+  bool off64 = false;
+  uint32_t nwords = 0;  // bitmap words, padded to a multiple of 32 (one warp-chunk)
+  void* off = nullptr;  // uint32 or uint64 [n+1]  (CSR, out-neighbours)
+  uint32_t* idx = nullptr;
+  void* coff = nullptr;  // CSC (in-neighbours); aliases off when symmetric
+  uint32_t* cidx = nullptr;
+  uint32_t* isolated = nullptr;  // nwords: bit = no in- and no out-edges, or padding
+  // BFS working set
+  uint32_t* vis[2] = {nullptr, nullptr};
+  uint32_t* L[2] = {nullptr, nullptr};
+  uint2* H[2] = {nullptr, nullptr};
+  int64_t hcap = 0;
+  pp::LevelCtr* ctr = nullptr;
+  pp::LevelStat* stats = nullptr;
+  int stats_cap = 0;
+  pp::GridBarrier* bar = nullptr;
+  pp::BfsStatus* status = nullptr;
+  pp::BfsStatus* status_host = nullptr;  // pinned
+  // mxv scratch
+  uint32_t* sbits[4] = {nullptr, nullptr, nullptr, nullptr};  // t, u, mask, w (bitmaps)
+  uint32_t* sblock = nullptr;        // per-block counts for bitmap->list
+  unsigned long long* scount = nullptr;  // device counters (mxv)
+  unsigned long long* scount_host = nullptr;
+  int64_t* dtmp[2] = {nullptr, nullptr};  // upload staging / host-output staging
+  int bfs_grid = 0;
+  int64_t device_bytes = 0;
+};
+
+namespace pp {
+void set_error(const char* fmt, ...);
+pp_status cuda_fail(cudaError_t e, const char* what);
+
+// launchers (bfs.cu / mxv.cu / graph.cu); each returns cudaSuccess or the launch error
+cudaError_t launch_graph_prepare(pp_graph g, const int64_t* d_off64, const int64_t* d_coff64,
+                                 unsigned long long* d_scratch, uint64_t* launches);
+cudaError_t launch_graph_validate(pp_graph g, const int64_t* d_off64, const uint32_t* d_idx,
+                                  unsigned long long* d_bad, uint64_t* launches);
+int bfs_grid_size(pp_graph g, bool parents);
+cudaError_t launch_bfs(pp_graph g, uint32_t source, int mode, int rule, double alpha, double beta,
+                       uint32_t toggles, int32_t* depth, uint32_t* parent, int max_levels);
+
+struct MxvPlan {
+  int pull;              // 1 = row-based (Alg. 2), 0 = column-based (Alg. 3)
+  int transpose;         // operator A^T (1) or A (0)
+  const uint32_t* u_bits;  // u as bitmap (pull) or nullptr
+  const uint32_t* u_list;  // u as list (push) or nullptr
+  int64_t u_nnz;
+  const uint32_t* mask_bits;  // nullptr = no mask
+  int complement, accum, replace, early_exit;
+  const uint32_t* win_bits;  // w_in as bitmap (may alias out_bits)
+  uint32_t* out_bits;        // result bitmap
+};
+cudaError_t launch_list_to_bitmap(pp_graph g, const uint32_t* list, int64_t m, uint32_t* bits,
+                                  unsigned long long* d_bad);
+cudaError_t launch_mxv(pp_graph g, const MxvPlan& p);
+cudaError_t launch_popcount(pp_graph g, const uint32_t* bits, unsigned long long* d_out);
+cudaError_t launch_bitmap_to_list(pp_graph g, const uint32_t* bits, uint32_t* list,
+                                  int64_t capacity, unsigned long long* d_count);
+}  // namespace pp
