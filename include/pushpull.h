@@ -166,9 +166,11 @@ pp_status pp_bfs_options_default(pp_bfs_options* o);
 
 /* Per-level record of level k (1-based) at index k-1: dir (0 push, 1 pull),
  * c = |frontier discovered by level k|, m_f = sum of its out-degrees (Eq. 1),
- * m_u = sum of in-degrees still unvisited after level k.  Arrays are
- * caller-owned host memory of `capacity` entries (any may be NULL).  levels =
- * number of levels executed (= max depth); reached = #vertices with depth > 0. */
+ * m_u = sum of in-degrees still unvisited after level k, ns = device time of the
+ * level (GPU %globaltimer between grid barriers, incl. a following convert).
+ * Arrays are caller-owned host memory of `capacity` entries (any may be NULL).
+ * levels = number of levels executed (= max depth); reached = #vertices with
+ * depth > 0; init_ns = device time of the initialisation phase. */
 typedef struct {
   int32_t levels;
   int64_t reached;
@@ -177,6 +179,8 @@ typedef struct {
   int64_t* c;
   int64_t* m_f;
   int64_t* m_u;
+  int64_t* ns;
+  int64_t init_ns;
 } pp_bfs_stats;
 
 pp_status pp_bfs(pp_graph g, int64_t source, const pp_bfs_options* opts, int32_t* depth,

@@ -69,7 +69,8 @@ class pp_bfs_stats(ctypes.Structure):
     _fields_ = [("levels", ctypes.c_int32), ("reached", ctypes.c_int64),
                 ("capacity", ctypes.c_int32), ("dir", ctypes.POINTER(ctypes.c_int8)),
                 ("c", ctypes.POINTER(ctypes.c_int64)), ("m_f", ctypes.POINTER(ctypes.c_int64)),
-                ("m_u", ctypes.POINTER(ctypes.c_int64))]
+                ("m_u", ctypes.POINTER(ctypes.c_int64)), ("ns", ctypes.POINTER(ctypes.c_int64)),
+                ("init_ns", ctypes.c_int64)]
 
 
 _vp, _i64, _u32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32
@@ -264,18 +265,21 @@ def bfs(graph: Graph, source: int, depth, parent=None, heuristic=PP_HEUR_EDGES, 
     arrays = None
     if stats_capacity > 0:
         arrays = dict(dir=np.zeros(stats_capacity, np.int8), c=np.zeros(stats_capacity, np.int64),
-                      m_f=np.zeros(stats_capacity, np.int64), m_u=np.zeros(stats_capacity, np.int64))
+                      m_f=np.zeros(stats_capacity, np.int64), m_u=np.zeros(stats_capacity, np.int64),
+                      ns=np.zeros(stats_capacity, np.int64))
         st = pp_bfs_stats(0, 0, stats_capacity,
                           arrays["dir"].ctypes.data_as(ctypes.POINTER(ctypes.c_int8)),
                           arrays["c"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                           arrays["m_f"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
-                          arrays["m_u"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)))
+                          arrays["m_u"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                          arrays["ns"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), 0)
     pp_bfs(graph.handle, source, o, _ptr(depth), _ptr(parent), st)
     if st is None:
         return None
     L = min(st.levels, stats_capacity)
     return dict(levels=st.levels, reached=st.reached, dir=arrays["dir"][:L], c=arrays["c"][:L],
-                m_f=arrays["m_f"][:L], m_u=arrays["m_u"][:L])
+                m_f=arrays["m_f"][:L], m_u=arrays["m_u"][:L], ns=arrays["ns"][:L],
+                init_ns=st.init_ns)
 
 
 def make_vector(fmt: int, n: int, data=None, nnz: int = -1, capacity: int = 0) -> pp_vector:

@@ -99,15 +99,37 @@ struct Acc {
   unsigned long long c, mf, mfin;
 };
 
-__device__ __forceinline__ void flush_acc(Acc& acc, LevelCtr* out) {
+// CTA-level reduction, then one set of atomics per CTA (single-address L2 atomics
+// serialise; per-warp flushing cost ~3 x #warps atomics per level).
+__device__ __forceinline__ void flush_acc(Acc& acc, LevelCtr* out,
+                                          unsigned long long (*red)[3]) {
+  const unsigned warp = threadIdx.x >> 5;
   unsigned long long c = warp_sum(acc.c), mf = warp_sum(acc.mf), mfin = warp_sum(acc.mfin);
-  if (lane_id() == 0 && c) {
-    atomicAdd(&out->c, c);
-    atomicAdd(&out->m_f, mf);
-    atomicAdd(&out->m_fin, mfin);
+  if (lane_id() == 0) {
+    red[warp][0] = c;
+    red[warp][1] = mf;
+    red[warp][2] = mfin;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long tc = 0, tm = 0, ti = 0;
+    for (int k = 0; k < kBfsWarps; ++k) {
+      tc += red[k][0];
+      tm += red[k][1];
+      ti += red[k][2];
+    }
+    if (tc) {
+      atomicAdd(&out->c, tc);
+      atomicAdd(&out->m_f, tm);
+      atomicAdd(&out->m_fin, ti);
+    }
   }
   acc.c = acc.mf = acc.mfin = 0;
 }
+
+// Warp work assignment: static round-robin over all warps of the grid (no atomics).
+__device__ __forceinline__ unsigned gwarp() { return blockIdx.x * kBfsWarps + (threadIdx.x >> 5); }
+__device__ __forceinline__ unsigned nwarps() { return gridDim.x * kBfsWarps; }
 
 // Append newly discovered vertex v (valid lanes) to the next frontier: light list if
 // 0 < deg < kHeavy, else ceil(deg/kChunk) heavy chunks.  Warp-collective.
@@ -126,229 +148,368 @@ __device__ __forceinline__ void append_frontier(bool valid, uint32_t v, Off deg,
   }
   unsigned hm = __ballot_sync(kFull, heavy);
   if (hm) {
-    unsigned nch = heavy ? (unsigned)((deg + (Off)kChunk - 1) / (Off)kChunk) : 0u;
-    unsigned incl = warp_incl_scan(nch);
-    unsigned tot = __shfl_sync(kFull, incl, 31), base = 0;
+    const unsigned nch = heavy ? (unsigned)((deg + (Off)kChunk - 1) / (Off)kChunk) : 0u;
+    const unsigned incl = warp_incl_scan(nch);
+    const unsigned excl = incl - nch;
+    const unsigned tot = __shfl_sync(kFull, incl, 31);
+    unsigned base = 0;
     if (lane == 0) base = atomicAdd(&out->nH, tot);
     base = __shfl_sync(kFull, base, 0);
-    for (unsigned k = 0; k < nch; ++k) Hout[base + incl - nch + k] = make_uint2(v, k);
-  }
-}
-
-// Push visit of edge (u, w): the mask test (w unvisited) precedes the OR-merge
-// (atomicOr).  Parents: atomicMin over every edge whose head was unvisited when the
-// level started: bit clear in a post-barrier read, or depth still 0
-// or newdepth (i.e. discovered during this level).
-template <bool PARENTS>
-__device__ __forceinline__ bool push_visit(uint32_t* vis, int32_t* depth, uint32_t* parent,
-                                           uint32_t u, uint32_t w, int newdepth) {
-  const uint32_t wi = w >> 5, bit = 1u << (w & 31u);
-  const uint32_t cur = vis[wi];
-  bool disc = false;
-  if (!(cur & bit)) {
-    uint32_t old = atomicOr(&vis[wi], bit);
-    disc = !(old & bit);
-  }
-  if (disc) depth[w] = newdepth;
-  if (PARENTS) {
-    bool fresh = disc || !(cur & bit);
-    if (!fresh) {
-      int dw = ld_relaxed_s32(&depth[w]);
-      fresh = (dw == 0 || dw == newdepth);
+    for (unsigned c0 = 0; c0 < tot; c0 += 32) {  // 32 descriptors per step
+      const unsigned c = c0 + lane;
+      const unsigned j = warp_owner(incl, c);
+      const uint32_t vj = __shfl_sync(kFull, v, j);
+      const unsigned xj = __shfl_sync(kFull, excl, j);
+      if (c < tot) Hout[base + c] = make_uint2(vj, c - xj);
     }
-    if (fresh) atomicMin(&parent[w], u);
   }
-  return disc;
 }
 
+constexpr int kU = 4;  // edges (push) in flight per lane
+
+// The same for kU candidates per lane, with one atomic per list per warp.
+template <typename Off>
+__device__ __forceinline__ void append_frontier4(const bool (&disc)[kU], const uint32_t (&w)[kU],
+                                                 const Off (&deg)[kU], uint32_t* Lout, uint2* Hout,
+                                                 LevelCtr* out) {
+  const unsigned lane = lane_id();
+  unsigned lm[kU], ltot = 0, hsum = 0;
+#pragma unroll
+  for (int t = 0; t < kU; ++t) {
+    const bool light = disc[t] && deg[t] > 0 && deg[t] < (Off)kHeavy;
+    lm[t] = __ballot_sync(kFull, light);
+    ltot += __popc(lm[t]);
+    if (disc[t] && deg[t] >= (Off)kHeavy) hsum += (unsigned)((deg[t] + (Off)kChunk - 1) / (Off)kChunk);
+  }
+  if (ltot) {
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(&out->nL, ltot);
+    base = __shfl_sync(kFull, base, 0);
+#pragma unroll
+    for (int t = 0; t < kU; ++t) {
+      if ((lm[t] >> lane) & 1u) Lout[base + __popc(lm[t] & lanemask_lt())] = w[t];
+      base += __popc(lm[t]);
+    }
+  }
+  if (__any_sync(kFull, hsum != 0)) {
+    // heavy chunks written warp-cooperatively: 32 consecutive descriptors per step
+    const unsigned incl = warp_incl_scan(hsum);
+    const unsigned excl = incl - hsum;
+    const unsigned tot = __shfl_sync(kFull, incl, 31);
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(&out->nH, tot);
+    base = __shfl_sync(kFull, base, 0);
+    unsigned nch[kU];
+#pragma unroll
+    for (int t = 0; t < kU; ++t)
+      nch[t] = (disc[t] && deg[t] >= (Off)kHeavy) ? (unsigned)((deg[t] + (Off)kChunk - 1) / (Off)kChunk) : 0u;
+    for (unsigned c0 = 0; c0 < tot; c0 += 32) {
+      const unsigned c = c0 + lane;
+      const unsigned j = warp_owner(incl, c);
+      unsigned r = c - __shfl_sync(kFull, excl, j);
+      uint32_t vv = 0;
+      bool done = false;
+#pragma unroll
+      for (int t = 0; t < kU; ++t) {
+        const unsigned nt = __shfl_sync(kFull, nch[t], j);
+        const uint32_t wt = __shfl_sync(kFull, w[t], j);
+        if (!done && r < nt) {
+          vv = wt;
+          done = true;
+        } else if (!done) {
+          r -= nt;
+        }
+      }
+      if (c < tot) Hout[base + c] = make_uint2(vv, r);
+    }
+  }
+}
+
+// Push visit of kU edges (u, w) per lane, all loads issued before use.  The mask test
+// (w unvisited) precedes the OR-merge (atomicOr on the visited bitmap).  Parents:
+// atomicMin over every edge whose head was unvisited when the level started
+// (SURVEY.md G14): bit clear in a post-barrier read, or depth 0 / newdepth.
 template <typename Off, bool PARENTS>
-__device__ __forceinline__ void push_edge_batch(const BfsArgs<Off>& a, bool valid, uint32_t u,
-                                                uint32_t w, uint32_t* vis, int newdepth,
-                                                uint32_t* Lout, uint2* Hout, LevelCtr* out,
-                                                Acc& acc) {
-  bool disc = valid && push_visit<PARENTS>(vis, a.depth, a.parent, u, w, newdepth);
-  if (__ballot_sync(kFull, disc) == 0) return;
-  Off deg = 0, degin = 0;
-  if (disc) {
-    Off b = a.off[w], e = a.off[w + 1];
-    deg = e - b;
-    degin = a.symmetric ? deg : (Off)(a.coff[w + 1] - a.coff[w]);
-    acc.c += 1;
-    acc.mf += (unsigned long long)deg;
-    acc.mfin += (unsigned long long)degin;
+__device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&valid)[kU],
+                                            const uint32_t (&u)[kU], const uint32_t (&w)[kU],
+                                            uint32_t* vis, int newdepth, uint32_t* Lout,
+                                            uint2* Hout, LevelCtr* out, Acc& acc) {
+  uint32_t cur[kU];
+  bool disc[kU];
+#pragma unroll
+  for (int t = 0; t < kU; ++t) cur[t] = valid[t] ? vis[w[t] >> 5] : 0xFFFFFFFFu;
+#pragma unroll
+  for (int t = 0; t < kU; ++t) {
+    const uint32_t bit = 1u << (w[t] & 31u);
+    disc[t] = false;
+    if (!(cur[t] & bit)) {
+      const uint32_t old = atomicOr(&vis[w[t] >> 5], bit);
+      disc[t] = !(old & bit);
+    }
   }
-  append_frontier<Off>(disc, w, deg, Lout, Hout, out);
+#pragma unroll
+  for (int t = 0; t < kU; ++t)
+    if (disc[t]) a.depth[w[t]] = newdepth;
+  if (PARENTS) {
+#pragma unroll
+    for (int t = 0; t < kU; ++t) {
+      if (!valid[t]) continue;
+      bool fresh = disc[t] || !((cur[t] >> (w[t] & 31u)) & 1u);
+      if (!fresh) {
+        const int dw = ld_relaxed_s32(&a.depth[w[t]]);
+        fresh = (dw == 0 || dw == newdepth);
+      }
+      if (fresh) atomicMin(&a.parent[w[t]], u[t]);
+    }
+  }
+  if (!__any_sync(kFull, disc[0] || disc[1] || disc[2] || disc[3])) return;
+  Off deg[kU];
+#pragma unroll
+  for (int t = 0; t < kU; ++t) {
+    deg[t] = 0;
+    if (disc[t]) {
+      deg[t] = a.off[w[t] + 1] - a.off[w[t]];
+      const Off degin = a.symmetric ? deg[t] : (Off)(a.coff[w[t] + 1] - a.coff[w[t]]);
+      acc.c += 1;
+      acc.mf += (unsigned long long)deg[t];
+      acc.mfin += (unsigned long long)degin;
+    }
+  }
+  append_frontier4<Off>(disc, w, deg, Lout, Hout, out);
 }
 
-// Column-based masked mxv over the frontier (light list + heavy chunks).
+// Column-based masked mxv over the frontier (light list + heavy chunks).  Heavy chunk =
+// kChunk = 128 consecutive edges = one warp iteration with 4 coalesced loads per lane.
+// Light round = R frontier vertices (R = 32, or fewer when the frontier is too small to
+// occupy every warp), their edges balanced over lanes by a warp scan of degrees.
 template <typename Off, bool PARENTS>
 __device__ void push_phase(const BfsArgs<Off>& a, const uint32_t* Lin, unsigned nL,
                            const uint2* Hin, unsigned nH, uint32_t* Lout, uint2* Hout,
                            LevelCtr* out, uint32_t* vis, int newdepth, Acc& acc) {
   const unsigned lane = lane_id();
-  const unsigned nRounds = (nL + 31u) / 32u;
+  const unsigned NW = nwarps();
+  unsigned R = 32;
+  while (R > 1 && (nL + R / 2 - 1) / (R / 2) <= NW) R >>= 1;
+  const unsigned nRounds = (nL + R - 1) / R;
   const unsigned total = nH + nRounds;
-  for (;;) {
-    const unsigned item = warp_grab(&out->work);
-    if (item >= total) break;
+  for (unsigned item = gwarp(); item < total; item += NW) {
+    bool valid[kU];
+    uint32_t u[kU], w[kU];
     if (item < nH) {
-      // heavy chunk: kChunk consecutive edges of one vertex, fully coalesced
       const uint2 h = Hin[item];
-      const uint32_t u = h.x;
-      const Off rb = a.off[u], re = a.off[u + 1];
+      const Off rb = a.off[h.x], re = a.off[h.x + 1];
       const Off b = rb + (Off)h.y * (Off)kChunk;
       const Off e = min(re, b + (Off)kChunk);
-      for (Off base = b; base < e; base += 32) {
-        const Off p = base + lane;
-        const bool valid = p < e;
-        const uint32_t w = valid ? a.idx[p] : 0u;
-        push_edge_batch<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc);
+#pragma unroll
+      for (int t = 0; t < kU; ++t) {
+        const Off p = b + (Off)(t * 32) + lane;
+        valid[t] = p < e;
+        u[t] = h.x;
+        w[t] = valid[t] ? a.idx[p] : 0u;
       }
+      push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc);
     } else {
-      // light round: 32 frontier vertices, edges balanced across lanes by a warp scan
-      const unsigned i = (item - nH) * 32u + lane;
-      uint32_t u = 0;
+      const unsigned i = (item - nH) * R + lane;
+      uint32_t v = 0;
       Off b = 0;
       unsigned deg = 0;
-      if (i < nL) {
-        u = Lin[i];
-        b = a.off[u];
-        deg = (unsigned)(a.off[u + 1] - b);
+      if (lane < R && i < nL) {
+        v = Lin[i];
+        b = a.off[v];
+        deg = (unsigned)(a.off[v + 1] - b);
       }
       const unsigned incl = warp_incl_scan(deg);
       const unsigned excl = incl - deg;
       const unsigned tot = __shfl_sync(kFull, incl, 31);
-      for (unsigned base = 0; base < tot; base += 32) {
-        const unsigned e = base + lane;
-        const unsigned j = warp_owner(incl, e);
-        const uint32_t uj = __shfl_sync(kFull, u, j);
-        const Off bj = __shfl_sync(kFull, b, j);
-        const unsigned xj = __shfl_sync(kFull, excl, j);
-        const bool valid = e < tot;
-        const uint32_t w = valid ? a.idx[bj + (Off)(e - xj)] : 0u;
-        push_edge_batch<Off, PARENTS>(a, valid, uj, w, vis, newdepth, Lout, Hout, out, acc);
+      for (unsigned base = 0; base < tot; base += 32 * kU) {
+#pragma unroll
+        for (int t = 0; t < kU; ++t) {
+          const unsigned e = base + t * 32 + lane;
+          const unsigned j = warp_owner(incl, e);
+          u[t] = __shfl_sync(kFull, v, j);
+          const Off bj = __shfl_sync(kFull, b, j);
+          const unsigned xj = __shfl_sync(kFull, excl, j);
+          valid[t] = e < tot;
+          w[t] = valid[t] ? a.idx[bj + (Off)(e - xj)] : 0u;
+        }
+        push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc);
       }
     }
   }
 }
 
-constexpr int kLaneProbe = 8;  // indices per lane-probe round (one 32 B sector)
-constexpr int kLaneRounds = 2;
+constexpr unsigned kPW = 8;   // bitmap words per pull item (256 rows)
+constexpr int kC = 2;         // candidates in flight per lane
+constexpr int kLaneMax = 32;  // rows with <= this many ids left finish lane-parallel
+
+__device__ __forceinline__ uint4 ld_nc_u4(const uint32_t* p) {
+  return __ldg(reinterpret_cast<const uint4*>(p));
+}
 
 // Row-based masked mxv with early exit over the complement of the visited snapshot.
-// Warp item = 32 bitmap words (1024 rows); candidates are enumerated warp-balanced.
+// Warp item = kPW bitmap words; candidates (zero bits) are enumerated warp-balanced and
+// processed kC per lane at a time so their loads overlap.  First probe = the aligned
+// 8-id block (one 32 B sector) holding the row's first id, two ld.global.nc.v4, all
+// ids tested together; the first hit in sorted order is the min-id parent (R14).  Rows
+// with <= kLaneMax ids left continue lane-parallel (8 ids per step); longer rows are
+// finished warp-cooperatively, 128 ids per step with a ballot early exit.  Found bits are
+// OR-ed in shared memory; the owning lane writes v' = v | found (no global atomics).
 template <typename Off, bool PARENTS>
 __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
                            uint32_t* __restrict__ vout, LevelCtr* out, int d, Acc& acc,
                            uint32_t* sfound) {
   const unsigned lane = lane_id();
-  const unsigned nchunks = a.nwords / 32u;
+  const unsigned nitems = a.nwords / kPW;
   const bool early_exit = !(a.toggles & PP_OPT_NO_EARLYEXIT);
   const bool no_mask = (a.toggles & PP_OPT_NO_MASKING) != 0;
   const bool no_reuse = (a.toggles & PP_OPT_NO_REUSE) != 0;
-  for (;;) {
-    const unsigned item = warp_grab(&out->work);
-    if (item >= nchunks) break;
-    const unsigned wbase = item * 32u;
-    const uint32_t vw = vin[wbase + lane];
+  auto hit = [&](uint32_t x) -> bool {
+    return no_reuse ? (a.depth[x] == d) : bit_test(vin, x);
+  };
+  // test ids [q0, q0+8) clipped to [rb, e); record the first hit
+  auto probe8 = [&](Off q0, Off rb, Off e, bool& found, uint32_t& par) {
+    const uint4 lo = ld_nc_u4(a.cidx + q0), hi = ld_nc_u4(a.cidx + q0 + 4);
+    const uint32_t x[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    bool h[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      const Off q = q0 + (Off)t;
+      h[t] = q >= rb && q < e && hit(x[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      if (h[t] && !found) {
+        found = true;
+        par = x[t];
+      }
+    }
+  };
+  for (unsigned item = gwarp(); item < nitems; item += nwarps()) {
+    const unsigned wbase = item * kPW;
+    const bool own = lane < kPW;
+    const uint32_t vw = own ? vin[wbase + lane] : 0xFFFFFFFFu;
     const uint32_t unvisited = ~vw;
     // Masking (Opt. 2): only rows with !v(i) are computed.  Without it every
     // non-isolated row is computed and the result filtered afterwards.
-    const uint32_t cand = no_mask ? ~a.isolated[wbase + lane] : unvisited;
+    const uint32_t cand = no_mask ? (own ? ~a.isolated[wbase + lane] : 0u) : unvisited;
     sfound[lane] = 0u;
     __syncwarp();
     const unsigned cnt = __popc(cand);
     const unsigned incl = warp_incl_scan(cnt);
     const unsigned excl = incl - cnt;
     const unsigned tot = __shfl_sync(kFull, incl, 31);
-    for (unsigned base = 0; base < tot; base += 32) {
-      const unsigned k = base + lane;
-      const bool valid = k < tot;
-      const unsigned j = warp_owner(incl, k);
-      const uint32_t mj = __shfl_sync(kFull, cand, j);
-      const unsigned xj = __shfl_sync(kFull, excl, j);
-      const uint32_t uj = __shfl_sync(kFull, unvisited, j);
-      const unsigned bitpos = valid ? __fns(mj, 0, (int)(k - xj) + 1) : 0u;
-      const uint32_t i = (wbase + j) * 32u + bitpos;
-      Off p = 0, e = 0, rb = 0;
-      bool found = false;
-      uint32_t par = 0;
-      if (valid) {
-        rb = p = a.coff[i];
-        e = a.coff[i + 1];
-        // Lane probes: up to kLaneRounds sector-aligned groups of indices, loaded
-        // together, tested together; the first hit in sorted order is the parent.
-        for (int r = 0; r < kLaneRounds && p < e && !(found && early_exit); ++r) {
-          const Off lim = min(e, (p | (Off)(kLaneProbe - 1)) + 1);
-          uint32_t x[kLaneProbe];
+    for (unsigned base = 0; base < tot; base += 32 * kC) {
+      bool valid[kC], found[kC];
+      unsigned jj[kC], bitpos[kC];
+      uint32_t i[kC], uj[kC], par[kC];
+      Off rb[kC], e[kC], p[kC];
 #pragma unroll
-          for (int t = 0; t < kLaneProbe; ++t) x[t] = (p + t < lim) ? a.cidx[p + t] : 0u;
+      for (int t = 0; t < kC; ++t) {
+        const unsigned k = base + t * 32 + lane;
+        valid[t] = k < tot;
+        jj[t] = warp_owner(incl, k);
+        const uint32_t mj = __shfl_sync(kFull, cand, jj[t]);
+        const unsigned xj = __shfl_sync(kFull, excl, jj[t]);
+        uj[t] = __shfl_sync(kFull, unvisited, jj[t]);
+        bitpos[t] = valid[t] ? __fns(mj, 0, (int)(k - xj) + 1) : 0u;
+        i[t] = (wbase + jj[t]) * 32u + bitpos[t];
+        found[t] = false;
+        par[t] = 0;
+        rb[t] = e[t] = p[t] = 0;
+      }
 #pragma unroll
-          for (int t = 0; t < kLaneProbe; ++t) {
-            if (p + t < lim) {
-              const bool hit = no_reuse ? (a.depth[x[t]] == d) : bit_test(vin, x[t]);
-              if (hit && !found) {
-                found = true;
-                par = x[t];
+      for (int t = 0; t < kC; ++t) {
+        if (valid[t]) {
+          rb[t] = a.coff[i[t]];
+          e[t] = a.coff[i[t] + 1];
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < kC; ++t) {
+        if (valid[t] && rb[t] < e[t]) {
+          const Off q0 = rb[t] & ~(Off)7;
+          probe8(q0, rb[t], e[t], found[t], par[t]);
+          p[t] = q0 + 8;
+        } else {
+          p[t] = e[t];
+        }
+      }
+      // lane-parallel continuation of short rows
+      while (true) {
+        bool act[kC], any = false;
+#pragma unroll
+        for (int t = 0; t < kC; ++t) {
+          act[t] = valid[t] && p[t] < e[t] && !(found[t] && early_exit) &&
+                   (e[t] - p[t]) <= (Off)kLaneMax;
+          any = any || act[t];
+        }
+        if (!__any_sync(kFull, any)) break;
+#pragma unroll
+        for (int t = 0; t < kC; ++t) {
+          if (act[t]) {
+            probe8(p[t], rb[t], e[t], found[t], par[t]);
+            p[t] += 8;
+          }
+        }
+      }
+      // warp-cooperative continuation for long rows still unresolved
+#pragma unroll
+      for (int t = 0; t < kC; ++t) {
+        const bool deferred = valid[t] && p[t] < e[t] && !(found[t] && early_exit);
+        unsigned dm = __ballot_sync(kFull, deferred);
+        while (dm) {
+          const unsigned l = __ffs(dm) - 1;
+          dm &= dm - 1;
+          const Off pb = __shfl_sync(kFull, p[t], l), pe = __shfl_sync(kFull, e[t], l);
+          bool f = __shfl_sync(kFull, found[t] ? 1 : 0, l) != 0;
+          uint32_t fx = __shfl_sync(kFull, par[t], l);
+          for (Off q0 = pb; q0 < pe; q0 += 128) {
+            uint32_t x[4];
+            bool h[4];
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+              const Off q = q0 + (Off)(s * 32) + lane;
+              x[s] = q < pe ? a.cidx[q] : 0u;
+            }
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+              const Off q = q0 + (Off)(s * 32) + lane;
+              h[s] = q < pe && hit(x[s]);
+            }
+            bool stop = false;
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+              const unsigned bm = __ballot_sync(kFull, h[s]);
+              if (bm && !f) {
+                f = true;
+                fx = __shfl_sync(kFull, x[s], __ffs(bm) - 1);
               }
+              stop = stop || (f && early_exit);
             }
+            if (stop) break;
           }
-          p = lim;
+          if (lane == l) {
+            found[t] = f;
+            par[t] = fx;
+          }
         }
       }
-      // Warp-cooperative continuation for rows still unresolved: 128 indices per
-      // step (4 coalesced loads per lane), ballot early exit.
-      const bool deferred = valid && p < e && (!found || !early_exit);
-      unsigned dm = __ballot_sync(kFull, deferred);
-      while (dm) {
-        const unsigned l = __ffs(dm) - 1;
-        dm &= dm - 1;
-        const Off pb = __shfl_sync(kFull, p, l), pe = __shfl_sync(kFull, e, l);
-        bool f = __shfl_sync(kFull, found ? 1 : 0, l) != 0;
-        uint32_t fx = __shfl_sync(kFull, par, l);
-        for (Off q0 = pb; q0 < pe; q0 += 128) {
-          uint32_t x[4];
-          bool h[4];
 #pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const Off q = q0 + (Off)(t * 32) + lane;
-            x[t] = q < pe ? a.cidx[q] : 0u;
-          }
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const Off q = q0 + (Off)(t * 32) + lane;
-            h[t] = q < pe && (no_reuse ? (a.depth[x[t]] == d) : bit_test(vin, x[t]));
-          }
-          bool stop = false;
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const unsigned bm = __ballot_sync(kFull, h[t]);
-            if (bm && !f) {
-              f = true;
-              fx = __shfl_sync(kFull, x[t], __ffs(bm) - 1);
-            }
-            stop = stop || (f && early_exit);
-          }
-          if (stop) break;
+      for (int t = 0; t < kC; ++t) {
+        if (found[t] && ((uj[t] >> bitpos[t]) & 1u)) {
+          atomicOr(&sfound[jj[t]], 1u << bitpos[t]);
+          a.depth[i[t]] = d + 1;
+          if (PARENTS) a.parent[i[t]] = par[t];
+          const Off degin = e[t] - rb[t];
+          const Off deg = a.symmetric ? degin : (Off)(a.off[i[t] + 1] - a.off[i[t]]);
+          acc.c += 1;
+          acc.mf += (unsigned long long)deg;
+          acc.mfin += (unsigned long long)degin;
         }
-        if (lane == l) {
-          found = f;
-          par = fx;
-        }
-      }
-      if (found && ((uj >> bitpos) & 1u)) {
-        atomicOr(&sfound[j], 1u << bitpos);
-        a.depth[i] = d + 1;
-        if (PARENTS) a.parent[i] = par;
-        const Off degin = e - rb;
-        const Off deg = a.symmetric ? degin : (Off)(a.off[i + 1] - a.off[i]);
-        acc.c += 1;
-        acc.mf += (unsigned long long)deg;
-        acc.mfin += (unsigned long long)degin;
       }
     }
     __syncwarp();
-    vout[wbase + lane] = vw | sfound[lane];
+    if (own) vout[wbase + lane] = vw | sfound[lane];
     __syncwarp();
   }
 }
@@ -359,9 +520,7 @@ __device__ void convert_phase(const BfsArgs<Off>& a, const uint32_t* vnew, const
                               uint32_t* Lout, uint2* Hout, LevelCtr* out) {
   const unsigned lane = lane_id();
   const unsigned nchunks = a.nwords / 32u;
-  for (;;) {
-    const unsigned item = warp_grab(&out->work2);
-    if (item >= nchunks) break;
+  for (unsigned item = gwarp(); item < nchunks; item += nwarps()) {
     const unsigned w = item * 32u + lane;
     uint32_t diff = vnew[w] & ~vold[w];
     while (__ballot_sync(kFull, diff != 0u)) {
@@ -392,13 +551,32 @@ __device__ __forceinline__ int decide(int rule, int dir, long long c_old, long l
   return (c_new < c_old && cn < __dmul_rn(beta, nn)) ? 0 : 1;
 }
 
+struct BfsShared {
+  uint32_t sfound[kBfsWarps][32];
+  unsigned long long red[kBfsWarps][3];
+  long long lvl[5];  // c, m_f, m_fin, nL, nH of the level just finished
+};
+
+// thread 0 reads a level's counters once (post-barrier) and broadcasts them via smem
+__device__ __forceinline__ void read_level(const LevelCtr* out, BfsShared& sh) {
+  if (threadIdx.x == 0) {
+    sh.lvl[0] = (long long)ld_relaxed_u64(&out->c);
+    sh.lvl[1] = (long long)ld_relaxed_u64(&out->m_f);
+    sh.lvl[2] = (long long)ld_relaxed_u64(&out->m_fin);
+    sh.lvl[3] = (long long)ld_relaxed_u32(&out->nL);
+    sh.lvl[4] = (long long)ld_relaxed_u32(&out->nH);
+  }
+  __syncthreads();
+}
+
 template <typename Off, bool PARENTS>
-__global__ void __launch_bounds__(kBlock, 4) bfs_persistent(BfsArgs<Off> a) {
-  __shared__ uint32_t sfound[kWarps][32];
+__global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
+  __shared__ BfsShared sh;
   const unsigned warp = threadIdx.x >> 5;
   const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned long long gsize = (unsigned long long)gridDim.x * blockDim.x;
   const uint32_t s = a.source;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t_start = (long long)global_timer_ns();
 
   // ---- Alg. 1 lines 2-4: d <- 1, f <- e_s, v <- 0 (depth 0 = unvisited) ----
   for (unsigned long long v = gtid; v < (unsigned long long)a.n; v += gsize) {
@@ -424,6 +602,9 @@ __global__ void __launch_bounds__(kBlock, 4) bfs_persistent(BfsArgs<Off> a) {
     }
   }
   if (!grid_barrier(a.bar, a.status)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t_init = (long long)global_timer_ns();
+  read_level(&a.ctr[0], sh);
+  unsigned nL = (unsigned)sh.lvl[3], nH = (unsigned)sh.lvl[4];
 
   int dir = (a.mode == 2) ? 1 : 0;
   int cur = 0;  // visited bitmap in use
@@ -435,24 +616,23 @@ __global__ void __launch_bounds__(kBlock, 4) bfs_persistent(BfsArgs<Off> a) {
   Acc acc{0, 0, 0};
   int d = 1;
   for (;; ++d) {
-    LevelCtr* in = &a.ctr[(d - 1) & (kRing - 1)];
     LevelCtr* out = &a.ctr[d & (kRing - 1)];
     if (blockIdx.x == 0 && threadIdx.x < sizeof(LevelCtr) / 4)
       reinterpret_cast<unsigned*>(&a.ctr[(d + 1) & (kRing - 1)])[threadIdx.x] = 0u;
     uint32_t* vis = cur ? a.vis1 : a.vis0;
     uint32_t* vis_other = cur ? a.vis0 : a.vis1;
     if (dir == 0) {
-      const unsigned nL = ld_relaxed_u32(&in->nL), nH = ld_relaxed_u32(&in->nH);
       push_phase<Off, PARENTS>(a, sel ? a.L1 : a.L0, nL, sel ? a.H1 : a.H0, nH,
                                sel ? a.L0 : a.L1, sel ? a.H0 : a.H1, out, vis, d + 1, acc);
     } else {
-      pull_phase<Off, PARENTS>(a, vis, vis_other, out, d, acc, sfound[warp]);
+      pull_phase<Off, PARENTS>(a, vis, vis_other, out, d, acc, sh.sfound[warp]);
     }
-    flush_acc(acc, out);
+    flush_acc(acc, out, sh.red);
     if (!grid_barrier(a.bar, a.status)) return;
-    const long long c_new = (long long)ld_relaxed_u64(&out->c);
-    const long long mf = (long long)ld_relaxed_u64(&out->m_f);
-    const long long mfin = (long long)ld_relaxed_u64(&out->m_fin);
+    read_level(out, sh);
+    const long long c_new = sh.lvl[0], mf = sh.lvl[1], mfin = sh.lvl[2];
+    nL = (unsigned)sh.lvl[3];
+    nH = (unsigned)sh.lvl[4];
     if (dir == 1) cur ^= 1;
     else sel ^= 1;
     m_u -= a.symmetric ? mf : mfin;
@@ -464,6 +644,7 @@ __global__ void __launch_bounds__(kBlock, 4) bfs_persistent(BfsArgs<Off> a) {
       st.c = c_new;
       st.m_f = mf;
       st.m_u = m_u;
+      st.t_ns = (long long)global_timer_ns();
       a.stats[d - 1] = st;
     }
     if (c_new == 0 || d >= a.max_levels) break;
@@ -475,6 +656,9 @@ __global__ void __launch_bounds__(kBlock, 4) bfs_persistent(BfsArgs<Off> a) {
       uint32_t* vold = cur ? a.vis0 : a.vis1;
       convert_phase<Off>(a, vnew, vold, sel ? a.L1 : a.L0, sel ? a.H1 : a.H0, out);
       if (!grid_barrier(a.bar, a.status)) return;
+      read_level(out, sh);
+      nL = (unsigned)sh.lvl[3];
+      nH = (unsigned)sh.lvl[4];
     }
     dir = next;
     c_old = c_new;
@@ -492,7 +676,7 @@ static int grid_for() {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bfs_persistent<Off, PARENTS>, kBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bfs_persistent<Off, PARENTS>, kBfsBlock, 0);
     cached = sms * (per > 0 ? per : 1);
   }
   return cached;
@@ -509,7 +693,7 @@ static cudaError_t launch_t(pp_graph g, const BfsArgs<Off>& args) {
   void* params[] = {(void*)&args};
   g->ctx->launches += 1;
   return cudaLaunchCooperativeKernel((const void*)bfs_persistent<Off, PARENTS>, dim3(grid),
-                                     dim3(kBlock), params, 0, g->ctx->stream);
+                                     dim3(kBfsBlock), params, 0, g->ctx->stream);
 }
 
 template <typename Off>

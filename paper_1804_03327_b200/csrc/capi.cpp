@@ -202,12 +202,15 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr
             (long long)ends[2], (long long)ends[3], (long long)nnz);
 
   // column ids
-  if ((s = dalloc(&g->idx, (size_t)nnz, &bytes, "csr idx")) != PP_OK) return s;
+  // ids padded by 8 zero entries: the pull kernel reads aligned 16-byte blocks
+  if ((s = dalloc(&g->idx, (size_t)nnz + 8, &bytes, "csr idx")) != PP_OK) return s;
+  PP_CK(cudaMemsetAsync(g->idx + nnz, 0, 8 * sizeof(uint32_t), st), "pad idx");
   if (nnz) PP_CK(cudaMemcpyAsync(g->idx, csr_idx, sizeof(uint32_t) * nnz, cudaMemcpyDefault, st), "copy idx");
   if (symmetric) {
     g->cidx = g->idx;
   } else {
-    if ((s = dalloc(&g->cidx, (size_t)nnz, &bytes, "csc idx")) != PP_OK) return s;
+    if ((s = dalloc(&g->cidx, (size_t)nnz + 8, &bytes, "csc idx")) != PP_OK) return s;
+    PP_CK(cudaMemsetAsync(g->cidx + nnz, 0, 8 * sizeof(uint32_t), st), "pad csc idx");
     if (nnz)
       PP_CK(cudaMemcpyAsync(g->cidx, csc_idx, sizeof(uint32_t) * nnz, cudaMemcpyDefault, st),
             "copy csc idx");
@@ -493,6 +496,7 @@ pp_status pp_bfs(pp_graph g, int64_t source, const pp_bfs_options* opts, int32_t
   }
   if (stats) {
     stats->levels = g->status_host->levels;
+    stats->init_ns = g->status_host->t_init - g->status_host->t_start;
     stats->reached = g->status_host->reached;
     const int m = std::min(std::min(stats->capacity, g->status_host->levels), g->stats_cap);
     if (m > 0) {
@@ -503,6 +507,7 @@ pp_status pp_bfs(pp_graph g, int64_t source, const pp_bfs_options* opts, int32_t
         return cuda_fail(e, "copy stats");
       }
       for (int k = 0; k < m; ++k) {
+        if (stats->ns) stats->ns[k] = hs[k].t_ns - (k ? hs[k - 1].t_ns : g->status_host->t_init);
         if (stats->dir) stats->dir[k] = (int8_t)hs[k].dir;
         if (stats->c) stats->c[k] = hs[k].c;
         if (stats->m_f) stats->m_f[k] = hs[k].m_f;

@@ -80,7 +80,7 @@ __global__ void k_b2l_count(const uint32_t* __restrict__ bits, uint32_t nwords,
 
 __global__ void k_b2l_scan(uint32_t* __restrict__ bsum, uint32_t nblk,
                            unsigned long long* total) {
-  __shared__ unsigned long long s[kWarps];
+  __shared__ unsigned long long s[32];  // launched with 1024 threads
   __shared__ unsigned long long carry;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
@@ -244,11 +244,18 @@ __global__ void __launch_bounds__(kBlock) k_classify(int64_t n, const uint32_t* 
     if (hm) {
       const unsigned nch = heavy ? (unsigned)((deg + (Off)kChunk - 1) / (Off)kChunk) : 0u;
       const unsigned incl = warp_incl_scan(nch);
+      const unsigned excl = incl - nch;
       const unsigned tot = __shfl_sync(kFull, incl, 31);
       unsigned base = 0;
       if (lane == 0) base = atomicAdd(&ctr->nH, tot);
       base = __shfl_sync(kFull, base, 0);
-      for (unsigned q = 0; q < nch; ++q) H[base + incl - nch + q] = make_uint2(single, q);
+      for (unsigned c0 = 0; c0 < tot; c0 += 32) {  // 32 descriptors per step
+        const unsigned c = c0 + lane;
+        const unsigned j = warp_owner(incl, c);
+        const uint32_t vj = __shfl_sync(kFull, single, j);
+        const unsigned xj = __shfl_sync(kFull, excl, j);
+        if (c < tot) H[base + c] = make_uint2(vj, c - xj);
+      }
     }
   }
 }

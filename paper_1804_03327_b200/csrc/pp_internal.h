@@ -12,9 +12,11 @@ namespace pp {
 // ---- tunables ---------------------------------------------------------------
 constexpr int kBlock = 256;        // threads per CTA of every kernel
 constexpr int kWarps = kBlock / 32;
-constexpr unsigned kHeavy = 256;   // out-degree >= kHeavy: expanded as kChunk-edge chunks
-constexpr unsigned kChunk = 256;   // edges per heavy chunk (push load balance)
+constexpr unsigned kHeavy = 128;   // out-degree >= kHeavy: expanded as kChunk-edge chunks
+constexpr unsigned kChunk = 128;   // edges per heavy chunk = one 4-deep warp iteration
 constexpr int kRing = 4;           // level-counter ring
+constexpr int kBfsBlock = 1024;    // persistent BFS: one 1024-thread CTA per SM
+constexpr int kBfsWarps = kBfsBlock / 32;
 
 // Per-level counters, written with atomics during a level, read after the grid barrier.
 struct LevelCtr {
@@ -31,6 +33,7 @@ struct LevelStat {
   int dir;
   int pad;
   long long c, m_f, m_u;
+  long long t_ns;  // %globaltimer when the level's barrier released (block 0)
 };
 
 struct GridBarrier {
@@ -45,6 +48,7 @@ struct BfsStatus {
   int error;   // 0 or pp_status
   int levels;  // levels executed
   long long reached;
+  long long t_start, t_init;  // %globaltimer at kernel entry / after the init barrier
 };
 
 }  // namespace pp
