@@ -267,7 +267,7 @@ def main():
             mt += step_ms[k] * 1e-3
         del off_t, idx_t, rows_t, deg_t, noniso, gd
         peak, peak_src = measured_peaks()
-        achieved = mb / mt / 1e9
+        achieved = mb / mt / 1e9 if mt > 0 else 0.0
         traffic = None
         prof = os.path.join(ROOT, "profiles", f"ncu_{args.config}.json")
         if os.path.exists(prof):

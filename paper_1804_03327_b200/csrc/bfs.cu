@@ -155,12 +155,14 @@ __device__ __forceinline__ void append_frontier(bool valid, uint32_t v, Off deg,
     unsigned base = 0;
     if (lane == 0) base = atomicAdd(&out->nH, tot);
     base = __shfl_sync(kFull, base, 0);
-    for (unsigned c0 = 0; c0 < tot; c0 += 32) {  // 32 descriptors per step
-      const unsigned c = c0 + lane;
-      const unsigned j = warp_owner(incl, c);
-      const uint32_t vj = __shfl_sync(kFull, v, j);
-      const unsigned xj = __shfl_sync(kFull, excl, j);
-      if (c < tot) Hout[base + c] = make_uint2(vj, c - xj);
+    unsigned hb = hm;
+    while (hb) {  // vertex by vertex, 32 descriptors per step
+      const unsigned l = __ffs(hb) - 1;
+      hb &= hb - 1;
+      const uint32_t vl = __shfl_sync(kFull, v, l);
+      const unsigned n = __shfl_sync(kFull, nch, l);
+      const unsigned st = base + __shfl_sync(kFull, excl, l);
+      for (unsigned c = lane; c < n; c += 32) Hout[st + c] = make_uint2(vl, c);
     }
   }
 }
@@ -192,35 +194,26 @@ __device__ __forceinline__ void append_frontier4(const bool (&disc)[kU], const u
     }
   }
   if (__any_sync(kFull, hsum != 0)) {
-    // heavy chunks written warp-cooperatively: 32 consecutive descriptors per step
+    // heavy chunks: one atomic per warp, then vertex by vertex, 32 descriptors per step
     const unsigned incl = warp_incl_scan(hsum);
-    const unsigned excl = incl - hsum;
     const unsigned tot = __shfl_sync(kFull, incl, 31);
     unsigned base = 0;
     if (lane == 0) base = atomicAdd(&out->nH, tot);
-    base = __shfl_sync(kFull, base, 0);
-    unsigned nch[kU];
+    unsigned start = __shfl_sync(kFull, base, 0) + incl - hsum;
 #pragma unroll
-    for (int t = 0; t < kU; ++t)
-      nch[t] = (disc[t] && deg[t] >= (Off)kHeavy) ? (unsigned)((deg[t] + (Off)kChunk - 1) / (Off)kChunk) : 0u;
-    for (unsigned c0 = 0; c0 < tot; c0 += 32) {
-      const unsigned c = c0 + lane;
-      const unsigned j = warp_owner(incl, c);
-      unsigned r = c - __shfl_sync(kFull, excl, j);
-      uint32_t vv = 0;
-      bool done = false;
-#pragma unroll
-      for (int t = 0; t < kU; ++t) {
-        const unsigned nt = __shfl_sync(kFull, nch[t], j);
-        const uint32_t wt = __shfl_sync(kFull, w[t], j);
-        if (!done && r < nt) {
-          vv = wt;
-          done = true;
-        } else if (!done) {
-          r -= nt;
-        }
+    for (int t = 0; t < kU; ++t) {
+      const unsigned nch = (disc[t] && deg[t] >= (Off)kHeavy)
+                               ? (unsigned)((deg[t] + (Off)kChunk - 1) / (Off)kChunk) : 0u;
+      unsigned hb = __ballot_sync(kFull, nch != 0);
+      while (hb) {
+        const unsigned l = __ffs(hb) - 1;
+        hb &= hb - 1;
+        const uint32_t v = __shfl_sync(kFull, w[t], l);
+        const unsigned n = __shfl_sync(kFull, nch, l);
+        const unsigned st = __shfl_sync(kFull, start, l);
+        for (unsigned c = lane; c < n; c += 32) Hout[st + c] = make_uint2(v, c);
       }
-      if (c < tot) Hout[base + c] = make_uint2(vv, r);
+      start += nch;
     }
   }
 }
@@ -340,41 +333,48 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint32_t* Lin, unsigned 
 
 constexpr unsigned kPW = 8;   // bitmap words per pull item (256 rows)
 constexpr int kC = 2;         // candidates in flight per lane
-constexpr int kLaneMax = 32;  // rows with <= this many ids left finish lane-parallel
+constexpr int kLaneMax = 64;  // residual rows with <= this many ids left go lane-parallel
+constexpr int kQ = 96;        // residual-queue entries per warp (31 + 32*kC fits)
+constexpr uint32_t kNone = 0xFFFFFFFFu;
+
+// Rows whose first sector did not decide them, parked per warp in shared memory and
+// processed 32 at a time so no lane idles behind one long row.
+template <typename Off>
+struct ResidualQ {
+  uint32_t i[kQ];
+  uint32_t par[kQ];  // kNone = not found yet (else: committed, scan continues w/o early exit)
+  Off p[kQ];
+  uint32_t rem[kQ];
+  uint32_t degin[kQ];
+};
 
 __device__ __forceinline__ uint4 ld_nc_u4(const uint32_t* p) {
   return __ldg(reinterpret_cast<const uint4*>(p));
 }
 
-// Row-based masked mxv with early exit over the complement of the visited snapshot.
-// Warp item = kPW bitmap words; candidates (zero bits) are enumerated warp-balanced and
-// processed kC per lane at a time so their loads overlap.  First probe = the aligned
-// 8-id block (one 32 B sector) holding the row's first id, two ld.global.nc.v4, all
-// ids tested together; the first hit in sorted order is the min-id parent (R14).  Rows
-// with <= kLaneMax ids left continue lane-parallel (8 ids per step); longer rows are
-// finished warp-cooperatively, 128 ids per step with a ballot early exit.  Found bits are
-// OR-ed in shared memory; the owning lane writes v' = v | found (no global atomics).
 template <typename Off, bool PARENTS>
-__device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
-                           uint32_t* __restrict__ vout, LevelCtr* out, int d, Acc& acc,
-                           uint32_t* sfound) {
-  const unsigned lane = lane_id();
-  const unsigned nitems = a.nwords / kPW;
-  const bool early_exit = !(a.toggles & PP_OPT_NO_EARLYEXIT);
-  const bool no_mask = (a.toggles & PP_OPT_NO_MASKING) != 0;
-  const bool no_reuse = (a.toggles & PP_OPT_NO_REUSE) != 0;
-  auto hit = [&](uint32_t x) -> bool {
+struct PullCtx {
+  const BfsArgs<Off>& a;
+  const uint32_t* __restrict__ vin;
+  uint32_t* __restrict__ vout;
+  int d;
+  bool early_exit, no_reuse;
+  Acc& acc;
+  uint32_t* sfound;
+  ResidualQ<Off>& q;
+
+  __device__ __forceinline__ bool hit(uint32_t x) const {
     return no_reuse ? (a.depth[x] == d) : bit_test(vin, x);
-  };
-  // test ids [q0, q0+8) clipped to [rb, e); record the first hit
-  auto probe8 = [&](Off q0, Off rb, Off e, bool& found, uint32_t& par) {
+  }
+  // test ids [q0, q0+8) clipped to [rb, e) (q0 8-aligned: one 32 B sector); first hit wins
+  __device__ __forceinline__ void probe8(Off q0, Off rb, Off e, bool& found, uint32_t& par) const {
     const uint4 lo = ld_nc_u4(a.cidx + q0), hi = ld_nc_u4(a.cidx + q0 + 4);
     const uint32_t x[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
     bool h[8];
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
-      const Off q = q0 + (Off)t;
-      h[t] = q >= rb && q < e && hit(x[t]);
+      const Off qq = q0 + (Off)t;
+      h[t] = qq >= rb && qq < e && hit(x[t]);
     }
 #pragma unroll
     for (int t = 0; t < 8; ++t) {
@@ -383,9 +383,113 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
         par = x[t];
       }
     }
-  };
+  }
+  // discovery of row i (found this level): Alg. 1 lines 7-8 fused
+  __device__ __forceinline__ void commit(uint32_t i, uint32_t par, Off degin, unsigned wbase,
+                                         bool in_item) const {
+    const uint32_t bit = 1u << (i & 31u);
+    if (in_item) atomicOr(&sfound[(i >> 5) - wbase], bit);
+    else atomicOr(&vout[i >> 5], bit);
+    a.depth[i] = d + 1;
+    if (PARENTS) a.parent[i] = par;
+    const Off deg = a.symmetric ? degin : (Off)(a.off[i + 1] - a.off[i]);
+    acc.c += 1;
+    acc.mf += (unsigned long long)deg;
+    acc.mfin += (unsigned long long)degin;
+  }
+  // process the top `cnt` (<= 32) residual rows, one per lane
+  __device__ void residual_batch(int& qn, int cnt, unsigned wbase, bool item_open) const {
+    const unsigned lane = lane_id();
+    const int slot = qn - cnt + (int)lane;
+    const bool valid = (int)lane < cnt;
+    uint32_t i = 0, par = kNone, degin = 0;
+    Off p = 0, e = 0;
+    if (valid) {
+      i = q.i[slot];
+      par = q.par[slot];
+      p = q.p[slot];
+      e = p + (Off)q.rem[slot];
+      degin = q.degin[slot];
+    }
+    __syncwarp();
+    qn -= cnt;
+    const bool committed = par != kNone;
+    bool found = committed;
+    while (true) {
+      const bool act = valid && p < e && !(found && early_exit) && (e - p) <= (Off)kLaneMax;
+      if (!__any_sync(kFull, act)) break;
+      if (act) {
+        probe8(p, p, e, found, par);
+        p += 8;
+      }
+    }
+    const bool deferred = valid && p < e && !(found && early_exit);
+    unsigned dm = __ballot_sync(kFull, deferred);
+    while (dm) {  // long rows: warp-cooperative, 128 ids per step, ballot early exit
+      const unsigned l = __ffs(dm) - 1;
+      dm &= dm - 1;
+      const Off pb = __shfl_sync(kFull, p, l), pe = __shfl_sync(kFull, e, l);
+      bool f = __shfl_sync(kFull, found ? 1 : 0, l) != 0;
+      uint32_t fx = __shfl_sync(kFull, par, l);
+      for (Off q0 = pb; q0 < pe; q0 += 128) {
+        uint32_t x[4];
+        bool h[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          const Off qq = q0 + (Off)(s * 32) + lane;
+          x[s] = qq < pe ? a.cidx[qq] : 0u;
+        }
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          const Off qq = q0 + (Off)(s * 32) + lane;
+          h[s] = qq < pe && hit(x[s]);
+        }
+        bool stop = false;
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          const unsigned bm = __ballot_sync(kFull, h[s]);
+          if (bm && !f) {
+            f = true;
+            fx = __shfl_sync(kFull, x[s], __ffs(bm) - 1);
+          }
+          stop = stop || (f && early_exit);
+        }
+        if (stop) break;
+      }
+      if (lane == l) {
+        found = f;
+        par = fx;
+      }
+    }
+    if (valid && found && !committed) {
+      const bool in_item = item_open && (i >> 5) >= wbase && (i >> 5) < wbase + kPW;
+      commit(i, par, (Off)degin, wbase, in_item);
+    }
+  }
+};
+
+// Row-based masked mxv with early exit over the complement of the visited snapshot
+// (Alg. 2 re-designed).  Warp item = kPW bitmap words; candidates (zero bits) are
+// enumerated warp-balanced and processed kC per lane at a time so their loads overlap:
+// offsets, then the aligned 8-id block (one 32 B sector) holding the row's first id
+// (two ld.global.nc.v4), all ids tested together; first hit in sorted order = min-id
+// parent (R14).  Rows the first sector does not decide are parked in the warp's residual
+// queue and finished 32 at a time (lane-parallel for short remainders, warp-cooperative
+// with a ballot early exit for long ones).  Found bits are OR-ed in shared memory and the
+// owning lane writes v' = v | found; rows resolved after their item closed use atomicOr.
+template <typename Off, bool PARENTS>
+__device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
+                           uint32_t* __restrict__ vout, LevelCtr* out, int d, Acc& acc,
+                           uint32_t* sfound, ResidualQ<Off>& rq) {
+  const unsigned lane = lane_id();
+  const unsigned nitems = a.nwords / kPW;
+  const bool no_mask = (a.toggles & PP_OPT_NO_MASKING) != 0;
+  PullCtx<Off, PARENTS> C{a, vin, vout, d, !(a.toggles & PP_OPT_NO_EARLYEXIT),
+                          (a.toggles & PP_OPT_NO_REUSE) != 0, acc, sfound, rq};
+  int qn = 0;
+  unsigned wbase = 0;
   for (unsigned item = gwarp(); item < nitems; item += nwarps()) {
-    const unsigned wbase = item * kPW;
+    wbase = item * kPW;
     const bool own = lane < kPW;
     const uint32_t vw = own ? vin[wbase + lane] : 0xFFFFFFFFu;
     const uint32_t unvisited = ~vw;
@@ -400,22 +504,22 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
     const unsigned tot = __shfl_sync(kFull, incl, 31);
     for (unsigned base = 0; base < tot; base += 32 * kC) {
       bool valid[kC], found[kC];
-      unsigned jj[kC], bitpos[kC];
       uint32_t i[kC], uj[kC], par[kC];
+      unsigned bitpos[kC];
       Off rb[kC], e[kC], p[kC];
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
         const unsigned k = base + t * 32 + lane;
         valid[t] = k < tot;
-        jj[t] = warp_owner(incl, k);
-        const uint32_t mj = __shfl_sync(kFull, cand, jj[t]);
-        const unsigned xj = __shfl_sync(kFull, excl, jj[t]);
-        uj[t] = __shfl_sync(kFull, unvisited, jj[t]);
+        const unsigned j = warp_owner(incl, k);
+        const uint32_t mj = __shfl_sync(kFull, cand, j);
+        const unsigned xj = __shfl_sync(kFull, excl, j);
+        uj[t] = __shfl_sync(kFull, unvisited, j);
         bitpos[t] = valid[t] ? __fns(mj, 0, (int)(k - xj) + 1) : 0u;
-        i[t] = (wbase + jj[t]) * 32u + bitpos[t];
+        i[t] = (wbase + j) * 32u + bitpos[t];
         found[t] = false;
-        par[t] = 0;
-        rb[t] = e[t] = p[t] = 0;
+        par[t] = kNone;
+        rb[t] = e[t] = 0;
       }
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
@@ -426,88 +530,35 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
       }
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
+        p[t] = e[t];
         if (valid[t] && rb[t] < e[t]) {
           const Off q0 = rb[t] & ~(Off)7;
-          probe8(q0, rb[t], e[t], found[t], par[t]);
+          C.probe8(q0, rb[t], e[t], found[t], par[t]);
           p[t] = q0 + 8;
-        } else {
-          p[t] = e[t];
-        }
-      }
-      // lane-parallel continuation of short rows
-      while (true) {
-        bool act[kC], any = false;
-#pragma unroll
-        for (int t = 0; t < kC; ++t) {
-          act[t] = valid[t] && p[t] < e[t] && !(found[t] && early_exit) &&
-                   (e[t] - p[t]) <= (Off)kLaneMax;
-          any = any || act[t];
-        }
-        if (!__any_sync(kFull, any)) break;
-#pragma unroll
-        for (int t = 0; t < kC; ++t) {
-          if (act[t]) {
-            probe8(p[t], rb[t], e[t], found[t], par[t]);
-            p[t] += 8;
-          }
-        }
-      }
-      // warp-cooperative continuation for long rows still unresolved
-#pragma unroll
-      for (int t = 0; t < kC; ++t) {
-        const bool deferred = valid[t] && p[t] < e[t] && !(found[t] && early_exit);
-        unsigned dm = __ballot_sync(kFull, deferred);
-        while (dm) {
-          const unsigned l = __ffs(dm) - 1;
-          dm &= dm - 1;
-          const Off pb = __shfl_sync(kFull, p[t], l), pe = __shfl_sync(kFull, e[t], l);
-          bool f = __shfl_sync(kFull, found[t] ? 1 : 0, l) != 0;
-          uint32_t fx = __shfl_sync(kFull, par[t], l);
-          for (Off q0 = pb; q0 < pe; q0 += 128) {
-            uint32_t x[4];
-            bool h[4];
-#pragma unroll
-            for (int s = 0; s < 4; ++s) {
-              const Off q = q0 + (Off)(s * 32) + lane;
-              x[s] = q < pe ? a.cidx[q] : 0u;
-            }
-#pragma unroll
-            for (int s = 0; s < 4; ++s) {
-              const Off q = q0 + (Off)(s * 32) + lane;
-              h[s] = q < pe && hit(x[s]);
-            }
-            bool stop = false;
-#pragma unroll
-            for (int s = 0; s < 4; ++s) {
-              const unsigned bm = __ballot_sync(kFull, h[s]);
-              if (bm && !f) {
-                f = true;
-                fx = __shfl_sync(kFull, x[s], __ffs(bm) - 1);
-              }
-              stop = stop || (f && early_exit);
-            }
-            if (stop) break;
-          }
-          if (lane == l) {
-            found[t] = f;
-            par[t] = fx;
-          }
         }
       }
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
-        if (found[t] && ((uj[t] >> bitpos[t]) & 1u)) {
-          atomicOr(&sfound[jj[t]], 1u << bitpos[t]);
-          a.depth[i[t]] = d + 1;
-          if (PARENTS) a.parent[i[t]] = par[t];
-          const Off degin = e[t] - rb[t];
-          const Off deg = a.symmetric ? degin : (Off)(a.off[i[t] + 1] - a.off[i[t]]);
-          acc.c += 1;
-          acc.mf += (unsigned long long)deg;
-          acc.mfin += (unsigned long long)degin;
+        const bool fresh = valid[t] && ((uj[t] >> bitpos[t]) & 1u);  // unvisited row
+        if (found[t] && fresh) C.commit(i[t], par[t], e[t] - rb[t], wbase, true);
+        // park undecided rows (and, without early exit, rows with ids left)
+        const bool park = valid[t] && p[t] < e[t] && !(found[t] && C.early_exit) &&
+                          (fresh || !found[t]);
+        const unsigned pm = __ballot_sync(kFull, park);
+        if (park) {
+          const int slot = qn + __popc(pm & lanemask_lt());
+          rq.i[slot] = fresh ? i[t] : kNone - 1;  // visited rows (no masking) never commit
+          rq.par[slot] = (found[t] || !fresh) ? (found[t] ? par[t] : 0u) : kNone;
+          rq.p[slot] = p[t];
+          rq.rem[slot] = (uint32_t)(e[t] - p[t]);
+          rq.degin[slot] = (uint32_t)(e[t] - rb[t]);
         }
+        qn += __popc(pm);
+        __syncwarp();
       }
+      while (qn >= 32) C.residual_batch(qn, 32, wbase, true);
     }
+    if (qn > 0) C.residual_batch(qn, qn, wbase, true);
     __syncwarp();
     if (own) vout[wbase + lane] = vw | sfound[lane];
     __syncwarp();
@@ -551,14 +602,16 @@ __device__ __forceinline__ int decide(int rule, int dir, long long c_old, long l
   return (c_new < c_old && cn < __dmul_rn(beta, nn)) ? 0 : 1;
 }
 
-struct BfsShared {
+template <typename Off>
+struct BfsShared {  // static part; the residual queues live in dynamic shared memory
   uint32_t sfound[kBfsWarps][32];
   unsigned long long red[kBfsWarps][3];
   long long lvl[5];  // c, m_f, m_fin, nL, nH of the level just finished
 };
 
 // thread 0 reads a level's counters once (post-barrier) and broadcasts them via smem
-__device__ __forceinline__ void read_level(const LevelCtr* out, BfsShared& sh) {
+template <typename Off>
+__device__ __forceinline__ void read_level(const LevelCtr* out, BfsShared<Off>& sh) {
   if (threadIdx.x == 0) {
     sh.lvl[0] = (long long)ld_relaxed_u64(&out->c);
     sh.lvl[1] = (long long)ld_relaxed_u64(&out->m_f);
@@ -571,7 +624,9 @@ __device__ __forceinline__ void read_level(const LevelCtr* out, BfsShared& sh) {
 
 template <typename Off, bool PARENTS>
 __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
-  __shared__ BfsShared sh;
+  __shared__ BfsShared<Off> sh;
+  extern __shared__ __align__(16) unsigned char dyn_smem[];
+  ResidualQ<Off>* rqs = reinterpret_cast<ResidualQ<Off>*>(dyn_smem);
   const unsigned warp = threadIdx.x >> 5;
   const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned long long gsize = (unsigned long long)gridDim.x * blockDim.x;
@@ -625,7 +680,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       push_phase<Off, PARENTS>(a, sel ? a.L1 : a.L0, nL, sel ? a.H1 : a.H0, nH,
                                sel ? a.L0 : a.L1, sel ? a.H0 : a.H1, out, vis, d + 1, acc);
     } else {
-      pull_phase<Off, PARENTS>(a, vis, vis_other, out, d, acc, sh.sfound[warp]);
+      pull_phase<Off, PARENTS>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp]);
     }
     flush_acc(acc, out, sh.red);
     if (!grid_barrier(a.bar, a.status)) return;
@@ -669,6 +724,9 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   }
 }
 
+template <typename Off>
+constexpr size_t dyn_smem_bytes() { return sizeof(ResidualQ<Off>) * kBfsWarps; }
+
 template <typename Off, bool PARENTS>
 static int grid_for() {
   static int cached = -1;
@@ -676,7 +734,10 @@ static int grid_for() {
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bfs_persistent<Off, PARENTS>, kBfsBlock, 0);
+    cudaFuncSetAttribute(bfs_persistent<Off, PARENTS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)dyn_smem_bytes<Off>());
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bfs_persistent<Off, PARENTS>, kBfsBlock,
+                                                  dyn_smem_bytes<Off>());
     cached = sms * (per > 0 ? per : 1);
   }
   return cached;
@@ -693,7 +754,8 @@ static cudaError_t launch_t(pp_graph g, const BfsArgs<Off>& args) {
   void* params[] = {(void*)&args};
   g->ctx->launches += 1;
   return cudaLaunchCooperativeKernel((const void*)bfs_persistent<Off, PARENTS>, dim3(grid),
-                                     dim3(kBfsBlock), params, 0, g->ctx->stream);
+                                     dim3(kBfsBlock), params, dyn_smem_bytes<Off>(),
+                                     g->ctx->stream);
 }
 
 template <typename Off>
