@@ -127,8 +127,16 @@ __device__ __forceinline__ void flush_acc(Acc& acc, LevelCtr* out,
   acc.c = acc.mf = acc.mfin = 0;
 }
 
-// Warp work assignment: static round-robin over all warps of the grid (no atomics).
-__device__ __forceinline__ unsigned gwarp() { return blockIdx.x * kBfsWarps + (threadIdx.x >> 5); }
+// Work assignment: CTA b owns items b, b+G, b+2G, ... (interleaved, so every CTA sees the
+// same mix of heavy and light items) and its warps grab them dynamically through a
+// shared-memory counter (reset to 0 before each phase by read_level), which balances the
+// irregular per-item cost inside the CTA without any global atomics.
+__device__ __forceinline__ unsigned cta_grab(unsigned* sctr) {
+  unsigned j = 0;
+  if (lane_id() == 0) j = atomicAdd(sctr, 1u);
+  j = __shfl_sync(kFull, j, 0);
+  return blockIdx.x + j * gridDim.x;
+}
 __device__ __forceinline__ unsigned nwarps() { return gridDim.x * kBfsWarps; }
 
 // Append newly discovered vertex v (valid lanes) to the next frontier: light list if
@@ -278,14 +286,14 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
 template <typename Off, bool PARENTS>
 __device__ void push_phase(const BfsArgs<Off>& a, const uint32_t* Lin, unsigned nL,
                            const uint2* Hin, unsigned nH, uint32_t* Lout, uint2* Hout,
-                           LevelCtr* out, uint32_t* vis, int newdepth, Acc& acc) {
+                           LevelCtr* out, uint32_t* vis, int newdepth, Acc& acc, unsigned* sctr) {
   const unsigned lane = lane_id();
   const unsigned NW = nwarps();
   unsigned R = 32;
   while (R > 1 && (nL + R / 2 - 1) / (R / 2) <= NW) R >>= 1;
   const unsigned nRounds = (nL + R - 1) / R;
   const unsigned total = nH + nRounds;
-  for (unsigned item = gwarp(); item < total; item += NW) {
+  for (unsigned item = cta_grab(sctr); item < total; item = cta_grab(sctr)) {
     bool valid[kU];
     uint32_t u[kU], w[kU];
     if (item < nH) {
@@ -333,7 +341,8 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint32_t* Lin, unsigned 
 
 constexpr unsigned kPW = 8;   // bitmap words per pull item (256 rows)
 constexpr int kC = 2;         // candidates in flight per lane
-constexpr int kLaneMax = 64;  // residual rows with <= this many ids left go lane-parallel
+constexpr int kLaneMax = 16;    // residual rows with <= this many ids left: one lane each
+constexpr int kGroupMax = 1024;  // <= this many: 8-lane groups; longer: the whole warp
 constexpr int kQ = 96;        // residual-queue entries per warp (31 + 32*kC fits)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
@@ -415,6 +424,7 @@ struct PullCtx {
     qn -= cnt;
     const bool committed = par != kNone;
     bool found = committed;
+    // tier 0: short remainders, one lane per row, 8 ids per step
     while (true) {
       const bool act = valid && p < e && !(found && early_exit) && (e - p) <= (Off)kLaneMax;
       if (!__any_sync(kFull, act)) break;
@@ -423,38 +433,69 @@ struct PullCtx {
         p += 8;
       }
     }
-    const bool deferred = valid && p < e && !(found && early_exit);
-    unsigned dm = __ballot_sync(kFull, deferred);
-    while (dm) {  // long rows: warp-cooperative, 128 ids per step, ballot early exit
+    // tier 1: medium remainders, 8-lane groups (64 ids per step), 4 rows at once
+    unsigned m1 = __ballot_sync(kFull, valid && p < e && !(found && early_exit) &&
+                                           (e - p) <= (Off)kGroupMax);
+    const unsigned g = lane >> 3, sub = lane & 7u;
+    while (m1) {
+      unsigned pick = 0, mm = m1;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        pick |= mm & (0u - mm);  // lowest set bit
+        mm &= mm - 1;
+      }
+      m1 &= ~pick;
+      const bool has = g < (unsigned)__popc(pick);
+      const unsigned rl = has ? (unsigned)__fns(pick, 0, (int)g + 1) : 0u;
+      Off gp = __shfl_sync(kFull, p, rl);
+      const Off ge = __shfl_sync(kFull, e, rl);
+      bool gf = __shfl_sync(kFull, found ? 1 : 0, rl) != 0;
+      uint32_t gx = __shfl_sync(kFull, par, rl);
+      while (true) {
+        const bool gact = has && gp < ge && !(gf && early_exit);
+        if (!__any_sync(kFull, gact)) break;
+        bool lf = false;
+        uint32_t lx = 0;
+        const Off qq = gp + (Off)(sub * 8u);
+        if (gact && qq < ge) probe8(qq, qq, ge, lf, lx);
+        const unsigned bm = __ballot_sync(kFull, lf) & (0xFFu << (g * 8u));
+        const uint32_t fx = __shfl_sync(kFull, lx, bm ? (unsigned)(__ffs(bm) - 1) : lane);
+        if (gact && bm && !gf) {
+          gf = true;
+          gx = fx;
+        }
+        if (gact) gp += 64;
+      }
+      const bool mine = (pick >> lane) & 1u;
+      const unsigned src = mine ? (unsigned)__popc(pick & lanemask_lt()) * 8u : lane;
+      const bool rf = __shfl_sync(kFull, gf ? 1 : 0, src) != 0;
+      const uint32_t rx = __shfl_sync(kFull, gx, src);
+      const Off rp = __shfl_sync(kFull, gp, src);
+      if (mine) {
+        found = rf;
+        par = rx;
+        p = rp;
+      }
+    }
+    // tier 2: long remainders, whole warp (256 ids per step: 8 per lane), ballot early exit
+    unsigned dm = __ballot_sync(kFull, valid && p < e && !(found && early_exit));
+    while (dm) {
       const unsigned l = __ffs(dm) - 1;
       dm &= dm - 1;
       const Off pb = __shfl_sync(kFull, p, l), pe = __shfl_sync(kFull, e, l);
       bool f = __shfl_sync(kFull, found ? 1 : 0, l) != 0;
       uint32_t fx = __shfl_sync(kFull, par, l);
-      for (Off q0 = pb; q0 < pe; q0 += 128) {
-        uint32_t x[4];
-        bool h[4];
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          const Off qq = q0 + (Off)(s * 32) + lane;
-          x[s] = qq < pe ? a.cidx[qq] : 0u;
+      for (Off q0 = pb; q0 < pe; q0 += 256) {
+        bool lf = false;
+        uint32_t lx = 0;
+        const Off qq = q0 + (Off)(lane * 8u);
+        if (qq < pe) probe8(qq, qq, pe, lf, lx);
+        const unsigned bm = __ballot_sync(kFull, lf);
+        if (bm && !f) {
+          f = true;
+          fx = __shfl_sync(kFull, lx, __ffs(bm) - 1);
         }
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          const Off qq = q0 + (Off)(s * 32) + lane;
-          h[s] = qq < pe && hit(x[s]);
-        }
-        bool stop = false;
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          const unsigned bm = __ballot_sync(kFull, h[s]);
-          if (bm && !f) {
-            f = true;
-            fx = __shfl_sync(kFull, x[s], __ffs(bm) - 1);
-          }
-          stop = stop || (f && early_exit);
-        }
-        if (stop) break;
+        if (f && early_exit) break;
       }
       if (lane == l) {
         found = f;
@@ -480,7 +521,7 @@ struct PullCtx {
 template <typename Off, bool PARENTS>
 __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
                            uint32_t* __restrict__ vout, LevelCtr* out, int d, Acc& acc,
-                           uint32_t* sfound, ResidualQ<Off>& rq) {
+                           uint32_t* sfound, ResidualQ<Off>& rq, unsigned* sctr) {
   const unsigned lane = lane_id();
   const unsigned nitems = a.nwords / kPW;
   const bool no_mask = (a.toggles & PP_OPT_NO_MASKING) != 0;
@@ -488,7 +529,7 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
                           (a.toggles & PP_OPT_NO_REUSE) != 0, acc, sfound, rq};
   int qn = 0;
   unsigned wbase = 0;
-  for (unsigned item = gwarp(); item < nitems; item += nwarps()) {
+  for (unsigned item = cta_grab(sctr); item < nitems; item = cta_grab(sctr)) {
     wbase = item * kPW;
     const bool own = lane < kPW;
     const uint32_t vw = own ? vin[wbase + lane] : 0xFFFFFFFFu;
@@ -568,10 +609,10 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
 // Dense2sparse of the new frontier v' & !v after a pull level (pull->push switch).
 template <typename Off>
 __device__ void convert_phase(const BfsArgs<Off>& a, const uint32_t* vnew, const uint32_t* vold,
-                              uint32_t* Lout, uint2* Hout, LevelCtr* out) {
+                              uint32_t* Lout, uint2* Hout, LevelCtr* out, unsigned* sctr) {
   const unsigned lane = lane_id();
   const unsigned nchunks = a.nwords / 32u;
-  for (unsigned item = gwarp(); item < nchunks; item += nwarps()) {
+  for (unsigned item = cta_grab(sctr); item < nchunks; item = cta_grab(sctr)) {
     const unsigned w = item * 32u + lane;
     uint32_t diff = vnew[w] & ~vold[w];
     while (__ballot_sync(kFull, diff != 0u)) {
@@ -607,6 +648,7 @@ struct BfsShared {  // static part; the residual queues live in dynamic shared m
   uint32_t sfound[kBfsWarps][32];
   unsigned long long red[kBfsWarps][3];
   long long lvl[5];  // c, m_f, m_fin, nL, nH of the level just finished
+  unsigned work;     // CTA-local work counter (cta_grab)
 };
 
 // thread 0 reads a level's counters once (post-barrier) and broadcasts them via smem
@@ -618,6 +660,7 @@ __device__ __forceinline__ void read_level(const LevelCtr* out, BfsShared<Off>& 
     sh.lvl[2] = (long long)ld_relaxed_u64(&out->m_fin);
     sh.lvl[3] = (long long)ld_relaxed_u32(&out->nL);
     sh.lvl[4] = (long long)ld_relaxed_u32(&out->nH);
+    sh.work = 0u;
   }
   __syncthreads();
 }
@@ -678,9 +721,10 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
     uint32_t* vis_other = cur ? a.vis0 : a.vis1;
     if (dir == 0) {
       push_phase<Off, PARENTS>(a, sel ? a.L1 : a.L0, nL, sel ? a.H1 : a.H0, nH,
-                               sel ? a.L0 : a.L1, sel ? a.H0 : a.H1, out, vis, d + 1, acc);
+                               sel ? a.L0 : a.L1, sel ? a.H0 : a.H1, out, vis, d + 1, acc,
+                               &sh.work);
     } else {
-      pull_phase<Off, PARENTS>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp]);
+      pull_phase<Off, PARENTS>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp], &sh.work);
     }
     flush_acc(acc, out, sh.red);
     if (!grid_barrier(a.bar, a.status)) return;
@@ -709,7 +753,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       // pull -> push: Dense2sparse of the frontier just discovered
       uint32_t* vnew = cur ? a.vis1 : a.vis0;
       uint32_t* vold = cur ? a.vis0 : a.vis1;
-      convert_phase<Off>(a, vnew, vold, sel ? a.L1 : a.L0, sel ? a.H1 : a.H0, out);
+      convert_phase<Off>(a, vnew, vold, sel ? a.L1 : a.L0, sel ? a.H1 : a.H0, out, &sh.work);
       if (!grid_barrier(a.bar, a.status)) return;
       read_level(out, sh);
       nL = (unsigned)sh.lvl[3];
