@@ -38,6 +38,11 @@ struct BfsArgs {
   const uint32_t* __restrict__ isolated;
   uint32_t* vis0;
   uint32_t* vis1;
+  uint32_t* fr;  // frontier bitmap written by pull levels (push-from-bitmap)
+  const uint4* __restrict__ head;  // first 4 in-neighbours of every row (pull), kNoId padded
+  uint32_t* sumv;      // visited summary: bit per 2^sum_shift vertices, isolated excluded
+  int sum_shift;
+  uint32_t sum_words;
   uint32_t* L0;
   uint32_t* L1;
   uint2* H0;
@@ -96,35 +101,39 @@ __device__ __forceinline__ bool grid_barrier(GridBarrier* b, BfsStatus* st) {
 
 // Per-lane accumulators of a level's counters, flushed once per phase.
 struct Acc {
-  unsigned long long c, mf, mfin;
+  unsigned long long c, mf, mfin, big;
 };
 
 // CTA-level reduction, then one set of atomics per CTA (single-address L2 atomics
 // serialise; per-warp flushing cost ~3 x #warps atomics per level).
 __device__ __forceinline__ void flush_acc(Acc& acc, LevelCtr* out,
-                                          unsigned long long (*red)[3]) {
+                                          unsigned long long (*red)[4]) {
   const unsigned warp = threadIdx.x >> 5;
-  unsigned long long c = warp_sum(acc.c), mf = warp_sum(acc.mf), mfin = warp_sum(acc.mfin);
+  unsigned long long c = warp_sum(acc.c), mf = warp_sum(acc.mf), mfin = warp_sum(acc.mfin),
+                     big = warp_sum(acc.big);
   if (lane_id() == 0) {
     red[warp][0] = c;
     red[warp][1] = mf;
     red[warp][2] = mfin;
+    red[warp][3] = big;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned long long tc = 0, tm = 0, ti = 0;
+    unsigned long long tc = 0, tm = 0, ti = 0, tb = 0;
     for (int k = 0; k < kBfsWarps; ++k) {
       tc += red[k][0];
       tm += red[k][1];
       ti += red[k][2];
+      tb += red[k][3];
     }
     if (tc) {
       atomicAdd(&out->c, tc);
       atomicAdd(&out->m_f, tm);
       atomicAdd(&out->m_fin, ti);
     }
+    if (tb) atomicAdd(&out->nbig, tb);
   }
-  acc.c = acc.mf = acc.mfin = 0;
+  acc.c = acc.mf = acc.mfin = acc.big = 0;
 }
 
 // Work assignment: CTA b owns items b, b+G, b+2G, ... (interleaved, so every CTA sees the
@@ -249,8 +258,15 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
     }
   }
 #pragma unroll
-  for (int t = 0; t < kU; ++t)
-    if (disc[t]) a.depth[w[t]] = newdepth;
+  for (int t = 0; t < kU; ++t) {
+    if (disc[t]) {
+      a.depth[w[t]] = newdepth;
+      if (kSumWordsMax) {
+        const uint32_t gi = w[t] >> a.sum_shift;
+        atomicOr(&a.sumv[gi >> 5], 1u << (gi & 31u));
+      }
+    }
+  }
   if (PARENTS) {
 #pragma unroll
     for (int t = 0; t < kU; ++t) {
@@ -279,24 +295,57 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
   append_frontier4<Off>(disc, w, deg, Lout, Hout, out);
 }
 
-// Column-based masked mxv over the frontier (light list + heavy chunks).  Heavy chunk =
-// kChunk = 128 consecutive edges = one warp iteration with 4 coalesced loads per lane.
-// Light round = R frontier vertices (R = 32, or fewer when the frontier is too small to
-// occupy every warp), their edges balanced over lanes by a warp scan of degrees.
+// Edges of up to 32 light frontier vertices (lane l holds v, row begin b, degree deg),
+// balanced over lanes by a warp scan of the degrees, kU edges in flight per lane.
+template <typename Off, bool PARENTS>
+__device__ __forceinline__ void push_round(const BfsArgs<Off>& a, uint32_t v, Off b, unsigned deg,
+                                           uint32_t* Lout, uint2* Hout, LevelCtr* out,
+                                           uint32_t* vis, int newdepth, Acc& acc) {
+  const unsigned lane = lane_id();
+  const unsigned incl = warp_incl_scan(deg);
+  const unsigned excl = incl - deg;
+  const unsigned tot = __shfl_sync(kFull, incl, 31);
+  bool valid[kU];
+  uint32_t u[kU], w[kU];
+  for (unsigned base = 0; base < tot; base += 32 * kU) {
+#pragma unroll
+    for (int t = 0; t < kU; ++t) {
+      const unsigned e = base + t * 32 + lane;
+      const unsigned j = warp_owner(incl, e);
+      u[t] = __shfl_sync(kFull, v, j);
+      const Off bj = __shfl_sync(kFull, b, j);
+      const unsigned xj = __shfl_sync(kFull, excl, j);
+      valid[t] = e < tot;
+      w[t] = valid[t] ? a.idx[bj + (Off)(e - xj)] : 0u;
+    }
+    push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc);
+  }
+}
+
+constexpr unsigned kPW = 8;  // bitmap words per warp item (256 rows) for bitmap sweeps
+
+// Column-based masked mxv over the frontier (Alg. 3 re-designed).  The frontier is
+// either (list mode) a light list + heavy chunks, or (bitmap mode, right after a pull
+// level whose discoveries all have out-degree < kBig) the pull's frontier bitmap `fr`,
+// which skips the Dense2sparse conversion and its grid barrier.  Heavy chunk = kChunk =
+// 128 consecutive edges = one warp iteration with 4 coalesced loads per lane.  Light
+// round = R frontier vertices (R = 32, or fewer when the frontier is too small to occupy
+// every warp), their edges balanced over lanes by a warp scan of degrees.
 template <typename Off, bool PARENTS>
 __device__ void push_phase(const BfsArgs<Off>& a, const uint32_t* Lin, unsigned nL,
-                           const uint2* Hin, unsigned nH, uint32_t* Lout, uint2* Hout,
-                           LevelCtr* out, uint32_t* vis, int newdepth, Acc& acc, unsigned* sctr) {
+                           const uint2* Hin, unsigned nH, const uint32_t* fr, uint32_t* Lout,
+                           uint2* Hout, LevelCtr* out, uint32_t* vis, int newdepth, Acc& acc,
+                           unsigned* sctr) {
   const unsigned lane = lane_id();
   const unsigned NW = nwarps();
   unsigned R = 32;
   while (R > 1 && (nL + R / 2 - 1) / (R / 2) <= NW) R >>= 1;
-  const unsigned nRounds = (nL + R - 1) / R;
+  const unsigned nRounds = fr ? a.nwords / kPW : (nL + R - 1) / R;
   const unsigned total = nH + nRounds;
   for (unsigned item = cta_grab(sctr); item < total; item = cta_grab(sctr)) {
-    bool valid[kU];
-    uint32_t u[kU], w[kU];
     if (item < nH) {
+      bool valid[kU];
+      uint32_t u[kU], w[kU];
       const uint2 h = Hin[item];
       const Off rb = a.off[h.x], re = a.off[h.x + 1];
       const Off b = rb + (Off)h.y * (Off)kChunk;
@@ -309,7 +358,7 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint32_t* Lin, unsigned 
         w[t] = valid[t] ? a.idx[p] : 0u;
       }
       push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc);
-    } else {
+    } else if (!fr) {
       const unsigned i = (item - nH) * R + lane;
       uint32_t v = 0;
       Off b = 0;
@@ -319,32 +368,39 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint32_t* Lin, unsigned 
         b = a.off[v];
         deg = (unsigned)(a.off[v + 1] - b);
       }
-      const unsigned incl = warp_incl_scan(deg);
-      const unsigned excl = incl - deg;
+      push_round<Off, PARENTS>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc);
+    } else {
+      const unsigned wbase = (item - nH) * kPW;
+      const uint32_t fw = lane < kPW ? fr[wbase + lane] : 0u;
+      const unsigned cnt = __popc(fw);
+      const unsigned incl = warp_incl_scan(cnt);
+      const unsigned excl = incl - cnt;
       const unsigned tot = __shfl_sync(kFull, incl, 31);
-      for (unsigned base = 0; base < tot; base += 32 * kU) {
-#pragma unroll
-        for (int t = 0; t < kU; ++t) {
-          const unsigned e = base + t * 32 + lane;
-          const unsigned j = warp_owner(incl, e);
-          u[t] = __shfl_sync(kFull, v, j);
-          const Off bj = __shfl_sync(kFull, b, j);
-          const unsigned xj = __shfl_sync(kFull, excl, j);
-          valid[t] = e < tot;
-          w[t] = valid[t] ? a.idx[bj + (Off)(e - xj)] : 0u;
+      for (unsigned base = 0; base < tot; base += 32) {
+        const unsigned k = base + lane;
+        const unsigned j = warp_owner(incl, k);
+        const uint32_t mj = __shfl_sync(kFull, fw, j);
+        const unsigned xj = __shfl_sync(kFull, excl, j);
+        uint32_t v = 0;
+        Off b = 0;
+        unsigned deg = 0;
+        if (k < tot) {
+          v = (wbase + j) * 32u + __fns(mj, 0, (int)(k - xj) + 1);
+          b = a.off[v];
+          deg = (unsigned)(a.off[v + 1] - b);
         }
-        push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc);
+        push_round<Off, PARENTS>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc);
       }
     }
   }
 }
 
-constexpr unsigned kPW = 8;   // bitmap words per pull item (256 rows)
 constexpr int kC = 2;         // candidates in flight per lane
 constexpr int kLaneMax = 16;    // residual rows with <= this many ids left: one lane each
-constexpr int kGroupMax = 1024;  // <= this many: 8-lane groups; longer: the whole warp
+constexpr int kGroupMax = 512;   // <= this many: 8-lane groups; longer: the whole warp
 constexpr int kQ = 96;        // residual-queue entries per warp (31 + 32*kC fits)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr unsigned kSoffStride = 264;  // per-warp shared copy of an item's 257 offsets
 
 // Rows whose first sector did not decide them, parked per warp in shared memory and
 // processed 32 at a time so no lane idles behind one long row.
@@ -361,6 +417,23 @@ __device__ __forceinline__ uint4 ld_nc_u4(const uint32_t* p) {
   return __ldg(reinterpret_cast<const uint4*>(p));
 }
 
+// One 32-byte sector of column ids in a single 256-bit load (LDG.E.ENL2.256 on sm_100a).
+struct V8 {
+  uint32_t x[8];
+};
+__device__ __forceinline__ V8 ld_nc_v8(const uint32_t* p) {
+  V8 v;
+#ifdef PP_IDX_NOALLOC
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+#else
+  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+#endif
+               : "=r"(v.x[0]), "=r"(v.x[1]), "=r"(v.x[2]), "=r"(v.x[3]), "=r"(v.x[4]),
+                 "=r"(v.x[5]), "=r"(v.x[6]), "=r"(v.x[7])
+               : "l"(p));
+  return v;
+}
+
 template <typename Off, bool PARENTS>
 struct PullCtx {
   const BfsArgs<Off>& a;
@@ -371,40 +444,74 @@ struct PullCtx {
   Acc& acc;
   uint32_t* sfound;
   ResidualQ<Off>& q;
+  const uint32_t* ssum;  // shared-memory copy of the visited summary (snapshot)
 
+  // Visited test of a probed neighbour.  The summary in shared memory rejects most
+  // unvisited neighbours without a global access (false positives only: a set summary
+  // bit is confirmed against the exact snapshot bitmap).
   __device__ __forceinline__ bool hit(uint32_t x) const {
-    return no_reuse ? (a.depth[x] == d) : bit_test(vin, x);
+    if (no_reuse) return a.depth[x] == d;
+    if (kSumWordsMax) {
+      const uint32_t gi = x >> a.sum_shift;
+      if (!((ssum[gi >> 5] >> (gi & 31u)) & 1u)) return false;
+    }
+    return bit_test(vin, x);
   }
-  // test ids [q0, q0+8) clipped to [rb, e) (q0 8-aligned: one 32 B sector); first hit wins
-  __device__ __forceinline__ void probe8(Off q0, Off rb, Off e, bool& found, uint32_t& par) const {
-    const uint4 lo = ld_nc_u4(a.cidx + q0), hi = ld_nc_u4(a.cidx + q0 + 4);
-    const uint32_t x[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+  // Ids [q0, q0+8) (q0 8-aligned: one 32-byte sector, a single 256-bit load) clipped to
+  // [rb, e).  The first valid id is probed alone and the others only if it misses:
+  // every probe is a scattered visited-bitmap load, and most rows hit at their first
+  // id.  First hit in sorted order = parent.
+  __device__ __forceinline__ void test8(const V8& v, Off q0, Off rb, Off e, bool& found,
+                                        uint32_t& par) const {
+    const Off f0 = rb > q0 ? rb - q0 : (Off)0;  // first valid slot (0..7)
+    if (q0 + f0 >= e || (found && early_exit)) return;
+    uint32_t xf = v.x[0];
+#pragma unroll
+    for (int t = 1; t < 8; ++t)
+      if ((Off)t == f0) xf = v.x[t];
+    if (hit(xf)) {
+      if (!found) {
+        found = true;
+        par = xf;
+      }
+      if (early_exit) return;
+    }
     bool h[8];
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
-      const Off qq = q0 + (Off)t;
-      h[t] = qq >= rb && qq < e && hit(x[t]);
-    }
+    for (int t = 1; t < 8; ++t) h[t] = (Off)t > f0 && q0 + (Off)t < e && hit(v.x[t]);
 #pragma unroll
-    for (int t = 0; t < 8; ++t) {
+    for (int t = 1; t < 8; ++t) {
       if (h[t] && !found) {
         found = true;
-        par = x[t];
+        par = v.x[t];
       }
     }
+  }
+  __device__ __forceinline__ void probe8(Off q0, Off rb, Off e, bool& found, uint32_t& par) const {
+    const V8 v = ld_nc_v8(a.cidx + q0);
+    test8(v, q0, rb, e, found, par);
   }
   // discovery of row i (found this level): Alg. 1 lines 7-8 fused
   __device__ __forceinline__ void commit(uint32_t i, uint32_t par, Off degin, unsigned wbase,
                                          bool in_item) const {
     const uint32_t bit = 1u << (i & 31u);
-    if (in_item) atomicOr(&sfound[(i >> 5) - wbase], bit);
-    else atomicOr(&vout[i >> 5], bit);
+    if (in_item) {
+      atomicOr(&sfound[(i >> 5) - wbase], bit);
+    } else {
+      atomicOr(&vout[i >> 5], bit);
+      atomicOr(&a.fr[i >> 5], bit);
+    }
     a.depth[i] = d + 1;
     if (PARENTS) a.parent[i] = par;
+    if (kSumWordsMax) {
+      const uint32_t gi = i >> a.sum_shift;
+      atomicOr(&a.sumv[gi >> 5], 1u << (gi & 31u));
+    }
     const Off deg = a.symmetric ? degin : (Off)(a.off[i + 1] - a.off[i]);
     acc.c += 1;
     acc.mf += (unsigned long long)deg;
     acc.mfin += (unsigned long long)degin;
+    acc.big += deg >= (Off)kBig ? 1u : 0u;
   }
   // process the top `cnt` (<= 32) residual rows, one per lane
   __device__ void residual_batch(int& qn, int cnt, unsigned wbase, bool item_open) const {
@@ -429,8 +536,9 @@ struct PullCtx {
       const bool act = valid && p < e && !(found && early_exit) && (e - p) <= (Off)kLaneMax;
       if (!__any_sync(kFull, act)) break;
       if (act) {
-        probe8(p, p, e, found, par);
-        p += 8;
+        const Off q0 = p & ~(Off)7;
+        probe8(q0, p, e, found, par);
+        p = q0 + 8;
       }
     }
     // tier 1: medium remainders, 8-lane groups (64 ids per step), 4 rows at once
@@ -456,15 +564,15 @@ struct PullCtx {
         if (!__any_sync(kFull, gact)) break;
         bool lf = false;
         uint32_t lx = 0;
-        const Off qq = gp + (Off)(sub * 8u);
-        if (gact && qq < ge) probe8(qq, qq, ge, lf, lx);
+        const Off qq = (gp & ~(Off)7) + (Off)(sub * 8u);
+        if (gact && qq < ge) probe8(qq, gp, ge, lf, lx);
         const unsigned bm = __ballot_sync(kFull, lf) & (0xFFu << (g * 8u));
         const uint32_t fx = __shfl_sync(kFull, lx, bm ? (unsigned)(__ffs(bm) - 1) : lane);
         if (gact && bm && !gf) {
           gf = true;
           gx = fx;
         }
-        if (gact) gp += 64;
+        if (gact) gp = (gp & ~(Off)7) + 64;
       }
       const bool mine = (pick >> lane) & 1u;
       const unsigned src = mine ? (unsigned)__popc(pick & lanemask_lt()) * 8u : lane;
@@ -485,11 +593,11 @@ struct PullCtx {
       const Off pb = __shfl_sync(kFull, p, l), pe = __shfl_sync(kFull, e, l);
       bool f = __shfl_sync(kFull, found ? 1 : 0, l) != 0;
       uint32_t fx = __shfl_sync(kFull, par, l);
-      for (Off q0 = pb; q0 < pe; q0 += 256) {
+      for (Off q0 = pb & ~(Off)7; q0 < pe; q0 += 256) {
         bool lf = false;
         uint32_t lx = 0;
         const Off qq = q0 + (Off)(lane * 8u);
-        if (qq < pe) probe8(qq, qq, pe, lf, lx);
+        if (qq < pe) probe8(qq, pb, pe, lf, lx);
         const unsigned bm = __ballot_sync(kFull, lf);
         if (bm && !f) {
           f = true;
@@ -510,23 +618,26 @@ struct PullCtx {
 };
 
 // Row-based masked mxv with early exit over the complement of the visited snapshot
-// (Alg. 2 re-designed).  Warp item = kPW bitmap words; candidates (zero bits) are
-// enumerated warp-balanced and processed kC per lane at a time so their loads overlap:
-// offsets, then the aligned 8-id block (one 32 B sector) holding the row's first id
-// (two ld.global.nc.v4), all ids tested together; first hit in sorted order = min-id
-// parent (R14).  Rows the first sector does not decide are parked in the warp's residual
-// queue and finished 32 at a time (lane-parallel for short remainders, warp-cooperative
-// with a ballot early exit for long ones).  Found bits are OR-ed in shared memory and the
-// owning lane writes v' = v | found; rows resolved after their item closed use atomicOr.
+// (Alg. 2 re-designed).  Warp item = kPW bitmap words (256 rows); candidates (zero bits)
+// are enumerated warp-balanced and processed kC per lane at a time with every stage's
+// loads in flight together: offsets (for dense items one coalesced load of the item's
+// 257 offsets into shared memory), then each row's aligned 4-id block (ld.global.nc.v4),
+// then the first valid id's visited bit, then the block's other ids only for rows that
+// missed.  First hit in sorted order = min-id parent (R14).  Rows the block does not
+// decide are parked in the warp's residual queue and finished 32 at a time (lane / 8-lane
+// group / warp tiers).  Found bits are OR-ed in shared memory; the owning lane writes
+// v' = v | found and the frontier bitmap; rows resolved after their item closed use
+// atomicOr.
 template <typename Off, bool PARENTS>
 __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
                            uint32_t* __restrict__ vout, LevelCtr* out, int d, Acc& acc,
-                           uint32_t* sfound, ResidualQ<Off>& rq, unsigned* sctr) {
+                           uint32_t* sfound, ResidualQ<Off>& rq, const uint32_t* ssum,
+                           unsigned* sctr) {
   const unsigned lane = lane_id();
   const unsigned nitems = a.nwords / kPW;
   const bool no_mask = (a.toggles & PP_OPT_NO_MASKING) != 0;
   PullCtx<Off, PARENTS> C{a, vin, vout, d, !(a.toggles & PP_OPT_NO_EARLYEXIT),
-                          (a.toggles & PP_OPT_NO_REUSE) != 0, acc, sfound, rq};
+                          (a.toggles & PP_OPT_NO_REUSE) != 0, acc, sfound, rq, ssum};
   int qn = 0;
   unsigned wbase = 0;
   for (unsigned item = cta_grab(sctr); item < nitems; item = cta_grab(sctr)) {
@@ -538,15 +649,14 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
     // non-isolated row is computed and the result filtered afterwards.
     const uint32_t cand = no_mask ? (own ? ~a.isolated[wbase + lane] : 0u) : unvisited;
     sfound[lane] = 0u;
-    __syncwarp();
     const unsigned cnt = __popc(cand);
     const unsigned incl = warp_incl_scan(cnt);
     const unsigned excl = incl - cnt;
     const unsigned tot = __shfl_sync(kFull, incl, 31);
+    __syncwarp();
     for (unsigned base = 0; base < tot; base += 32 * kC) {
-      bool valid[kC], found[kC];
-      uint32_t i[kC], uj[kC], par[kC];
-      unsigned bitpos[kC];
+      bool valid[kC], fresh[kC], found[kC];
+      uint32_t i[kC], par[kC];
       Off rb[kC], e[kC], p[kC];
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
@@ -555,53 +665,75 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
         const unsigned j = warp_owner(incl, k);
         const uint32_t mj = __shfl_sync(kFull, cand, j);
         const unsigned xj = __shfl_sync(kFull, excl, j);
-        uj[t] = __shfl_sync(kFull, unvisited, j);
-        bitpos[t] = valid[t] ? __fns(mj, 0, (int)(k - xj) + 1) : 0u;
-        i[t] = (wbase + j) * 32u + bitpos[t];
+        const uint32_t uj = __shfl_sync(kFull, unvisited, j);
+        const unsigned bitpos = valid[t] ? __fns(mj, 0, (int)(k - xj) + 1) : 0u;
+        const unsigned r = j * 32u + bitpos;  // row within the item
+        i[t] = wbase * 32u + r;
+        fresh[t] = valid[t] && ((uj >> bitpos) & 1u);
         found[t] = false;
         par[t] = kNone;
         rb[t] = e[t] = 0;
       }
+      // stage: offsets and the row's head (first 4 in-neighbours, one 16-byte load from a
+      // row-contiguous array: dense items stream it), all in flight
+      uint4 hd[kC];
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
         if (valid[t]) {
           rb[t] = a.coff[i[t]];
           e[t] = a.coff[i[t] + 1];
+          hd[t] = __ldg(a.head + i[t]);
+        }
+      }
+      // stage: probe the first neighbour, then the other head ids of rows that missed
+#pragma unroll
+      for (int t = 0; t < kC; ++t) {
+        const Off deg = e[t] - rb[t];
+        if (valid[t] && deg > 0 && C.hit(hd[t].x)) {
+          found[t] = true;
+          par[t] = hd[t].x;
         }
       }
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
-        p[t] = e[t];
-        if (valid[t] && rb[t] < e[t]) {
-          const Off q0 = rb[t] & ~(Off)7;
-          C.probe8(q0, rb[t], e[t], found[t], par[t]);
-          p[t] = q0 + 8;
+        const Off deg = e[t] - rb[t];
+        if (valid[t] && deg > 1 && !(found[t] && C.early_exit)) {
+          const bool h1 = C.hit(hd[t].y);
+          const bool h2 = deg > 2 && C.hit(hd[t].z);
+          const bool h3 = deg > 3 && C.hit(hd[t].w);
+          if (!found[t] && (h1 || h2 || h3)) {
+            found[t] = true;
+            par[t] = h1 ? hd[t].y : h2 ? hd[t].z : hd[t].w;
+          }
         }
+        p[t] = (valid[t] && deg > 4) ? rb[t] + 4 : e[t];  // the tail continues in idx
       }
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
-        const bool fresh = valid[t] && ((uj[t] >> bitpos[t]) & 1u);  // unvisited row
-        if (found[t] && fresh) C.commit(i[t], par[t], e[t] - rb[t], wbase, true);
+        if (found[t] && fresh[t]) C.commit(i[t], par[t], e[t] - rb[t], wbase, true);
         // park undecided rows (and, without early exit, rows with ids left)
         const bool park = valid[t] && p[t] < e[t] && !(found[t] && C.early_exit) &&
-                          (fresh || !found[t]);
+                          (fresh[t] || !found[t]);
         const unsigned pm = __ballot_sync(kFull, park);
         if (park) {
           const int slot = qn + __popc(pm & lanemask_lt());
-          rq.i[slot] = fresh ? i[t] : kNone - 1;  // visited rows (no masking) never commit
-          rq.par[slot] = (found[t] || !fresh) ? (found[t] ? par[t] : 0u) : kNone;
+          rq.i[slot] = fresh[t] ? i[t] : kNone - 1;  // visited rows (no masking) never commit
+          rq.par[slot] = (found[t] || !fresh[t]) ? (found[t] ? par[t] : 0u) : kNone;
           rq.p[slot] = p[t];
           rq.rem[slot] = (uint32_t)(e[t] - p[t]);
           rq.degin[slot] = (uint32_t)(e[t] - rb[t]);
         }
         qn += __popc(pm);
-        __syncwarp();
       }
+      __syncwarp();
       while (qn >= 32) C.residual_batch(qn, 32, wbase, true);
     }
     if (qn > 0) C.residual_batch(qn, qn, wbase, true);
     __syncwarp();
-    if (own) vout[wbase + lane] = vw | sfound[lane];
+    if (own) {
+      vout[wbase + lane] = vw | sfound[lane];
+      a.fr[wbase + lane] = sfound[lane];
+    }
     __syncwarp();
   }
 }
@@ -646,8 +778,8 @@ __device__ __forceinline__ int decide(int rule, int dir, long long c_old, long l
 template <typename Off>
 struct BfsShared {  // static part; the residual queues live in dynamic shared memory
   uint32_t sfound[kBfsWarps][32];
-  unsigned long long red[kBfsWarps][3];
-  long long lvl[5];  // c, m_f, m_fin, nL, nH of the level just finished
+  unsigned long long red[kBfsWarps][4];
+  long long lvl[6];  // c, m_f, m_fin, nL, nH, nbig of the level just finished
   unsigned work;     // CTA-local work counter (cta_grab)
 };
 
@@ -660,6 +792,7 @@ __device__ __forceinline__ void read_level(const LevelCtr* out, BfsShared<Off>& 
     sh.lvl[2] = (long long)ld_relaxed_u64(&out->m_fin);
     sh.lvl[3] = (long long)ld_relaxed_u32(&out->nL);
     sh.lvl[4] = (long long)ld_relaxed_u32(&out->nH);
+    sh.lvl[5] = (long long)ld_relaxed_u64(&out->nbig);
     sh.work = 0u;
   }
   __syncthreads();
@@ -670,6 +803,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   __shared__ BfsShared<Off> sh;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   ResidualQ<Off>* rqs = reinterpret_cast<ResidualQ<Off>*>(dyn_smem);
+  uint32_t* ssum = reinterpret_cast<uint32_t*>(dyn_smem + sizeof(ResidualQ<Off>) * kBfsWarps);
   const unsigned warp = threadIdx.x >> 5;
   const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned long long gsize = (unsigned long long)gridDim.x * blockDim.x;
@@ -685,6 +819,11 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   // compute and no push can reach (they have no edges).
   for (unsigned long long w = gtid; w < a.nwords; w += gsize)
     a.vis0[w] = a.isolated[w] | ((w == (s >> 5)) ? (1u << (s & 31u)) : 0u);
+  {
+    const uint32_t gs = s >> a.sum_shift;
+    for (unsigned long long w = gtid; w < a.sum_words; w += gsize)
+      a.sumv[w] = (w == (gs >> 5)) ? (1u << (gs & 31u)) : 0u;
+  }
   if (blockIdx.x == 0) {
     for (int t = threadIdx.x; t < kRing * (int)(sizeof(LevelCtr) / 4); t += blockDim.x)
       reinterpret_cast<unsigned*>(a.ctr)[t] = 0u;
@@ -711,7 +850,8 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   const Off indeg_s = a.coff[s + 1] - a.coff[s];
   long long m_u = a.nnz - (long long)indeg_s;
   long long reached = 1;
-  Acc acc{0, 0, 0};
+  Acc acc{0, 0, 0, 0};
+  bool from_bits = false;  // next push reads the pull's frontier bitmap
   int d = 1;
   for (;; ++d) {
     LevelCtr* out = &a.ctr[d & (kRing - 1)];
@@ -720,11 +860,18 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
     uint32_t* vis = cur ? a.vis1 : a.vis0;
     uint32_t* vis_other = cur ? a.vis0 : a.vis1;
     if (dir == 0) {
-      push_phase<Off, PARENTS>(a, sel ? a.L1 : a.L0, nL, sel ? a.H1 : a.H0, nH,
+      push_phase<Off, PARENTS>(a, sel ? a.L1 : a.L0, from_bits ? 0u : nL, sel ? a.H1 : a.H0,
+                               from_bits ? 0u : nH, from_bits ? a.fr : nullptr,
                                sel ? a.L0 : a.L1, sel ? a.H0 : a.H1, out, vis, d + 1, acc,
                                &sh.work);
+      from_bits = false;
     } else {
-      pull_phase<Off, PARENTS>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp], &sh.work);
+      if (kSumWordsMax) {
+        for (unsigned t = threadIdx.x; t < a.sum_words; t += blockDim.x) ssum[t] = a.sumv[t];
+        __syncthreads();
+      }
+      pull_phase<Off, PARENTS>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp],
+                               ssum, &sh.work);
     }
     flush_acc(acc, out, sh.red);
     if (!grid_barrier(a.bar, a.status)) return;
@@ -749,8 +896,11 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
     if (c_new == 0 || d >= a.max_levels) break;
     int next = dir;
     if (a.mode == 0) next = decide(a.rule, dir, c_old, c_new, mf, m_u, a.n, a.alpha, a.beta);
-    if (dir == 1 && next == 0) {
-      // pull -> push: Dense2sparse of the frontier just discovered
+    if (dir == 1 && next == 0 && sh.lvl[5] == 0) {
+      from_bits = true;  // every new frontier vertex is light: push straight from `fr`
+    } else if (dir == 1 && next == 0) {
+      // pull -> push with a high-degree vertex in the frontier: Dense2sparse into the
+      // light list / heavy chunks so the hub's edges are split across warps
       uint32_t* vnew = cur ? a.vis1 : a.vis0;
       uint32_t* vold = cur ? a.vis0 : a.vis1;
       convert_phase<Off>(a, vnew, vold, sel ? a.L1 : a.L0, sel ? a.H1 : a.H0, out, &sh.work);
@@ -769,7 +919,9 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
 }
 
 template <typename Off>
-constexpr size_t dyn_smem_bytes() { return sizeof(ResidualQ<Off>) * kBfsWarps; }
+constexpr size_t dyn_smem_bytes() {
+  return sizeof(ResidualQ<Off>) * kBfsWarps + sizeof(uint32_t) * kSumWordsMax;
+}
 
 template <typename Off, bool PARENTS>
 static int grid_for() {
@@ -818,6 +970,11 @@ static cudaError_t launch_off(pp_graph g, uint32_t source, int mode, int rule, d
   a.isolated = g->isolated;
   a.vis0 = g->vis[0];
   a.vis1 = g->vis[1];
+  a.fr = g->fr;
+  a.sumv = g->sumv;
+  a.head = g->head;
+  a.sum_shift = g->sum_shift;
+  a.sum_words = g->sum_words;
   a.L0 = g->L[0];
   a.L1 = g->L[1];
   a.H0 = g->H[0];

@@ -70,7 +70,7 @@ bool is_device_ptr(const void* p) {
 void free_graph(pp_graph g) {
   if (!g) return;
   void* ptrs[] = {g->off, g->idx, g->symmetric ? nullptr : g->coff,
-                  g->symmetric ? nullptr : (void*)g->cidx, g->isolated, g->vis[0], g->vis[1],
+                  g->symmetric ? nullptr : (void*)g->cidx, g->isolated, g->head, g->vis[0], g->vis[1], g->fr, g->sumv,
                   g->L[0], g->L[1], g->H[0], g->H[1], g->ctr, g->stats, g->bar,
                   g->sbits[0], g->sbits[1], g->sbits[2], g->sbits[3], g->sblock, g->scount,
                   g->dtmp[0], g->dtmp[1]};
@@ -237,21 +237,27 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr
   }
 
   // narrowed offsets, isolated bitmap, heavy-chunk capacities
+  // offsets padded to nwords*32 + 16 entries: the pull kernel loads an item's 257
+  // offsets with aligned vector loads (padding rows are never candidates)
   const size_t offb = g->off64 ? 8 : 4;
+  const size_t noff = (size_t)g->nwords * 32 + 16;
   {
     void* p = nullptr;
-    PP_CK(cudaMalloc(&p, offb * (n + 1)), "offsets");
+    PP_CK(cudaMalloc(&p, offb * noff), "offsets");
+    PP_CK(cudaMemsetAsync(p, 0, offb * noff, st), "memset offsets");
     g->off = p;
-    bytes += (int64_t)(offb * (n + 1));
+    bytes += (int64_t)(offb * noff);
     if (symmetric) {
       g->coff = g->off;
     } else {
-      PP_CK(cudaMalloc(&p, offb * (n + 1)), "csc offsets");
+      PP_CK(cudaMalloc(&p, offb * noff), "csc offsets");
+      PP_CK(cudaMemsetAsync(p, 0, offb * noff, st), "memset csc offsets");
       g->coff = p;
-      bytes += (int64_t)(offb * (n + 1));
+      bytes += (int64_t)(offb * noff);
     }
   }
   if ((s = dalloc(&g->isolated, g->nwords, &bytes, "isolated")) != PP_OK) return s;
+  if ((s = dalloc(&g->head, (size_t)n, &bytes, "row heads")) != PP_OK) return s;
   PP_CK(cudaMemsetAsync(g->scount, 0, 2 * sizeof(unsigned long long), st), "memset");
   PP_CK(launch_graph_prepare(g, d_off64, d_coff64, g->scount, &ctx->launches), "prepare kernels");
   PP_CK(cudaMemcpyAsync(g->scount_host, g->scount, 16, cudaMemcpyDeviceToHost, st), "copy");
@@ -264,6 +270,13 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr
     if ((s = dalloc(&g->L[k], (size_t)n, &bytes, "frontier list")) != PP_OK) return s;
     if ((s = dalloc(&g->H[k], (size_t)g->hcap, &bytes, "heavy chunks")) != PP_OK) return s;
   }
+  if ((s = dalloc(&g->fr, g->nwords, &bytes, "frontier bitmap")) != PP_OK) return s;
+  // visited summary: group size 2^shift >= 8 vertices, at most kSumWordsMax words
+  g->sum_shift = 3;
+  while (((n + ((int64_t)1 << g->sum_shift) - 1) >> g->sum_shift) > (int64_t)std::max(kSumWordsMax, 1u) * 32)
+    ++g->sum_shift;
+  g->sum_words = (uint32_t)((((n + ((int64_t)1 << g->sum_shift) - 1) >> g->sum_shift) + 31) / 32);
+  if ((s = dalloc(&g->sumv, g->sum_words, &bytes, "visited summary")) != PP_OK) return s;
   if ((s = dalloc(&g->ctr, kRing, &bytes, "level counters")) != PP_OK) return s;
   g->stats_cap = (int)std::min<int64_t>(n + 1, 1 << 16);
   if ((s = dalloc(&g->stats, (size_t)g->stats_cap, &bytes, "level stats")) != PP_OK) return s;

@@ -27,6 +27,23 @@ __global__ void k_isolated(const int64_t* __restrict__ off, const int64_t* __res
   }
 }
 
+// Pull-side row heads: the first 4 in-neighbours of every row (CSC), 0xFFFFFFFF-padded.
+// A row-contiguous 16-byte record per vertex lets the pull decide most rows without a
+// scattered access into the id array (ELL head + CSR tail).
+__global__ void k_head(const int64_t* __restrict__ coff, const uint32_t* __restrict__ cidx,
+                       int64_t n, uint4* __restrict__ head) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = coff[v], d = coff[v + 1] - b;
+    uint4 h;
+    h.x = d > 0 ? cidx[b] : 0xFFFFFFFFu;
+    h.y = d > 1 ? cidx[b + 1] : 0xFFFFFFFFu;
+    h.z = d > 2 ? cidx[b + 2] : 0xFFFFFFFFu;
+    h.w = d > 3 ? cidx[b + 3] : 0xFFFFFFFFu;
+    head[v] = h;
+  }
+}
+
 // Heavy-chunk capacity: sum over rows with degree >= kHeavy of ceil(deg / kChunk).
 __global__ void k_hcap(const int64_t* __restrict__ off, int64_t n, unsigned long long* out) {
   unsigned long long c = 0;
@@ -82,7 +99,8 @@ cudaError_t launch_graph_prepare(pp_graph g, const int64_t* d_off64, const int64
       k_off_narrow<uint32_t><<<blocks, kBlock, 0, st>>>(d_coff64, (uint32_t*)g->coff, g->n + 1);
     }
   }
-  *launches += 3;
+  *launches += 4;
+  k_head<<<blocks, kBlock, 0, st>>>(d_coff64, g->cidx, g->n, g->head);
   k_isolated<<<blocks, kBlock, 0, st>>>(d_off64, d_coff64, g->n, g->nwords, g->isolated);
   k_hcap<<<blocks, kBlock, 0, st>>>(d_off64, g->n, d_scratch + 0);
   k_hcap<<<blocks, kBlock, 0, st>>>(d_coff64, g->n, d_scratch + 1);

@@ -15,7 +15,16 @@ constexpr int kWarps = kBlock / 32;
 constexpr unsigned kHeavy = 128;   // out-degree >= kHeavy: expanded as kChunk-edge chunks
 constexpr unsigned kChunk = 128;   // edges per heavy chunk = one 4-deep warp iteration
 constexpr int kRing = 4;           // level-counter ring
-constexpr int kBfsBlock = 1024;    // persistent BFS: one 1024-thread CTA per SM
+#ifndef PP_SUM_WORDS
+#define PP_SUM_WORDS 0
+#endif
+constexpr unsigned kSumWordsMax = PP_SUM_WORDS;  // visited summary words in shared memory (0 = off)
+constexpr unsigned kBig = 1024;    // pull->push goes straight from the bitmap if no new
+                                   // frontier vertex has out-degree >= kBig
+#ifndef PP_BFS_BLOCK
+#define PP_BFS_BLOCK 1024
+#endif
+constexpr int kBfsBlock = PP_BFS_BLOCK;  // persistent BFS: one CTA per SM
 constexpr int kBfsWarps = kBfsBlock / 32;
 
 // Per-level counters, written with atomics during a level, read after the grid barrier.
@@ -25,7 +34,8 @@ struct LevelCtr {
   unsigned long long m_fin;  // sum of their in-degrees (m_u update, directed graphs)
   unsigned int nL, nH;       // next frontier: light-list length, heavy-chunk count
   unsigned int work, work2;  // dynamic work counters (phase, convert phase)
-  unsigned int pad[6];
+  unsigned long long nbig;   // discoveries with out-degree >= kBig (pull levels)
+  unsigned int pad[4];
 };
 static_assert(sizeof(LevelCtr) == 64, "LevelCtr layout");
 
@@ -72,8 +82,13 @@ struct pp_graph_s {
   void* coff = nullptr;  // CSC (in-neighbours); aliases off when symmetric
   uint32_t* cidx = nullptr;
   uint32_t* isolated = nullptr;  // nwords: bit = no in- and no out-edges, or padding
+  uint4* head = nullptr;         // n: first 4 in-neighbours of every row (pull heads)
   // BFS working set
   uint32_t* vis[2] = {nullptr, nullptr};
+  uint32_t* fr = nullptr;  // frontier bitmap of the last pull level
+  uint32_t* sumv = nullptr;  // visited summary (1 bit per 2^sum_shift vertices)
+  int sum_shift = 3;
+  uint32_t sum_words = 0;
   uint32_t* L[2] = {nullptr, nullptr};
   uint2* H[2] = {nullptr, nullptr};
   int64_t hcap = 0;

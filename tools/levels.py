@@ -37,3 +37,13 @@ for s in synth.sources(g, nsrc, seed=2):
     else:
         ns = st["ns"][:min(L, 70000)]
         print(f"   per-level us: mean {ns.mean()/1e3:.2f} median {np.median(ns)/1e3:.2f} max {ns.max()/1e3:.1f}")
+
+# fixed per-level cost: BFS from an isolated vertex = init + one empty level
+iso = int(np.nonzero(np.diff(g.off) == 0)[0][0]) if np.any(np.diff(g.off) == 0) else None
+if iso is not None:
+    vals = []
+    for _ in range(20):
+        st = pp.bfs(G, iso, depth, heuristic=heur, stats_capacity=4)
+        vals.append((st["init_ns"], st["ns"][0]))
+    v = np.array(vals)
+    print(f"isolated source: init {np.median(v[:,0])/1e3:.2f} us, empty level {np.median(v[:,1])/1e3:.2f} us")
