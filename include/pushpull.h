@@ -186,6 +186,12 @@ typedef struct {
 pp_status pp_bfs(pp_graph g, int64_t source, const pp_bfs_options* opts, int32_t* depth,
                  int32_t* parent, pp_bfs_stats* stats);
 
+/* Diagnostics (load-balance evidence): the first call with levels > 0 makes every later
+ * pp_bfs on g record, for each of its first `levels` levels and each persistent CTA, the
+ * CTA's work time in that level's phase (ns, before the grid barrier).  A call with
+ * out_ns != NULL copies the last BFS's records (levels x *nctas, level-major) to host. */
+pp_status pp_bfs_debug_times(pp_graph g, int32_t levels, int64_t* out_ns, int32_t* nctas);
+
 #ifdef __cplusplus
 }
 #endif

@@ -91,6 +91,7 @@ _SIGS = {
     "pp_bfs_options_default": ([ctypes.POINTER(pp_bfs_options)], ctypes.c_int),
     "pp_bfs": ([_vp, _i64, ctypes.POINTER(pp_bfs_options), _vp, _vp,
                 ctypes.POINTER(pp_bfs_stats)], ctypes.c_int),
+    "pp_bfs_debug_times": ([_vp, ctypes.c_int32, _vp, ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -168,6 +169,18 @@ def pp_mxv(g, w: pp_vector, desc: pp_descriptor, u: pp_vector):
 def pp_bfs(g, source, opts, depth_ptr, parent_ptr, stats):
     _check(_lib.pp_bfs(g, int(source), None if opts is None else ctypes.byref(opts), depth_ptr,
                        parent_ptr, None if stats is None else ctypes.byref(stats)))
+
+
+def pp_bfs_debug_times(g, levels=0, fetch=False):
+    """Enable (levels > 0) or fetch per-level, per-CTA phase durations (ns)."""
+    nct = ctypes.c_int32()
+    if not fetch:
+        _check(_lib.pp_bfs_debug_times(g, levels, None, ctypes.byref(nct)))
+        return nct.value
+    _check(_lib.pp_bfs_debug_times(g, 0, None, ctypes.byref(nct)))
+    out = np.zeros(levels * nct.value, np.int64)
+    _check(_lib.pp_bfs_debug_times(g, 0, out.ctypes.data, ctypes.byref(nct)))
+    return out.reshape(levels, nct.value)
 
 
 # ---- conveniences (torch tensors as device memory) ----------------------------------------

@@ -60,40 +60,54 @@ struct BfsArgs {
   double alpha, beta;
   uint32_t toggles;
   int max_levels;
+  long long* dbg;  // optional: per level, per CTA work duration (ns) of the level's phase
+  int dbg_levels;
 };
 
 constexpr unsigned long long kWatchdogNs = 4000000000ull;  // 4 s per barrier wait
 
-// Software grid barrier (all CTAs co-resident: cooperative launch).  The gpu-scope
-// fences around the arrival/wait order every CTA's writes before the release and
-// invalidate this SM's L1 after the acquire, so post-barrier loads see them.
-__device__ __forceinline__ bool grid_barrier(GridBarrier* b, BfsStatus* st) {
+// Software grid barrier (all CTAs co-resident: cooperative launch).  One 64-bit counter
+// grows monotonically through the BFS: barrier number `epoch` is complete when it reaches
+// epoch * gridDim.  Arrival is a single atom.add.release.gpu (orders this CTA's prior
+// writes, published to thread 0 by __syncthreads), waiting is ld.acquire.gpu polling, and
+// a gpu-scope fence afterwards invalidates this SM's L1 so post-barrier loads see every
+// CTA's writes.  Bit 63 is the abort flag (watchdog), which releases every waiter.
+constexpr unsigned long long kAbortBit = 1ull << 63;
+
+__device__ __forceinline__ unsigned long long atom_add_release_u64(unsigned long long* p,
+                                                                   unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.add.release.gpu.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ bool grid_barrier(GridBarrier* b, BfsStatus* st, unsigned& epoch) {
   __shared__ int s_ok;
   __syncthreads();
   if (threadIdx.x == 0) {
-    int ok = 1;
-    const unsigned nblocks = gridDim.x;
-    unsigned g = ld_acquire_gpu(&b->gen);
-    __threadfence();
-    unsigned arrived = atomicAdd(&b->count, 1u);
-    if (arrived == nblocks - 1) {
-      atomicExch(&b->count, 0u);
-      __threadfence();
-      st_release_gpu(&b->gen, g + 1);
-    } else {
-      unsigned long long t0 = global_timer_ns();
-      while (ld_acquire_gpu(&b->gen) == g) {
-        __nanosleep(32);
+    ++epoch;
+    const unsigned long long target = (unsigned long long)epoch * gridDim.x;
+    unsigned long long* cnt = reinterpret_cast<unsigned long long*>(&b->count);
+    unsigned long long v = atom_add_release_u64(cnt, 1ull) + 1ull;
+    if (v < target) {
+      const unsigned long long t0 = global_timer_ns();
+      while ((v = ld_acquire_u64(cnt)) < target) {
+        __nanosleep(16);
         if (global_timer_ns() - t0 > kWatchdogNs) {
-          ok = 0;
           atomicExch(&st->error, (int)PP_ERR_TIMEOUT);
+          atomicOr(cnt, kAbortBit);
+          v = kAbortBit;
           break;
         }
       }
     }
     __threadfence();
-    if (ld_relaxed_s32(&st->error) != 0) ok = 0;
-    s_ok = ok;
+    s_ok = (v & kAbortBit) ? 0 : 1;
   }
   __syncthreads();
   return s_ok != 0;
@@ -118,20 +132,19 @@ __device__ __forceinline__ void flush_acc(Acc& acc, LevelCtr* out,
     red[warp][3] = big;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long tc = 0, tm = 0, ti = 0, tb = 0;
-    for (int k = 0; k < kBfsWarps; ++k) {
-      tc += red[k][0];
-      tm += red[k][1];
-      ti += red[k][2];
-      tb += red[k][3];
+  if (warp == 0) {  // warp 0 reduces the CTA's per-warp partials, lane 0 publishes
+    const unsigned l = lane_id();
+    const bool in = l < (unsigned)kBfsWarps;
+    unsigned long long tc = warp_sum(in ? red[l][0] : 0ull), tm = warp_sum(in ? red[l][1] : 0ull),
+                       ti = warp_sum(in ? red[l][2] : 0ull), tb = warp_sum(in ? red[l][3] : 0ull);
+    if (l == 0) {
+      if (tc) {
+        atomicAdd(&out->c, tc);
+        atomicAdd(&out->m_f, tm);
+        atomicAdd(&out->m_fin, ti);
+      }
+      if (tb) atomicAdd(&out->nbig, tb);
     }
-    if (tc) {
-      atomicAdd(&out->c, tc);
-      atomicAdd(&out->m_f, tm);
-      atomicAdd(&out->m_fin, ti);
-    }
-    if (tb) atomicAdd(&out->nbig, tb);
   }
   acc.c = acc.mf = acc.mfin = acc.big = 0;
 }
@@ -147,6 +160,8 @@ __device__ __forceinline__ unsigned cta_grab(unsigned* sctr) {
   return blockIdx.x + j * gridDim.x;
 }
 __device__ __forceinline__ unsigned nwarps() { return gridDim.x * kBfsWarps; }
+
+constexpr unsigned kSelfChunks = 64;  // hubs with more chunks are emitted warp-cooperatively
 
 // Append newly discovered vertex v (valid lanes) to the next frontier: light list if
 // 0 < deg < kHeavy, else ceil(deg/kChunk) heavy chunks.  Warp-collective.
@@ -172,8 +187,10 @@ __device__ __forceinline__ void append_frontier(bool valid, uint32_t v, Off deg,
     unsigned base = 0;
     if (lane == 0) base = atomicAdd(&out->nH, tot);
     base = __shfl_sync(kFull, base, 0);
-    unsigned hb = hm;
-    while (hb) {  // vertex by vertex, 32 descriptors per step
+    if (nch <= kSelfChunks)
+      for (unsigned k = 0; k < nch; ++k) Hout[base + excl + k] = make_uint2(v, k);
+    unsigned hb = __ballot_sync(kFull, nch > kSelfChunks);
+    while (hb) {  // hubs: vertex by vertex, 32 descriptors per step
       const unsigned l = __ffs(hb) - 1;
       hb &= hb - 1;
       const uint32_t vl = __shfl_sync(kFull, v, l);
@@ -216,21 +233,32 @@ __device__ __forceinline__ void append_frontier4(const bool (&disc)[kU], const u
     const unsigned tot = __shfl_sync(kFull, incl, 31);
     unsigned base = 0;
     if (lane == 0) base = atomicAdd(&out->nH, tot);
-    unsigned start = __shfl_sync(kFull, base, 0) + incl - hsum;
+    const unsigned start0 = __shfl_sync(kFull, base, 0) + incl - hsum;
+    // Lanes write their own descriptors (all lanes in parallel); vertices with more than
+    // kSelfChunks chunks (hubs) are then written warp-cooperatively, 32 per step.
+    unsigned start = start0;
+    unsigned nch[kU];
 #pragma unroll
     for (int t = 0; t < kU; ++t) {
-      const unsigned nch = (disc[t] && deg[t] >= (Off)kHeavy)
-                               ? (unsigned)((deg[t] + (Off)kChunk - 1) / (Off)kChunk) : 0u;
-      unsigned hb = __ballot_sync(kFull, nch != 0);
+      nch[t] = (disc[t] && deg[t] >= (Off)kHeavy)
+                   ? (unsigned)((deg[t] + (Off)kChunk - 1) / (Off)kChunk) : 0u;
+      if (nch[t] <= kSelfChunks)
+        for (unsigned k = 0; k < nch[t]; ++k) Hout[start + k] = make_uint2(w[t], k);
+      start += nch[t];
+    }
+    start = start0;
+#pragma unroll
+    for (int t = 0; t < kU; ++t) {
+      unsigned hb = __ballot_sync(kFull, nch[t] > kSelfChunks);
       while (hb) {
         const unsigned l = __ffs(hb) - 1;
         hb &= hb - 1;
         const uint32_t v = __shfl_sync(kFull, w[t], l);
-        const unsigned n = __shfl_sync(kFull, nch, l);
+        const unsigned n = __shfl_sync(kFull, nch[t], l);
         const unsigned st = __shfl_sync(kFull, start, l);
         for (unsigned c = lane; c < n; c += 32) Hout[st + c] = make_uint2(v, c);
       }
-      start += nch;
+      start += nch[t];
     }
   }
 }
@@ -322,7 +350,10 @@ __device__ __forceinline__ void push_round(const BfsArgs<Off>& a, uint32_t v, Of
   }
 }
 
-constexpr unsigned kPW = 8;  // bitmap words per warp item (256 rows) for bitmap sweeps
+#ifndef PP_PULL_WORDS
+#define PP_PULL_WORDS 8
+#endif
+constexpr unsigned kPW = PP_PULL_WORDS;  // bitmap words per warp item (32*kPW rows)
 
 // Column-based masked mxv over the frontier (Alg. 3 re-designed).  The frontier is
 // either (list mode) a light list + heavy chunks, or (bitmap mode, right after a pull
@@ -395,7 +426,10 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint32_t* Lin, unsigned 
   }
 }
 
-constexpr int kC = 2;         // candidates in flight per lane
+#ifndef PP_PULL_KC
+#define PP_PULL_KC 2
+#endif
+constexpr int kC = PP_PULL_KC;  // candidates in flight per lane
 constexpr int kLaneMax = 16;    // residual rows with <= this many ids left: one lane each
 constexpr int kGroupMax = 512;   // <= this many: 8-lane groups; longer: the whole warp
 constexpr int kQ = 96;        // residual-queue entries per warp (31 + 32*kC fits)
@@ -809,6 +843,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   const unsigned long long gsize = (unsigned long long)gridDim.x * blockDim.x;
   const uint32_t s = a.source;
   if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t_start = (long long)global_timer_ns();
+  unsigned epoch = 0;  // grid barriers passed (thread 0)
 
   // ---- Alg. 1 lines 2-4: d <- 1, f <- e_s, v <- 0 (depth 0 = unvisited) ----
   for (unsigned long long v = gtid; v < (unsigned long long)a.n; v += gsize) {
@@ -838,7 +873,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       a.ctr[0].nL = 1;
     }
   }
-  if (!grid_barrier(a.bar, a.status)) return;
+  if (!grid_barrier(a.bar, a.status, epoch)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t_init = (long long)global_timer_ns();
   read_level(&a.ctr[0], sh);
   unsigned nL = (unsigned)sh.lvl[3], nH = (unsigned)sh.lvl[4];
@@ -854,6 +889,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   bool from_bits = false;  // next push reads the pull's frontier bitmap
   int d = 1;
   for (;; ++d) {
+    const long long t_lvl = (a.dbg && threadIdx.x == 0) ? (long long)global_timer_ns() : 0;
     LevelCtr* out = &a.ctr[d & (kRing - 1)];
     if (blockIdx.x == 0 && threadIdx.x < sizeof(LevelCtr) / 4)
       reinterpret_cast<unsigned*>(&a.ctr[(d + 1) & (kRing - 1)])[threadIdx.x] = 0u;
@@ -874,7 +910,9 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
                                ssum, &sh.work);
     }
     flush_acc(acc, out, sh.red);
-    if (!grid_barrier(a.bar, a.status)) return;
+    if (a.dbg && threadIdx.x == 0 && d - 1 < a.dbg_levels)
+      a.dbg[(size_t)(d - 1) * gridDim.x + blockIdx.x] = (long long)global_timer_ns() - t_lvl;
+    if (!grid_barrier(a.bar, a.status, epoch)) return;
     read_level(out, sh);
     const long long c_new = sh.lvl[0], mf = sh.lvl[1], mfin = sh.lvl[2];
     nL = (unsigned)sh.lvl[3];
@@ -904,7 +942,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       uint32_t* vnew = cur ? a.vis1 : a.vis0;
       uint32_t* vold = cur ? a.vis0 : a.vis1;
       convert_phase<Off>(a, vnew, vold, sel ? a.L1 : a.L0, sel ? a.H1 : a.H0, out, &sh.work);
-      if (!grid_barrier(a.bar, a.status)) return;
+      if (!grid_barrier(a.bar, a.status, epoch)) return;
       read_level(out, sh);
       nL = (unsigned)sh.lvl[3];
       nH = (unsigned)sh.lvl[4];
@@ -993,6 +1031,8 @@ static cudaError_t launch_off(pp_graph g, uint32_t source, int mode, int rule, d
   a.beta = beta;
   a.toggles = toggles;
   a.max_levels = max_levels;
+  a.dbg = g->dbg;
+  a.dbg_levels = g->dbg_levels;
   if (parent) return launch_t<Off, true>(g, a);
   return launch_t<Off, false>(g, a);
 }

@@ -73,7 +73,7 @@ void free_graph(pp_graph g) {
                   g->symmetric ? nullptr : (void*)g->cidx, g->isolated, g->head, g->vis[0], g->vis[1], g->fr, g->sumv,
                   g->L[0], g->L[1], g->H[0], g->H[1], g->ctr, g->stats, g->bar,
                   g->sbits[0], g->sbits[1], g->sbits[2], g->sbits[3], g->sblock, g->scount,
-                  g->dtmp[0], g->dtmp[1]};
+                  g->dtmp[0], g->dtmp[1], g->dbg};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (g->status_host) cudaFreeHost(g->status_host);
@@ -528,6 +528,25 @@ pp_status pp_bfs(pp_graph g, int64_t source, const pp_bfs_options* opts, int32_t
       }
       delete[] hs;
     }
+  }
+  return PP_OK;
+}
+
+pp_status pp_bfs_debug_times(pp_graph g, int32_t levels, int64_t* out_ns, int32_t* nctas) {
+  if (!g) PP_FAIL(PP_ERR_ARG, "pp_bfs_debug_times: NULL graph");
+  PP_CK(cudaSetDevice(g->ctx->device), "cudaSetDevice");
+  if (nctas) *nctas = g->bfs_grid;
+  if (levels > 0 && !g->dbg) {
+    pp_status s = dalloc(&g->dbg, (size_t)levels * g->bfs_grid, &g->device_bytes, "debug times");
+    if (s != PP_OK) return s;
+    PP_CK(cudaMemset(g->dbg, 0, sizeof(long long) * (size_t)levels * g->bfs_grid), "memset");
+    g->dbg_levels = levels;
+    return PP_OK;
+  }
+  if (out_ns && g->dbg) {
+    PP_CK(cudaStreamSynchronize(g->ctx->stream), "sync");
+    PP_CK(cudaMemcpy(out_ns, g->dbg, sizeof(long long) * (size_t)g->dbg_levels * g->bfs_grid,
+                     cudaMemcpyDeviceToHost), "copy debug times");
   }
   return PP_OK;
 }

@@ -47,8 +47,8 @@ struct LevelStat {
 };
 
 struct GridBarrier {
-  unsigned int count;
-  unsigned int pad0[31];
+  unsigned long long count;  // monotone arrival counter (bit 63: abort), zeroed per launch
+  unsigned int pad0[30];
   unsigned int gen;
   unsigned int pad1[31];
 };
@@ -105,6 +105,8 @@ struct pp_graph_s {
   unsigned long long* scount_host = nullptr;
   int64_t* dtmp[2] = {nullptr, nullptr};  // upload staging / host-output staging
   int bfs_grid = 0;
+  long long* dbg = nullptr;  // pp_bfs_debug_times: per level x CTA phase durations
+  int dbg_levels = 0;
   int64_t device_bytes = 0;
 };
 
