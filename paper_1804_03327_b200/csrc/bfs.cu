@@ -39,12 +39,12 @@ struct BfsArgs {
   uint32_t* vis0;
   uint32_t* vis1;
   uint32_t* fr;  // frontier bitmap written by pull levels (push-from-bitmap)
-  const uint4* __restrict__ head;  // first 4 in-neighbours of every row (pull), kNoId padded
+  const uint32_t* __restrict__ head;  // first 8 in-neighbours of every row (pull), 32 B each
   uint32_t* sumv;      // visited summary: bit per 2^sum_shift vertices, isolated excluded
   int sum_shift;
   uint32_t sum_words;
-  uint32_t* L0;
-  uint32_t* L1;
+  uint4* L0;  // light frontier entries {v, deg, begin_lo, begin_hi}
+  uint4* L1;
   uint2* H0;
   uint2* H1;
   int32_t* depth;
@@ -163,10 +163,22 @@ __device__ __forceinline__ unsigned nwarps() { return gridDim.x * kBfsWarps; }
 
 constexpr unsigned kSelfChunks = 64;  // hubs with more chunks are emitted warp-cooperatively
 
+// Light frontier entry: the discovering thread already loaded the row's offsets, so the
+// next push reads {v, deg, begin} in one 16-byte load instead of a list load followed by
+// a dependent offsets load.
+template <typename Off>
+__device__ __forceinline__ uint4 light_entry(uint32_t v, Off deg, Off begin) {
+  return make_uint4(v, (uint32_t)deg, (uint32_t)begin, (uint32_t)((unsigned long long)begin >> 32));
+}
+template <typename Off>
+__device__ __forceinline__ Off light_begin(const uint4& e) {
+  return (Off)(((unsigned long long)e.w << 32) | e.z);
+}
+
 // Append newly discovered vertex v (valid lanes) to the next frontier: light list if
 // 0 < deg < kHeavy, else ceil(deg/kChunk) heavy chunks.  Warp-collective.
 template <typename Off>
-__device__ __forceinline__ void append_frontier(bool valid, uint32_t v, Off deg, uint32_t* Lout,
+__device__ __forceinline__ void append_frontier(bool valid, uint32_t v, Off deg, Off begin, uint4* Lout,
                                                 uint2* Hout, LevelCtr* out) {
   const unsigned lane = lane_id();
   bool heavy = valid && deg >= (Off)kHeavy;
@@ -176,7 +188,7 @@ __device__ __forceinline__ void append_frontier(bool valid, uint32_t v, Off deg,
     unsigned leader = __ffs(lm) - 1, base = 0;
     if (lane == leader) base = atomicAdd(&out->nL, (unsigned)__popc(lm));
     base = __shfl_sync(kFull, base, leader);
-    if (light) Lout[base + __popc(lm & lanemask_lt())] = v;
+    if (light) Lout[base + __popc(lm & lanemask_lt())] = light_entry<Off>(v, deg, begin);
   }
   unsigned hm = __ballot_sync(kFull, heavy);
   if (hm) {
@@ -206,7 +218,8 @@ constexpr int kU = 4;  // edges (push) in flight per lane
 // The same for kU candidates per lane, with one atomic per list per warp.
 template <typename Off>
 __device__ __forceinline__ void append_frontier4(const bool (&disc)[kU], const uint32_t (&w)[kU],
-                                                 const Off (&deg)[kU], uint32_t* Lout, uint2* Hout,
+                                                 const Off (&deg)[kU], const Off (&beg)[kU],
+                                                 uint4* Lout, uint2* Hout,
                                                  LevelCtr* out) {
   const unsigned lane = lane_id();
   unsigned lm[kU], ltot = 0, hsum = 0;
@@ -223,7 +236,8 @@ __device__ __forceinline__ void append_frontier4(const bool (&disc)[kU], const u
     base = __shfl_sync(kFull, base, 0);
 #pragma unroll
     for (int t = 0; t < kU; ++t) {
-      if ((lm[t] >> lane) & 1u) Lout[base + __popc(lm[t] & lanemask_lt())] = w[t];
+      if ((lm[t] >> lane) & 1u)
+        Lout[base + __popc(lm[t] & lanemask_lt())] = light_entry<Off>(w[t], deg[t], beg[t]);
       base += __popc(lm[t]);
     }
   }
@@ -270,7 +284,7 @@ __device__ __forceinline__ void append_frontier4(const bool (&disc)[kU], const u
 template <typename Off, bool PARENTS>
 __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&valid)[kU],
                                             const uint32_t (&u)[kU], const uint32_t (&w)[kU],
-                                            uint32_t* vis, int newdepth, uint32_t* Lout,
+                                            uint32_t* vis, int newdepth, uint4* Lout,
                                             uint2* Hout, LevelCtr* out, Acc& acc) {
   uint32_t cur[kU];
   bool disc[kU];
@@ -308,26 +322,28 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
     }
   }
   if (!__any_sync(kFull, disc[0] || disc[1] || disc[2] || disc[3])) return;
-  Off deg[kU];
+  Off deg[kU], beg[kU];
 #pragma unroll
   for (int t = 0; t < kU; ++t) {
     deg[t] = 0;
+    beg[t] = 0;
     if (disc[t]) {
-      deg[t] = a.off[w[t] + 1] - a.off[w[t]];
+      beg[t] = a.off[w[t]];
+      deg[t] = a.off[w[t] + 1] - beg[t];
       const Off degin = a.symmetric ? deg[t] : (Off)(a.coff[w[t] + 1] - a.coff[w[t]]);
       acc.c += 1;
       acc.mf += (unsigned long long)deg[t];
       acc.mfin += (unsigned long long)degin;
     }
   }
-  append_frontier4<Off>(disc, w, deg, Lout, Hout, out);
+  append_frontier4<Off>(disc, w, deg, beg, Lout, Hout, out);
 }
 
 // Edges of up to 32 light frontier vertices (lane l holds v, row begin b, degree deg),
 // balanced over lanes by a warp scan of the degrees, kU edges in flight per lane.
 template <typename Off, bool PARENTS>
 __device__ __forceinline__ void push_round(const BfsArgs<Off>& a, uint32_t v, Off b, unsigned deg,
-                                           uint32_t* Lout, uint2* Hout, LevelCtr* out,
+                                           uint4* Lout, uint2* Hout, LevelCtr* out,
                                            uint32_t* vis, int newdepth, Acc& acc) {
   const unsigned lane = lane_id();
   const unsigned incl = warp_incl_scan(deg);
@@ -351,7 +367,7 @@ __device__ __forceinline__ void push_round(const BfsArgs<Off>& a, uint32_t v, Of
 }
 
 #ifndef PP_PULL_WORDS
-#define PP_PULL_WORDS 8
+#define PP_PULL_WORDS 32
 #endif
 constexpr unsigned kPW = PP_PULL_WORDS;  // bitmap words per warp item (32*kPW rows)
 
@@ -363,8 +379,8 @@ constexpr unsigned kPW = PP_PULL_WORDS;  // bitmap words per warp item (32*kPW r
 // round = R frontier vertices (R = 32, or fewer when the frontier is too small to occupy
 // every warp), their edges balanced over lanes by a warp scan of degrees.
 template <typename Off, bool PARENTS>
-__device__ void push_phase(const BfsArgs<Off>& a, const uint32_t* Lin, unsigned nL,
-                           const uint2* Hin, unsigned nH, const uint32_t* fr, uint32_t* Lout,
+__device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
+                           const uint2* Hin, unsigned nH, const uint32_t* fr, uint4* Lout,
                            uint2* Hout, LevelCtr* out, uint32_t* vis, int newdepth, Acc& acc,
                            unsigned* sctr) {
   const unsigned lane = lane_id();
@@ -395,9 +411,10 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint32_t* Lin, unsigned 
       Off b = 0;
       unsigned deg = 0;
       if (lane < R && i < nL) {
-        v = Lin[i];
-        b = a.off[v];
-        deg = (unsigned)(a.off[v + 1] - b);
+        const uint4 le = Lin[i];
+        v = le.x;
+        deg = le.y;
+        b = light_begin<Off>(le);
       }
       push_round<Off, PARENTS>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc);
     } else {
@@ -427,7 +444,7 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint32_t* Lin, unsigned 
 }
 
 #ifndef PP_PULL_KC
-#define PP_PULL_KC 2
+#define PP_PULL_KC 1
 #endif
 constexpr int kC = PP_PULL_KC;  // candidates in flight per lane
 constexpr int kLaneMax = 16;    // residual rows with <= this many ids left: one lane each
@@ -708,39 +725,42 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
         par[t] = kNone;
         rb[t] = e[t] = 0;
       }
-      // stage: offsets and the row's head (first 4 in-neighbours, one 16-byte load from a
-      // row-contiguous array: dense items stream it), all in flight
-      uint4 hd[kC];
+      // stage: offsets and the row's head (first 8 in-neighbours = one 32-byte sector, one
+      // 256-bit load from a row-contiguous array: dense items stream it), all in flight
+      V8 hd[kC];
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
         if (valid[t]) {
           rb[t] = a.coff[i[t]];
           e[t] = a.coff[i[t] + 1];
-          hd[t] = __ldg(a.head + i[t]);
+          hd[t] = ld_nc_v8(a.head + (size_t)i[t] * 8u);
         }
       }
       // stage: probe the first neighbour, then the other head ids of rows that missed
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
         const Off deg = e[t] - rb[t];
-        if (valid[t] && deg > 0 && C.hit(hd[t].x)) {
+        if (valid[t] && deg > 0 && C.hit(hd[t].x[0])) {
           found[t] = true;
-          par[t] = hd[t].x;
+          par[t] = hd[t].x[0];
         }
       }
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
         const Off deg = e[t] - rb[t];
         if (valid[t] && deg > 1 && !(found[t] && C.early_exit)) {
-          const bool h1 = C.hit(hd[t].y);
-          const bool h2 = deg > 2 && C.hit(hd[t].z);
-          const bool h3 = deg > 3 && C.hit(hd[t].w);
-          if (!found[t] && (h1 || h2 || h3)) {
-            found[t] = true;
-            par[t] = h1 ? hd[t].y : h2 ? hd[t].z : hd[t].w;
+          bool h[8];
+#pragma unroll
+          for (int q = 1; q < 8; ++q) h[q] = deg > (Off)q && C.hit(hd[t].x[q]);
+#pragma unroll
+          for (int q = 1; q < 8; ++q) {
+            if (h[q] && !found[t]) {
+              found[t] = true;
+              par[t] = hd[t].x[q];
+            }
           }
         }
-        p[t] = (valid[t] && deg > 4) ? rb[t] + 4 : e[t];  // the tail continues in idx
+        p[t] = (valid[t] && deg > 8) ? rb[t] + 8 : e[t];  // the tail continues in idx
       }
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
@@ -775,7 +795,7 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
 // Dense2sparse of the new frontier v' & !v after a pull level (pull->push switch).
 template <typename Off>
 __device__ void convert_phase(const BfsArgs<Off>& a, const uint32_t* vnew, const uint32_t* vold,
-                              uint32_t* Lout, uint2* Hout, LevelCtr* out, unsigned* sctr) {
+                              uint4* Lout, uint2* Hout, LevelCtr* out, unsigned* sctr) {
   const unsigned lane = lane_id();
   const unsigned nchunks = a.nwords / 32u;
   for (unsigned item = cta_grab(sctr); item < nchunks; item = cta_grab(sctr)) {
@@ -784,14 +804,15 @@ __device__ void convert_phase(const BfsArgs<Off>& a, const uint32_t* vnew, const
     while (__ballot_sync(kFull, diff != 0u)) {
       const bool valid = diff != 0u;
       uint32_t v = 0;
-      Off deg = 0;
+      Off deg = 0, beg = 0;
       if (valid) {
         const unsigned b = __ffs(diff) - 1;
         diff &= diff - 1;
         v = w * 32u + b;
-        deg = a.off[v + 1] - a.off[v];
+        beg = a.off[v];
+        deg = a.off[v + 1] - beg;
       }
-      append_frontier<Off>(valid, v, deg, Lout, Hout, out);
+      append_frontier<Off>(valid, v, deg, beg, Lout, Hout, out);
     }
   }
 }
@@ -869,7 +890,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       for (unsigned k = threadIdx.x; k < nch; k += blockDim.x) a.H0[k] = make_uint2(s, k);
       if (threadIdx.x == 0) a.ctr[0].nH = nch;
     } else if (deg > 0 && threadIdx.x == 0) {
-      a.L0[0] = s;
+      a.L0[0] = light_entry<Off>(s, deg, a.off[s]);
       a.ctr[0].nL = 1;
     }
   }
@@ -1013,8 +1034,8 @@ static cudaError_t launch_off(pp_graph g, uint32_t source, int mode, int rule, d
   a.head = g->head;
   a.sum_shift = g->sum_shift;
   a.sum_words = g->sum_words;
-  a.L0 = g->L[0];
-  a.L1 = g->L[1];
+  a.L0 = reinterpret_cast<uint4*>(g->L[0]);
+  a.L1 = reinterpret_cast<uint4*>(g->L[1]);
   a.H0 = g->H[0];
   a.H1 = g->H[1];
   a.depth = depth;

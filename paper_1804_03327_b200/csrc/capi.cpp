@@ -257,7 +257,7 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr
     }
   }
   if ((s = dalloc(&g->isolated, g->nwords, &bytes, "isolated")) != PP_OK) return s;
-  if ((s = dalloc(&g->head, (size_t)n, &bytes, "row heads")) != PP_OK) return s;
+  if ((s = dalloc(&g->head, (size_t)n * 8, &bytes, "row heads")) != PP_OK) return s;
   PP_CK(cudaMemsetAsync(g->scount, 0, 2 * sizeof(unsigned long long), st), "memset");
   PP_CK(launch_graph_prepare(g, d_off64, d_coff64, g->scount, &ctx->launches), "prepare kernels");
   PP_CK(cudaMemcpyAsync(g->scount_host, g->scount, 16, cudaMemcpyDeviceToHost, st), "copy");
@@ -267,7 +267,8 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr
   // BFS / mxv working set
   for (int k = 0; k < 2; ++k) {
     if ((s = dalloc(&g->vis[k], g->nwords, &bytes, "visited")) != PP_OK) return s;
-    if ((s = dalloc(&g->L[k], (size_t)n, &bytes, "frontier list")) != PP_OK) return s;
+    // 16-byte light entries {v, deg, begin} (BFS); mxv reuses it as a uint32 list
+    if ((s = dalloc(&g->L[k], (size_t)n * 4, &bytes, "frontier list")) != PP_OK) return s;
     if ((s = dalloc(&g->H[k], (size_t)g->hcap, &bytes, "heavy chunks")) != PP_OK) return s;
   }
   if ((s = dalloc(&g->fr, g->nwords, &bytes, "frontier bitmap")) != PP_OK) return s;

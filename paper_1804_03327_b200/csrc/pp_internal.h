@@ -82,7 +82,7 @@ struct pp_graph_s {
   void* coff = nullptr;  // CSC (in-neighbours); aliases off when symmetric
   uint32_t* cidx = nullptr;
   uint32_t* isolated = nullptr;  // nwords: bit = no in- and no out-edges, or padding
-  uint4* head = nullptr;         // n: first 4 in-neighbours of every row (pull heads)
+  uint32_t* head = nullptr;      // 8n: first 8 in-neighbours of every row (pull heads)
   // BFS working set
   uint32_t* vis[2] = {nullptr, nullptr};
   uint32_t* fr = nullptr;  // frontier bitmap of the last pull level
