@@ -192,6 +192,25 @@ pp_status pp_bfs(pp_graph g, int64_t source, const pp_bfs_options* opts, int32_t
  * out_ns != NULL copies the last BFS's records (levels x *nctas, level-major) to host. */
 pp_status pp_bfs_debug_times(pp_graph g, int32_t levels, int64_t* out_ns, int32_t* nctas);
 
+/* ---- multi-GPU: 1D row partition + per-level NCCL all-gather ----------
+ * One process per GPU.  pp_nccl_unique_id: rank 0 creates the 128-byte NCCL id and shares it
+ * (e.g. a torch.distributed broadcast); PP_ERR_NCCL if libnccl.so.2 cannot be loaded.
+ * pp_ctx_create_dist: context with an NCCL communicator of nranks ranks (collective).
+ * pp_partition: rank's block [row_lo, row_hi): contiguous, 1024-vertex aligned, blocks of
+ * ceil(ceil(n/32)/32/nranks)*1024 vertices (pure function, no GPU).
+ * In a dist ctx pp_graph_upload takes the FULL graph on every rank (it stays resident) and
+ * adds the rank's push ranges; pp_graph_partition returns the block.  pp_bfs is then
+ * collective: every rank passes the same source/options; depth/parent hold the rank's block
+ * slice (row_hi - row_lo entries, same conventions); stats are global and identical on all
+ * ranks.  Each level: push (global frontier, owned targets) or pull (owned rows), then one
+ * in-place ncclAllGather of the next-frontier bitmap slices, then a finish kernel.  Ablation
+ * toggles are single-GPU only (PP_ERR_UNSUPPORTED). */
+pp_status pp_nccl_unique_id(void* out128);
+pp_status pp_ctx_create_dist(int device, void* cuda_stream, const void* nccl_unique_id, int rank,
+                             int nranks, pp_ctx* out);
+pp_status pp_partition(int64_t n, int32_t rank, int32_t nranks, int64_t* row_lo, int64_t* row_hi);
+pp_status pp_graph_partition(pp_graph g, int64_t* row_lo, int64_t* row_hi);
+
 #ifdef __cplusplus
 }
 #endif

@@ -92,6 +92,12 @@ _SIGS = {
     "pp_bfs": ([_vp, _i64, ctypes.POINTER(pp_bfs_options), _vp, _vp,
                 ctypes.POINTER(pp_bfs_stats)], ctypes.c_int),
     "pp_bfs_debug_times": ([_vp, ctypes.c_int32, _vp, ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),
+    "pp_nccl_unique_id": ([_vp], ctypes.c_int),
+    "pp_ctx_create_dist": ([ctypes.c_int, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)],
+                           ctypes.c_int),
+    "pp_partition": ([_i64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
+                     ctypes.c_int),
+    "pp_graph_partition": ([_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)], ctypes.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -183,6 +189,32 @@ def pp_bfs_debug_times(g, levels=0, fetch=False):
     return out.reshape(levels, nct.value)
 
 
+def pp_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.pp_nccl_unique_id(buf))
+    return buf.raw
+
+
+def pp_ctx_create_dist(device: int, cuda_stream: int, nccl_id: bytes, rank: int, nranks: int):
+    assert len(nccl_id) == 128
+    out = _vp()
+    buf = ctypes.create_string_buffer(nccl_id, 128)
+    _check(_lib.pp_ctx_create_dist(device, cuda_stream, buf, rank, nranks, ctypes.byref(out)))
+    return out.value
+
+
+def pp_partition(n: int, rank: int, nranks: int):
+    lo, hi = _i64(), _i64()
+    _check(_lib.pp_partition(n, rank, nranks, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
+def pp_graph_partition(g):
+    lo, hi = _i64(), _i64()
+    _check(_lib.pp_graph_partition(g, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
 # ---- conveniences (torch tensors as device memory) ----------------------------------------
 
 def _ptr(x):
@@ -222,6 +254,20 @@ class Context:
             pass
 
 
+class DistContext(Context):
+    """Distributed context: one GPU per process, NCCL communicator built from an id that
+    rank 0 creates and torch.distributed broadcasts (plumbing only)."""
+
+    def __init__(self, device: int, rank: int, nranks: int, nccl_id: bytes, stream=None):
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.device = device
+        self.stream = stream
+        self.rank, self.nranks = rank, nranks
+        self.handle = pp_ctx_create_dist(device, stream.cuda_stream, nccl_id, rank, nranks)
+
+
 class Graph:
     """Device-resident graph (library-owned copy of CSR + CSC)."""
 
@@ -256,6 +302,9 @@ class Graph:
 
     def info(self):
         return pp_graph_info(self.handle)
+
+    def partition(self):
+        return pp_graph_partition(self.handle)
 
     def close(self):
         if self.handle:

@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libpushpull.so")
-SOURCES = ["bfs.cu", "mxv.cu", "graph.cu", "capi.cpp"]
+SOURCES = ["bfs.cu", "mxv.cu", "graph.cu", "dist.cu", "capi.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC,-O3", "-shared", "-cudart", "static", "-I", os.path.join(ROOT, "include"),
@@ -28,6 +28,7 @@ def build(force=False, verbose=False):
     tmp = SO + f".tmp{os.getpid()}"
     extra = [f"-D{k}={os.environ[k]}" for k in ("PP_BFS_BLOCK", "PP_SUM_WORDS", "PP_PULL_WORDS", "PP_PULL_KC") if os.environ.get(k)]
     extra += ["-DPP_IDX_NOALLOC"] if os.environ.get("PP_IDX_NOALLOC") else []
+    extra += ["-ldl"]
     cmd = [NVCC] + FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + \
         [os.path.join(CSRC, f) for f in SOURCES] + ["-o", tmp]
     subprocess.check_call(cmd)

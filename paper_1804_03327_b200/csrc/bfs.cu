@@ -451,7 +451,6 @@ constexpr int kLaneMax = 16;    // residual rows with <= this many ids left: one
 constexpr int kGroupMax = 512;   // <= this many: 8-lane groups; longer: the whole warp
 constexpr int kQ = 96;        // residual-queue entries per warp (31 + 32*kC fits)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
-constexpr unsigned kSoffStride = 264;  // per-warp shared copy of an item's 257 offsets
 
 // Rows whose first sector did not decide them, parked per warp in shared memory and
 // processed 32 at a time so no lane idles behind one long row.

@@ -73,11 +73,13 @@ void free_graph(pp_graph g) {
                   g->symmetric ? nullptr : (void*)g->cidx, g->isolated, g->head, g->vis[0], g->vis[1], g->fr, g->sumv,
                   g->L[0], g->L[1], g->H[0], g->H[1], g->ctr, g->stats, g->bar,
                   g->sbits[0], g->sbits[1], g->sbits[2], g->sbits[3], g->sblock, g->scount,
-                  g->dtmp[0], g->dtmp[1], g->dbg};
+                  g->dtmp[0], g->dtmp[1], g->dbg,
+                  g->dvis, g->dfr, g->dnxt, g->diso, g->pbeg, g->pend, g->dcnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (g->status_host) cudaFreeHost(g->status_host);
   if (g->scount_host) cudaFreeHost(g->scount_host);
+  if (g->dcnt_host) cudaFreeHost(g->dcnt_host);
   delete g;
 }
 
@@ -122,7 +124,45 @@ pp_status pp_ctx_create(int device, void* cuda_stream, pp_ctx* out) {
 }
 
 static void ctx_release(pp_ctx ctx) {
-  if (--ctx->refs == 0) delete ctx;
+  if (--ctx->refs == 0) {
+    if (ctx->comm) nccl_comm_destroy(ctx->comm);
+    delete ctx;
+  }
+}
+
+pp_status pp_nccl_unique_id(void* out128) {
+  if (!out128) PP_FAIL(PP_ERR_ARG, "pp_nccl_unique_id: NULL output");
+  const char* why = "";
+  if (nccl_unique_id(out128, &why) != 0) PP_FAIL(PP_ERR_NCCL, "pp_nccl_unique_id: %s", why);
+  return PP_OK;
+}
+
+pp_status pp_ctx_create_dist(int device, void* cuda_stream, const void* nccl_unique_id_,
+                             int rank, int nranks, pp_ctx* out) {
+  if (!out || !nccl_unique_id_) PP_FAIL(PP_ERR_ARG, "pp_ctx_create_dist: NULL argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    PP_FAIL(PP_ERR_ARG, "pp_ctx_create_dist: rank %d of %d", rank, nranks);
+  pp_status s = pp_ctx_create(device, cuda_stream, out);
+  if (s != PP_OK) return s;
+  const char* why = "";
+  void* comm = nullptr;
+  if (nccl_comm_init(&comm, nranks, nccl_unique_id_, rank, &why) != 0) {
+    delete *out;
+    *out = nullptr;
+    PP_FAIL(PP_ERR_NCCL, "pp_ctx_create_dist: ncclCommInitRank: %s", why);
+  }
+  (*out)->comm = comm;
+  (*out)->rank = rank;
+  (*out)->nranks = nranks;
+  return PP_OK;
+}
+
+pp_status pp_partition(int64_t n, int32_t rank, int32_t nranks, int64_t* row_lo, int64_t* row_hi) {
+  if (!row_lo || !row_hi || n < 1 || nranks < 1 || rank < 0 || rank >= nranks)
+    PP_FAIL(PP_ERR_ARG, "pp_partition: bad arguments");
+  int64_t cw;
+  partition(n, rank, nranks, row_lo, row_hi, &cw);
+  return PP_OK;
 }
 
 pp_status pp_ctx_destroy(pp_ctx ctx) {
@@ -293,6 +333,25 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr
     g->dtmp[0] = nullptr;
   }
   g->bfs_grid = bfs_grid_size(g, false);
+  if (ctx->nranks > 0) {  // distributed context: owned block, replicated bitmaps, push ranges
+    partition(n, ctx->rank, ctx->nranks, &g->row_lo, &g->row_hi, &g->chunk_words);
+    g->dist_words = g->chunk_words * ctx->nranks;
+    const size_t W = (size_t)g->dist_words;
+    if ((s = dalloc(&g->dvis, W, &bytes, "dist visited")) != PP_OK) return s;
+    if ((s = dalloc(&g->dfr, W, &bytes, "dist frontier")) != PP_OK) return s;
+    if ((s = dalloc(&g->dnxt, W, &bytes, "dist next")) != PP_OK) return s;
+    if ((s = dalloc(&g->diso, W, &bytes, "dist isolated")) != PP_OK) return s;
+    PP_CK(cudaMemsetAsync(g->diso, 0xFF, sizeof(uint32_t) * W, st), "memset");
+    PP_CK(cudaMemcpyAsync(g->diso, g->isolated, sizeof(uint32_t) * std::min<size_t>(W, g->nwords),
+                          cudaMemcpyDeviceToDevice, st), "copy isolated");
+    PP_CK(cudaMalloc(&g->pbeg, offb * (size_t)n), "push ranges");
+    PP_CK(cudaMalloc(&g->pend, offb * (size_t)n), "push ranges");
+    bytes += (int64_t)(2 * offb * (size_t)n);
+    if ((s = dalloc(&g->dcnt, 4, &bytes, "dist counters")) != PP_OK) return s;
+    PP_CK(cudaMallocHost((void**)&g->dcnt_host, 4 * sizeof(unsigned long long)), "pinned");
+    PP_CK(launch_push_ranges(g), "push ranges kernel");
+    PP_CK(cudaStreamSynchronize(st), "sync");
+  }
   guard.g = nullptr;
   ctx->refs += 1;
   *out = g;
@@ -306,6 +365,13 @@ pp_status pp_graph_free(pp_graph g) {
   cudaStreamSynchronize(ctx->stream);
   free_graph(g);
   ctx_release(ctx);
+  return PP_OK;
+}
+
+pp_status pp_graph_partition(pp_graph g, int64_t* row_lo, int64_t* row_hi) {
+  if (!g || !row_lo || !row_hi) PP_FAIL(PP_ERR_ARG, "pp_graph_partition: NULL argument");
+  *row_lo = g->ctx->nranks ? g->row_lo : 0;
+  *row_hi = g->ctx->nranks ? g->row_hi : g->n;
   return PP_OK;
 }
 
@@ -491,6 +557,41 @@ pp_status pp_bfs(pp_graph g, int64_t source, const pp_bfs_options* opts, int32_t
     if (!g->dtmp[1] && (s = dalloc(&g->dtmp[1], (size_t)(g->n + 1) / 2 + 1, &g->device_bytes, "parent staging")) != PP_OK)
       return s;
     d_parent = (uint32_t*)g->dtmp[1];
+  }
+  if (g->ctx->nranks > 0 && o.toggles)
+    PP_FAIL(PP_ERR_UNSUPPORTED, "pp_bfs: ablation toggles are single-GPU only");
+  if (g->ctx->nranks > 0) {  // collective 1D-partitioned BFS; depth/parent are block slices
+    const int cap = stats ? std::max(stats->capacity, 0) : 0;
+    DistLevel* lv = cap ? new DistLevel[cap] : nullptr;
+    int nlev = 0;
+    long long reached = 0;
+    const char* why = "";
+    const int rc = launch_bfs_dist(g, (uint32_t)source, o.mode, o.heuristic, alpha, beta, d_depth,
+                                   d_parent, lv, cap, &nlev, &reached, &why);
+    if (rc != 0) {
+      delete[] lv;
+      PP_FAIL(rc == -2 ? PP_ERR_NCCL : PP_ERR_CUDA, "pp_bfs (distributed): %s", why);
+    }
+    const int64_t len = g->row_hi - g->row_lo;
+    if (host_depth && len)
+      PP_CK(cudaMemcpyAsync(depth, d_depth, sizeof(int32_t) * len, cudaMemcpyDeviceToHost, st), "copy");
+    if (host_parent && len)
+      PP_CK(cudaMemcpyAsync(parent, d_parent, sizeof(int32_t) * len, cudaMemcpyDeviceToHost, st), "copy");
+    PP_CK(cudaStreamSynchronize(st), "sync");
+    if (stats) {
+      stats->levels = nlev;
+      stats->reached = reached;
+      stats->init_ns = 0;
+      for (int k = 0; k < std::min(cap, nlev); ++k) {
+        if (stats->dir) stats->dir[k] = (int8_t)lv[k].dir;
+        if (stats->c) stats->c[k] = lv[k].c;
+        if (stats->m_f) stats->m_f[k] = lv[k].m_f;
+        if (stats->m_u) stats->m_u[k] = lv[k].m_u;
+        if (stats->ns) stats->ns[k] = 0;
+      }
+    }
+    delete[] lv;
+    return PP_OK;
   }
   PP_CK(cudaMemsetAsync(g->bar, 0, sizeof(GridBarrier) + sizeof(BfsStatus), st), "memset control");
   const int max_levels = (int)std::min<int64_t>(g->n + 1, 0x7FFFFFFF);

@@ -69,6 +69,8 @@ struct pp_ctx_s {
   int num_sms = 0;
   uint64_t launches = 0;
   int refs = 1;  // the caller's handle + one per live graph
+  int rank = 0, nranks = 0;  // nranks > 0: distributed context (NCCL communicator)
+  void* comm = nullptr;
 };
 
 struct pp_graph_s {
@@ -108,6 +110,12 @@ struct pp_graph_s {
   long long* dbg = nullptr;  // pp_bfs_debug_times: per level x CTA phase durations
   int dbg_levels = 0;
   int64_t device_bytes = 0;
+  // distributed (1D row partition): owned block, replicated bitmaps, push ranges
+  int64_t row_lo = 0, row_hi = 0, chunk_words = 0, dist_words = 0;
+  uint32_t *dvis = nullptr, *dfr = nullptr, *dnxt = nullptr, *diso = nullptr;
+  void *pbeg = nullptr, *pend = nullptr;
+  unsigned long long* dcnt = nullptr;
+  unsigned long long* dcnt_host = nullptr;
 };
 
 namespace pp {
@@ -140,4 +148,19 @@ cudaError_t launch_mxv(pp_graph g, const MxvPlan& p);
 cudaError_t launch_popcount(pp_graph g, const uint32_t* bits, unsigned long long* d_out);
 cudaError_t launch_bitmap_to_list(pp_graph g, const uint32_t* bits, uint32_t* list,
                                   int64_t capacity, unsigned long long* d_count);
+
+// dist.cu
+struct DistLevel {
+  int dir;
+  long long c, m_f, m_u;
+};
+bool nccl_load(const char** why);
+int nccl_unique_id(void* out128, const char** why);
+int nccl_comm_init(void** comm, int nranks, const void* id128, int rank, const char** why);
+void nccl_comm_destroy(void* comm);
+void partition(int64_t n, int rank, int nranks, int64_t* lo, int64_t* hi, int64_t* chunk_words);
+cudaError_t launch_push_ranges(pp_graph g);
+int launch_bfs_dist(pp_graph g, uint32_t source, int mode, int rule, double alpha, double beta,
+                    int32_t* depth, uint32_t* parent, DistLevel* levels, int cap, int* nlevels,
+                    long long* reached, const char** why);
 }  // namespace pp
