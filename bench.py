@@ -8,9 +8,11 @@ TEPS follows the paper: nnz(A) / BFS time.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
 
-N > 1 (torchrun): one process per GPU, each rank traverses its own sources on its own
-replica of the graph ("replicas only" / weak scaling), no data-path
-collective; timing is the max over ranks.  --impl reference times the CPU oracle
+N > 1 (torchrun): one process per GPU.  Default --mode replicas: each rank traverses its
+own sources on its own replica of the graph (independent problems, weak scaling, no
+data-path collective).  --mode partitioned: one BFS at a time over the 1D row partition
+(pp_ctx_create_dist; per-level ncclAllGather of the next-frontier bitmap), strong scaling.
+Timing is the max over ranks.  --impl reference times the CPU oracle
 (queue BFS, 1 core) on the same graph, sources, metric and unit.
 """
 from __future__ import annotations
@@ -174,6 +176,7 @@ def main():
     ap.add_argument("--heuristic", default="edges", choices=["edges", "paper"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--model-sources", type=int, default=4)
+    ap.add_argument("--mode", default="replicas", choices=["replicas", "partitioned"])
     args = ap.parse_args()
     rank, world, local = env_rank()
     if args.impl == "reference":
@@ -190,16 +193,23 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     g = synth.make(args.config)
-    ctx = pp.Context(local)
+    partitioned = args.mode == "partitioned" and world > 1
+    if partitioned:
+        nid = [pp.pp_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(nid, src=0)
+        ctx = pp.DistContext(local, rank, world, nid[0])
+    else:
+        ctx = pp.Context(local)
     G = pp.Graph.from_csr(ctx, g)
     n, nnz = g.n, g.nnz
+    lo, hi = G.partition() if partitioned else (0, n)
     off_bytes = 4 if nnz < 2**32 - 1 else 8
     heur = pp.PP_HEUR_EDGES if args.heuristic == "edges" else pp.PP_HEUR_PAPER_R
     all_src = synth.sources(g, 64, seed=2)
-    def src(k):
-        return int(all_src[(rank * 17 + k) % len(all_src)])
+    def src(k):  # partitioned: every rank runs the same (collective) BFS
+        return int(all_src[((0 if partitioned else rank) * 17 + k) % len(all_src)])
 
-    depth = torch.empty(n, dtype=torch.int32, device=dev)
+    depth = torch.empty(max(hi - lo, 1), dtype=torch.int32, device=dev)
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
     for k in range(args.warmup):
@@ -234,10 +244,11 @@ def main():
         dist.all_reduce(tot_ms, op=dist.ReduceOp.MAX)
     tot_ms = float(tot_ms.item())
     ms_per_step = tot_ms / args.steps
-    value = world * args.steps * nnz / (tot_ms * 1e-3) / 1e9
+    units = 1 if partitioned else world  # BFS traversals per step across the job
+    value = units * args.steps * nnz / (tot_ms * 1e-3) / 1e9
 
     # ---- end to end through the public API: host output buffer, D2H inside the call ----
-    host_depth = torch.empty(n, dtype=torch.int32).pin_memory().numpy()
+    host_depth = torch.empty(max(hi - lo, 1), dtype=torch.int32).pin_memory().numpy()
     e2e_t = []
     for k in range(args.steps):
         flush.zero_()
@@ -248,36 +259,38 @@ def main():
     e2e_tot = torch.tensor([sum(e2e_t)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_tot, op=dist.ReduceOp.MAX)
-    e2e_val = world * args.steps * nnz / float(e2e_tot.item()) / 1e9
+    e2e_val = units * args.steps * nnz / float(e2e_tot.item()) / 1e9
 
     line = None
     if rank == 0:
-        # ---- roofline of the dominant (only) kernel: bfs_persistent ----
-        off_t = torch.from_numpy(g.off).to(dev)
-        idx_t = torch.from_numpy(g.idx.astype(np.int64)).to(dev)
-        deg_t = off_t[1:] - off_t[:-1]
-        rows_t = torch.repeat_interleave(torch.arange(n, device=dev), deg_t)
-        noniso = deg_t > 0
-        gd = (off_t, idx_t, rows_t, deg_t, noniso)
-        mb, mt = 0, 0.0
-        for k in range(min(args.model_sources, args.steps)):
-            s = src(args.warmup + k)
-            st = pp.bfs(G, s, depth, heuristic=heur, stats_capacity=4096)
-            mb += byte_model(torch, gd, depth, list(st["dir"]), n, nnz, off_bytes)
-            mt += step_ms[k] * 1e-3
-        del off_t, idx_t, rows_t, deg_t, noniso, gd
         peak, peak_src = measured_peaks()
-        achieved = mb / mt / 1e9 if mt > 0 else 0.0
+        nmod = 0 if partitioned else min(args.model_sources, args.steps)
+        mb, mt = 0, 0.0
+        if nmod:
+            # ---- roofline of the dominant (only) kernel: bfs_persistent ----
+            off_t = torch.from_numpy(g.off).to(dev)
+            idx_t = torch.from_numpy(g.idx.astype(np.int64)).to(dev)
+            deg_t = off_t[1:] - off_t[:-1]
+            rows_t = torch.repeat_interleave(torch.arange(n, device=dev), deg_t)
+            noniso = deg_t > 0
+            gd = (off_t, idx_t, rows_t, deg_t, noniso)
+            for k in range(nmod):
+                s = src(args.warmup + k)
+                st = pp.bfs(G, s, depth, heuristic=heur, stats_capacity=4096)
+                mb += byte_model(torch, gd, depth, list(st["dir"]), n, nnz, off_bytes)
+                mt += step_ms[k] * 1e-3
+            del off_t, idx_t, rows_t, deg_t, noniso, gd
+        achieved = mb / mt / 1e9 if mt > 0 else None
         traffic = None
         prof = os.path.join(ROOT, "profiles", f"ncu_{args.config}.json")
-        if os.path.exists(prof):
+        if os.path.exists(prof) and not partitioned:
             try:
                 traffic = json.load(open(prof)).get("dram_bytes_per_launch")
             except Exception:
                 traffic = None
         # ---- CPU oracle baseline (bounded sample, 1 core) ----
         cpu = None
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and not partitioned:
             import oracle
             os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
             ts, k = [], 0
@@ -294,21 +307,25 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "scaling": "strong" if partitioned else "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic",
             "config": {"workload": f"{args.config}: {g.name} (Graph500 RMAT a,b,c=.57,.19,.19, "
                                    f"scrambled, symmetrised, dedup), n={n}, nnz={nnz}, one DO-BFS "
                                    f"per step from seeded sources",
                        "heuristic": args.heuristic, "l2": "flushed between steps (256 MiB write, "
-                       "not timed)", "parallelism": f"replicas x{world}"},
+                       "not timed)",
+                       "parallelism": (f"1D row partition x{world} (NCCL allgather per level)"
+                                       if partitioned else f"replicas x{world}")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "bfs_persistent (whole BFS in one cooperative launch)",
+                         "frac": achieved / peak if achieved else None, "traffic": traffic,
+                         "kernel": ("k_dist_push/k_dist_pull + ncclAllGather per level" if partitioned
+                                    else "bfs_persistent (whole BFS in one cooperative launch)"),
                          "peak_source": peak_src,
-                         "model": f"byte-exact DESIGN.md §6 over {min(args.model_sources, args.steps)} "
-                                  f"sources: {mb / max(1, min(args.model_sources, args.steps)) / 1e6:.1f} MB/BFS"},
+                         "model": f"byte-exact DESIGN.md §6 over {nmod} sources: "
+                                  f"{mb / max(1, nmod) / 1e6:.1f} MB/BFS"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8,
-                    "d2h_bytes_per_step": 4 * n,
+                    "d2h_bytes_per_step": 4 * (hi - lo),
                     "note": "pp_bfs with a pinned host depth buffer: launch + D2H copy of depth"},
             "gpu_launches": int(launches),
             "clocks": clk,

@@ -72,7 +72,7 @@ void free_graph(pp_graph g) {
   void* ptrs[] = {g->off, g->idx, g->symmetric ? nullptr : g->coff,
                   g->symmetric ? nullptr : (void*)g->cidx, g->isolated, g->head, g->vis[0], g->vis[1], g->fr, g->sumv,
                   g->L[0], g->L[1], g->H[0], g->H[1], g->ctr, g->stats, g->bar,
-                  g->sbits[0], g->sbits[1], g->sbits[2], g->sbits[3], g->sblock, g->scount,
+                  g->sbits[0], g->sbits[1], g->sbits[2], g->sbits[3], g->sblock, g->hubq, g->scount,
                   g->dtmp[0], g->dtmp[1], g->dbg,
                   g->dvis, g->dfr, g->dnxt, g->diso, g->pbeg, g->pend, g->dcnt};
   for (void* p : ptrs)
@@ -326,6 +326,9 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr
   for (int k = 0; k < 4; ++k)
     if ((s = dalloc(&g->sbits[k], g->nwords, &bytes, "scratch bitmap")) != PP_OK) return s;
   if ((s = dalloc(&g->sblock, g->nwords / 256 + 1, &bytes, "scan blocks")) != PP_OK) return s;
+  // long-row chunk queue of the row mxv: at most 2*nnz/1024 + 1 chunks
+  if ((s = dalloc(&g->hubq, (size_t)(2 * (nnz / 1024) + 2), &bytes, "row-mxv hub chunks")) != PP_OK)
+    return s;
   PP_CK(cudaMemsetAsync(g->bar, 0, sizeof(GridBarrier) * 2, st), "memset");
   PP_CK(cudaStreamSynchronize(st), "sync");
   if (g->dtmp[0]) {

@@ -15,6 +15,7 @@
 namespace pp {
 
 constexpr int kGridPerSM = 4;
+constexpr unsigned kHubIds = 1024;  // row-mxv rows with more ids left go to k_mxv_pull_hubs
 
 static int grid_blocks(pp_graph g) { return g->ctx->num_sms * kGridPerSM; }
 
@@ -128,7 +129,8 @@ template <typename Off>
 __global__ void __launch_bounds__(kBlock) k_mxv_pull(
     int64_t n, uint32_t nwords, const Off* __restrict__ roff, const uint32_t* __restrict__ ridx,
     const uint32_t* __restrict__ ubits, const uint32_t* __restrict__ mask, int complement,
-    int accum, int replace, int early_exit, const uint32_t* win, uint32_t* out) {
+    int accum, int replace, int early_exit, const uint32_t* win, uint32_t* out, uint4* hubq,
+    unsigned* nhub) {
   __shared__ uint32_t st[kWarps][32];
   uint32_t* tword = st[threadIdx.x >> 5];
   const unsigned lane = lane_id();
@@ -171,6 +173,22 @@ __global__ void __launch_bounds__(kBlock) k_mxv_pull(
         dm &= dm - 1;
         const Off pb = __shfl_sync(kFull, p, l), pe = __shfl_sync(kFull, e, l);
         bool f = false;
+        if (!early_exit && pe - pb > (Off)kHubIds) {
+          // long row: split into kHubIds-id chunks for k_mxv_pull_hubs (the whole grid);
+          // its bit is OR-ed into `out` there (exact: OR is idempotent and commutative)
+          const uint32_t il = __shfl_sync(kFull, i, l);
+          const unsigned nch = (unsigned)((pe - pb + (Off)kHubIds - 1) / (Off)kHubIds);
+          unsigned base = 0;
+          if (lane == 0) base = atomicAdd(nhub, nch);
+          base = __shfl_sync(kFull, base, 0);
+          for (unsigned c = lane; c < nch; c += 32) {
+            const Off st = pb + (Off)c * (Off)kHubIds;
+            const Off len = min((Off)kHubIds, pe - st);
+            hubq[base + c] = make_uint4(il, (uint32_t)len, (uint32_t)st,
+                                        (uint32_t)((unsigned long long)st >> 32));
+          }
+          continue;
+        }
         for (Off q0 = pb; q0 < pe; q0 += 128) {
           bool h = false;
 #pragma unroll
@@ -194,6 +212,34 @@ __global__ void __launch_bounds__(kBlock) k_mxv_pull(
       out[w] = ((pass & z) | (~pass & keep)) & valid_bits(n, w);
     }
     __syncwarp();
+  }
+}
+
+// Long rows of k_mxv_pull, kHubIds ids per chunk, spread over the whole grid (warp per chunk,
+// 128 ids per step, ballot early exit inside the chunk).
+template <typename Off>
+__global__ void __launch_bounds__(kBlock) k_mxv_pull_hubs(const uint4* __restrict__ hubq,
+                                                         const unsigned* __restrict__ nhub,
+                                                         const uint32_t* __restrict__ ridx,
+                                                         const uint32_t* __restrict__ ubits,
+                                                         int early_exit, uint32_t* out) {
+  const unsigned lane = lane_id();
+  const unsigned total = *nhub;
+  for (unsigned c = blockIdx.x * kWarps + (threadIdx.x >> 5); c < total; c += gridDim.x * kWarps) {
+    const uint4 h = hubq[c];
+    const Off st = (Off)(((unsigned long long)h.w << 32) | h.z), en = st + (Off)h.y;
+    bool f = false;
+    for (Off q0 = st; q0 < en; q0 += 128) {
+      bool hit = false;
+#pragma unroll
+      for (int s2 = 0; s2 < 4; ++s2) {
+        const Off q = q0 + (Off)(s2 * 32) + lane;
+        hit = hit || (q < en && bit_test(ubits, ridx[q]));
+      }
+      f = __any_sync(kFull, hit) || f;
+      if (f && early_exit) break;
+    }
+    if (f && lane == 0) atomicOr(&out[h.x >> 5], 1u << (h.x & 31u));
   }
 }
 
@@ -373,9 +419,23 @@ static cudaError_t mxv_t(pp_graph g, const MxvPlan& p) {
   const int blocks = grid_blocks(g);
   if (p.pull) {
     g->ctx->launches += 1;
+    // Without early exit, rows longer than kHubIds are split into chunks that a second
+    // kernel spreads over the grid; with early exit rows stay in their warp (most resolve in
+    // their first sector) and no second launch is needed.
+    unsigned* nhub = reinterpret_cast<unsigned*>(g->scount + 4);
+    if (!p.early_exit) {
+      cudaError_t e0 = cudaMemsetAsync(g->scount + 4, 0, sizeof(unsigned long long), st);
+      if (e0 != cudaSuccess) return e0;
+    }
+    g->ctx->launches += 1;
     k_mxv_pull<Off><<<blocks, kBlock, 0, st>>>(g->n, g->nwords, roff, ridx, p.u_bits, p.mask_bits,
                                                p.complement, p.accum, p.replace, p.early_exit,
-                                               p.win_bits, p.out_bits);
+                                               p.win_bits, p.out_bits, g->hubq, nhub);
+    if (!p.early_exit) {
+      g->ctx->launches += 1;
+      k_mxv_pull_hubs<Off><<<blocks, kBlock, 0, st>>>(g->hubq, nhub, ridx, p.u_bits, p.early_exit,
+                                                      p.out_bits);
+    }
     return cudaGetLastError();
   }
   uint32_t* t = g->sbits[0];

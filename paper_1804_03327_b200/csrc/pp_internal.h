@@ -103,6 +103,7 @@ struct pp_graph_s {
   // mxv scratch
   uint32_t* sbits[4] = {nullptr, nullptr, nullptr, nullptr};  // t, u, mask, w (bitmaps)
   uint32_t* sblock = nullptr;        // per-block counts for bitmap->list
+  uint4* hubq = nullptr;             // row-mxv long-row chunks {row, len, start}
   unsigned long long* scount = nullptr;  // device counters (mxv)
   unsigned long long* scount_host = nullptr;
   int64_t* dtmp[2] = {nullptr, nullptr};  // upload staging / host-output staging
