@@ -553,7 +553,7 @@ struct PullCtx {
     }
     a.depth[i] = d + 1;
     if (PARENTS) a.parent[i] = par;
-    if (kSumWordsMax) {
+    if (kSumWordsMax && !in_item) {  // in-item finds reach the summary at item close
       const uint32_t gi = i >> a.sum_shift;
       atomicOr(&a.sumv[gi >> 5], 1u << (gi & 31u));
     }
@@ -783,9 +783,21 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
     }
     if (qn > 0) C.residual_batch(qn, qn, wbase, true);
     __syncwarp();
+    const uint32_t fw = own ? sfound[lane] : 0u;
     if (own) {
-      vout[wbase + lane] = vw | sfound[lane];
-      a.fr[wbase + lane] = sfound[lane];
+      vout[wbase + lane] = vw | fw;
+      a.fr[wbase + lane] = fw;
+    }
+    if (kSumWordsMax && a.sum_shift >= 5) {
+      // the item's rows map into one summary word: one aggregated atomic per item
+      const uint32_t gi = ((wbase + lane) * 32u) >> a.sum_shift;
+      const uint32_t bits = __reduce_or_sync(kFull, fw ? (1u << (gi & 31u)) : 0u);
+      if (lane == 0 && bits) atomicOr(&a.sumv[(((wbase * 32u) >> a.sum_shift)) >> 5], bits);
+    } else if (kSumWordsMax && fw) {
+      for (uint32_t x = fw; x; x &= x - 1) {
+        const uint32_t gi = ((wbase + lane) * 32u + (__ffs(x) - 1)) >> a.sum_shift;
+        atomicOr(&a.sumv[gi >> 5], 1u << (gi & 31u));
+      }
     }
     __syncwarp();
   }
