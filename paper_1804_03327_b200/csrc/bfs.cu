@@ -724,42 +724,41 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
         par[t] = kNone;
         rb[t] = e[t] = 0;
       }
-      // stage: offsets and the row's head (first 8 in-neighbours = one 32-byte sector, one
-      // 256-bit load from a row-contiguous array: dense items stream it), all in flight
+      // stage: the row's head = {in-degree, first 7 in-neighbours}: one 32-byte sector, one
+      // 256-bit load from a row-contiguous array (dense items stream it); the offsets are
+      // only needed for rows longer than the head
       V8 hd[kC];
 #pragma unroll
-      for (int t = 0; t < kC; ++t) {
-        if (valid[t]) {
-          rb[t] = a.coff[i[t]];
-          e[t] = a.coff[i[t] + 1];
-          hd[t] = ld_nc_v8(a.head + (size_t)i[t] * 8u);
-        }
-      }
+      for (int t = 0; t < kC; ++t)
+        if (valid[t]) hd[t] = ld_nc_v8(a.head + (size_t)i[t] * 8u);
       // stage: probe the first neighbour, then the other head ids of rows that missed
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
-        const Off deg = e[t] - rb[t];
-        if (valid[t] && deg > 0 && C.hit(hd[t].x[0])) {
+        const uint32_t deg = valid[t] ? hd[t].x[0] : 0u;
+        if (deg > 0 && C.hit(hd[t].x[1])) {
           found[t] = true;
-          par[t] = hd[t].x[0];
+          par[t] = hd[t].x[1];
         }
       }
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
-        const Off deg = e[t] - rb[t];
-        if (valid[t] && deg > 1 && !(found[t] && C.early_exit)) {
+        const uint32_t deg = valid[t] ? hd[t].x[0] : 0u;
+        if (deg > 1 && !(found[t] && C.early_exit)) {
           bool h[8];
 #pragma unroll
-          for (int q = 1; q < 8; ++q) h[q] = deg > (Off)q && C.hit(hd[t].x[q]);
+          for (int q = 2; q < 8; ++q) h[q] = deg > (uint32_t)(q - 1) && C.hit(hd[t].x[q]);
 #pragma unroll
-          for (int q = 1; q < 8; ++q) {
+          for (int q = 2; q < 8; ++q) {
             if (h[q] && !found[t]) {
               found[t] = true;
               par[t] = hd[t].x[q];
             }
           }
         }
-        p[t] = (valid[t] && deg > 8) ? rb[t] + 8 : e[t];  // the tail continues in idx
+        const bool tail = deg > 7 && !(found[t] && C.early_exit);
+        rb[t] = tail ? a.coff[i[t]] : (Off)0;  // row begin only for rows that continue
+        e[t] = rb[t] + (Off)deg;
+        p[t] = tail ? rb[t] + 7 : e[t];        // the tail continues in idx
       }
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
