@@ -95,9 +95,15 @@ __device__ __forceinline__ bool grid_barrier(GridBarrier* b, BfsStatus* st, unsi
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(&b->count);
     unsigned long long v = atom_add_release_u64(cnt, 1ull) + 1ull;
     if (v < target) {
-      const unsigned long long t0 = global_timer_ns();
+      unsigned long long t0 = global_timer_ns();
+      unsigned hb = ld_relaxed_u32(&b->gen);
       while ((v = ld_acquire_u64(cnt)) < target) {
         __nanosleep(16);
+        const unsigned hb2 = ld_relaxed_u32(&b->gen);  // solo-mode heartbeat (CTA 0)
+        if (hb2 != hb) {
+          hb = hb2;
+          t0 = global_timer_ns();
+        }
         if (global_timer_ns() - t0 > kWatchdogNs) {
           atomicExch(&st->error, (int)PP_ERR_TIMEOUT);
           atomicOr(cnt, kAbortBit);
@@ -158,6 +164,12 @@ __device__ __forceinline__ unsigned cta_grab(unsigned* sctr) {
   if (lane_id() == 0) j = atomicAdd(sctr, 1u);
   j = __shfl_sync(kFull, j, 0);
   return blockIdx.x + j * gridDim.x;
+}
+// Solo mode (one CTA runs a tiny level): every item of the phase belongs to this CTA.
+__device__ __forceinline__ unsigned cta_grab_all(unsigned* sctr) {
+  unsigned j = 0;
+  if (lane_id() == 0) j = atomicAdd(sctr, 1u);
+  return __shfl_sync(kFull, j, 0);
 }
 __device__ __forceinline__ unsigned nwarps() { return gridDim.x * kBfsWarps; }
 
@@ -285,18 +297,36 @@ template <typename Off, bool PARENTS>
 __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&valid)[kU],
                                             const uint32_t (&u)[kU], const uint32_t (&w)[kU],
                                             uint32_t* vis, int newdepth, uint4* Lout,
-                                            uint2* Hout, LevelCtr* out, Acc& acc) {
+                                            uint2* Hout, LevelCtr* out, Acc& acc, bool lowlat) {
   uint32_t cur[kU];
   bool disc[kU];
+  Off sb[kU], se[kU];
+  if (lowlat) {
+    // small level: latency matters more than traffic — atomicOr without the pre-test, and
+    // the head's offsets loaded speculatively in parallel (one round trip instead of three)
 #pragma unroll
-  for (int t = 0; t < kU; ++t) cur[t] = valid[t] ? vis[w[t] >> 5] : 0xFFFFFFFFu;
+    for (int t = 0; t < kU; ++t) {
+      cur[t] = 0xFFFFFFFFu;
+      sb[t] = se[t] = 0;
+      if (valid[t]) {
+        cur[t] = atomicOr(&vis[w[t] >> 5], 1u << (w[t] & 31u));
+        sb[t] = a.off[w[t]];
+        se[t] = a.off[w[t] + 1];
+      }
+    }
 #pragma unroll
-  for (int t = 0; t < kU; ++t) {
-    const uint32_t bit = 1u << (w[t] & 31u);
-    disc[t] = false;
-    if (!(cur[t] & bit)) {
-      const uint32_t old = atomicOr(&vis[w[t] >> 5], bit);
-      disc[t] = !(old & bit);
+    for (int t = 0; t < kU; ++t) disc[t] = valid[t] && !((cur[t] >> (w[t] & 31u)) & 1u);
+  } else {
+#pragma unroll
+    for (int t = 0; t < kU; ++t) cur[t] = valid[t] ? vis[w[t] >> 5] : 0xFFFFFFFFu;
+#pragma unroll
+    for (int t = 0; t < kU; ++t) {
+      const uint32_t bit = 1u << (w[t] & 31u);
+      disc[t] = false;
+      if (!(cur[t] & bit)) {
+        const uint32_t old = atomicOr(&vis[w[t] >> 5], bit);
+        disc[t] = !(old & bit);
+      }
     }
   }
 #pragma unroll
@@ -328,8 +358,8 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
     deg[t] = 0;
     beg[t] = 0;
     if (disc[t]) {
-      beg[t] = a.off[w[t]];
-      deg[t] = a.off[w[t] + 1] - beg[t];
+      beg[t] = lowlat ? sb[t] : a.off[w[t]];
+      deg[t] = (lowlat ? se[t] : a.off[w[t] + 1]) - beg[t];
       const Off degin = a.symmetric ? deg[t] : (Off)(a.coff[w[t] + 1] - a.coff[w[t]]);
       acc.c += 1;
       acc.mf += (unsigned long long)deg[t];
@@ -344,7 +374,7 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
 template <typename Off, bool PARENTS>
 __device__ __forceinline__ void push_round(const BfsArgs<Off>& a, uint32_t v, Off b, unsigned deg,
                                            uint4* Lout, uint2* Hout, LevelCtr* out,
-                                           uint32_t* vis, int newdepth, Acc& acc) {
+                                           uint32_t* vis, int newdepth, Acc& acc, bool lowlat) {
   const unsigned lane = lane_id();
   const unsigned incl = warp_incl_scan(deg);
   const unsigned excl = incl - deg;
@@ -362,7 +392,7 @@ __device__ __forceinline__ void push_round(const BfsArgs<Off>& a, uint32_t v, Of
       valid[t] = e < tot;
       w[t] = valid[t] ? a.idx[bj + (Off)(e - xj)] : 0u;
     }
-    push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc);
+    push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat);
   }
 }
 
@@ -382,14 +412,15 @@ template <typename Off, bool PARENTS>
 __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
                            const uint2* Hin, unsigned nH, const uint32_t* fr, uint4* Lout,
                            uint2* Hout, LevelCtr* out, uint32_t* vis, int newdepth, Acc& acc,
-                           unsigned* sctr) {
+                           unsigned* sctr, bool solo, bool lowlat) {
   const unsigned lane = lane_id();
-  const unsigned NW = nwarps();
+  const unsigned NW = solo ? (unsigned)kBfsWarps : nwarps();
   unsigned R = 32;
   while (R > 1 && (nL + R / 2 - 1) / (R / 2) <= NW) R >>= 1;
   const unsigned nRounds = fr ? a.nwords / kPW : (nL + R - 1) / R;
   const unsigned total = nH + nRounds;
-  for (unsigned item = cta_grab(sctr); item < total; item = cta_grab(sctr)) {
+  for (unsigned item = solo ? cta_grab_all(sctr) : cta_grab(sctr); item < total;
+       item = solo ? cta_grab_all(sctr) : cta_grab(sctr)) {
     if (item < nH) {
       bool valid[kU];
       uint32_t u[kU], w[kU];
@@ -404,7 +435,7 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
         u[t] = h.x;
         w[t] = valid[t] ? a.idx[p] : 0u;
       }
-      push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc);
+      push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat);
     } else if (!fr) {
       const unsigned i = (item - nH) * R + lane;
       uint32_t v = 0;
@@ -416,7 +447,7 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
         deg = le.y;
         b = light_begin<Off>(le);
       }
-      push_round<Off, PARENTS>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc);
+      push_round<Off, PARENTS>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc, lowlat);
     } else {
       const unsigned wbase = (item - nH) * kPW;
       const uint32_t fw = lane < kPW ? fr[wbase + lane] : 0u;
@@ -437,7 +468,7 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
           b = a.off[v];
           deg = (unsigned)(a.off[v + 1] - b);
         }
-        push_round<Off, PARENTS>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc);
+        push_round<Off, PARENTS>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc, lowlat);
       }
     }
   }
@@ -724,41 +755,42 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
         par[t] = kNone;
         rb[t] = e[t] = 0;
       }
-      // stage: the row's head = {in-degree, first 7 in-neighbours}: one 32-byte sector, one
-      // 256-bit load from a row-contiguous array (dense items stream it); the offsets are
-      // only needed for rows longer than the head
+      // stage: offsets and the row's head (first 8 in-neighbours = one 32-byte sector, one
+      // 256-bit load from a row-contiguous array: dense items stream it), all in flight
       V8 hd[kC];
 #pragma unroll
-      for (int t = 0; t < kC; ++t)
-        if (valid[t]) hd[t] = ld_nc_v8(a.head + (size_t)i[t] * 8u);
+      for (int t = 0; t < kC; ++t) {
+        if (valid[t]) {
+          rb[t] = a.coff[i[t]];
+          e[t] = a.coff[i[t] + 1];
+          hd[t] = ld_nc_v8(a.head + (size_t)i[t] * 8u);
+        }
+      }
       // stage: probe the first neighbour, then the other head ids of rows that missed
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
-        const uint32_t deg = valid[t] ? hd[t].x[0] : 0u;
-        if (deg > 0 && C.hit(hd[t].x[1])) {
+        const Off deg = e[t] - rb[t];
+        if (valid[t] && deg > 0 && C.hit(hd[t].x[0])) {
           found[t] = true;
-          par[t] = hd[t].x[1];
+          par[t] = hd[t].x[0];
         }
       }
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
-        const uint32_t deg = valid[t] ? hd[t].x[0] : 0u;
-        if (deg > 1 && !(found[t] && C.early_exit)) {
+        const Off deg = e[t] - rb[t];
+        if (valid[t] && deg > 1 && !(found[t] && C.early_exit)) {
           bool h[8];
 #pragma unroll
-          for (int q = 2; q < 8; ++q) h[q] = deg > (uint32_t)(q - 1) && C.hit(hd[t].x[q]);
+          for (int q = 1; q < 8; ++q) h[q] = deg > (Off)q && C.hit(hd[t].x[q]);
 #pragma unroll
-          for (int q = 2; q < 8; ++q) {
+          for (int q = 1; q < 8; ++q) {
             if (h[q] && !found[t]) {
               found[t] = true;
               par[t] = hd[t].x[q];
             }
           }
         }
-        const bool tail = deg > 7 && !(found[t] && C.early_exit);
-        rb[t] = tail ? a.coff[i[t]] : (Off)0;  // row begin only for rows that continue
-        e[t] = rb[t] + (Off)deg;
-        p[t] = tail ? rb[t] + 7 : e[t];        // the tail continues in idx
+        p[t] = (valid[t] && deg > 8) ? rb[t] + 8 : e[t];  // the tail continues in idx
       }
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
@@ -918,8 +950,46 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   long long reached = 1;
   Acc acc{0, 0, 0, 0};
   bool from_bits = false;  // next push reads the pull's frontier bitmap
+  // Solo mode: a push level expanding <= kSoloEdges edges runs in CTA 0 alone, with
+  // CTA-local synchronisation instead of grid barriers, for as many consecutive tiny push
+  // levels as follow; the other CTAs wait in one grid barrier and then reload the level
+  // state CTA 0 publishes.  Every CTA evaluates the same condition from the same counters.
+  bool solo = kSoloEdges && dir == 0 && (unsigned long long)(a.off[s + 1] - a.off[s]) <= kSoloEdges;
+  long long mf_last = (long long)(a.off[s + 1] - a.off[s]);  // edges the next push expands
   int d = 1;
   for (;; ++d) {
+    if (solo && blockIdx.x != 0) {
+      if (!grid_barrier(a.bar, a.status, epoch)) return;
+      if (threadIdx.x == 0) {
+        sh.lvl[0] = ld_relaxed_s32(&a.status->solo_d);
+        sh.lvl[1] = ld_relaxed_s32(&a.status->solo_dir);
+        sh.lvl[2] = ld_relaxed_s32(&a.status->solo_sel);
+        sh.lvl[3] = ld_relaxed_s32(&a.status->solo_finished);
+        sh.lvl[4] = (long long)ld_relaxed_u64((const unsigned long long*)&a.status->solo_c_old);
+        sh.lvl[5] = (long long)ld_relaxed_u64((const unsigned long long*)&a.status->solo_m_u);
+        sh.red[0][0] = ld_relaxed_u64((const unsigned long long*)&a.status->solo_reached);
+        sh.red[0][1] = ld_relaxed_u32(&a.status->solo_nL);
+        sh.red[0][2] = ld_relaxed_u32(&a.status->solo_nH);
+        sh.red[0][3] = ld_relaxed_u64((const unsigned long long*)&a.status->solo_mf);
+        sh.work = 0u;
+      }
+      __syncthreads();
+      d = (int)sh.lvl[0];
+      dir = (int)sh.lvl[1];
+      sel = (int)sh.lvl[2];
+      c_old = sh.lvl[4];
+      m_u = sh.lvl[5];
+      reached = (long long)sh.red[0][0];
+      nL = (unsigned)sh.red[0][1];
+      nH = (unsigned)sh.red[0][2];
+      mf_last = (long long)sh.red[0][3];
+      const bool finished = sh.lvl[3] != 0;
+      __syncthreads();
+      solo = false;
+      if (finished) break;
+      --d;  // the loop increment brings d to the published next level
+      continue;
+    }
     const long long t_lvl = (a.dbg && threadIdx.x == 0) ? (long long)global_timer_ns() : 0;
     LevelCtr* out = &a.ctr[d & (kRing - 1)];
     if (blockIdx.x == 0 && threadIdx.x < sizeof(LevelCtr) / 4)
@@ -930,7 +1000,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       push_phase<Off, PARENTS>(a, sel ? a.L1 : a.L0, from_bits ? 0u : nL, sel ? a.H1 : a.H0,
                                from_bits ? 0u : nH, from_bits ? a.fr : nullptr,
                                sel ? a.L0 : a.L1, sel ? a.H0 : a.H1, out, vis, d + 1, acc,
-                               &sh.work);
+                               &sh.work, solo, (unsigned long long)mf_last <= kLowLatEdges);
       from_bits = false;
     } else {
       if (kSumWordsMax) {
@@ -941,9 +1011,15 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
                                ssum, &sh.work);
     }
     flush_acc(acc, out, sh.red);
-    if (a.dbg && threadIdx.x == 0 && d - 1 < a.dbg_levels)
-      a.dbg[(size_t)(d - 1) * gridDim.x + blockIdx.x] = (long long)global_timer_ns() - t_lvl;
-    if (!grid_barrier(a.bar, a.status, epoch)) return;
+    if (solo) {
+      __threadfence_block();
+      __syncthreads();
+      if (threadIdx.x == 0) st_release_gpu(&a.bar->gen, (unsigned)d);  // heartbeat
+    } else {
+      if (a.dbg && threadIdx.x == 0 && d - 1 < a.dbg_levels)
+        a.dbg[(size_t)(d - 1) * gridDim.x + blockIdx.x] = (long long)global_timer_ns() - t_lvl;
+      if (!grid_barrier(a.bar, a.status, epoch)) return;
+    }
     read_level(out, sh);
     const long long c_new = sh.lvl[0], mf = sh.lvl[1], mfin = sh.lvl[2];
     nL = (unsigned)sh.lvl[3];
@@ -962,9 +1038,32 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       st.t_ns = (long long)global_timer_ns();
       a.stats[d - 1] = st;
     }
-    if (c_new == 0 || d >= a.max_levels) break;
+    const bool done = c_new == 0 || d >= a.max_levels;
     int next = dir;
-    if (a.mode == 0) next = decide(a.rule, dir, c_old, c_new, mf, m_u, a.n, a.alpha, a.beta);
+    if (!done && a.mode == 0)
+      next = decide(a.rule, dir, c_old, c_new, mf, m_u, a.n, a.alpha, a.beta);
+    const bool solo_next = kSoloEdges && !done && dir == 0 && next == 0 &&
+                           (unsigned long long)mf <= kSoloEdges;
+    if (solo && !solo_next) {
+      // CTA 0 ends its solo run: publish the loop state for level d+1, release the others
+      if (threadIdx.x == 0) {
+        a.status->solo_d = d + 1;
+        a.status->solo_dir = next;
+        a.status->solo_sel = sel;
+        a.status->solo_finished = done ? 1 : 0;
+        a.status->solo_c_old = c_new;
+        a.status->solo_m_u = m_u;
+        a.status->solo_reached = reached;
+        a.status->solo_nL = nL;
+        a.status->solo_nH = nH;
+        a.status->solo_mf = mf;
+      }
+      if (!grid_barrier(a.bar, a.status, epoch)) return;
+      solo = false;
+    } else if (!solo && solo_next) {
+      solo = true;
+    }
+    if (done) break;
     if (dir == 1 && next == 0 && sh.lvl[5] == 0) {
       from_bits = true;  // every new frontier vertex is light: push straight from `fr`
     } else if (dir == 1 && next == 0) {
@@ -980,6 +1079,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
     }
     dir = next;
     c_old = c_new;
+    mf_last = mf;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.status->levels = d;

@@ -27,23 +27,23 @@ __global__ void k_isolated(const int64_t* __restrict__ off, const int64_t* __res
   }
 }
 
-// Pull-side row heads: {in-degree, first 7 in-neighbours} of every row (CSC), 32 bytes per
-// vertex, unused slots 0xFFFFFFFF.  One row-contiguous sector per vertex lets the pull decide
-// most rows with a single load and no offsets (ELL head + CSR tail).
+// Pull-side row heads: the first 8 in-neighbours of every row (CSC), 0xFFFFFFFF-padded,
+// 32 bytes per vertex.  A row-contiguous sector per vertex lets the pull decide most rows
+// without a scattered access into the id array (ELL head + CSR tail).
 __global__ void k_head(const int64_t* __restrict__ coff, const uint32_t* __restrict__ cidx,
                        int64_t n, uint32_t* __restrict__ head) {
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = coff[v], d = coff[v + 1] - b;
     uint4 h0, h1;
-    h0.x = (uint32_t)d;
-    h0.y = d > 0 ? cidx[b] : 0xFFFFFFFFu;
-    h0.z = d > 1 ? cidx[b + 1] : 0xFFFFFFFFu;
-    h0.w = d > 2 ? cidx[b + 2] : 0xFFFFFFFFu;
-    h1.x = d > 3 ? cidx[b + 3] : 0xFFFFFFFFu;
-    h1.y = d > 4 ? cidx[b + 4] : 0xFFFFFFFFu;
-    h1.z = d > 5 ? cidx[b + 5] : 0xFFFFFFFFu;
-    h1.w = d > 6 ? cidx[b + 6] : 0xFFFFFFFFu;
+    h0.x = d > 0 ? cidx[b] : 0xFFFFFFFFu;
+    h0.y = d > 1 ? cidx[b + 1] : 0xFFFFFFFFu;
+    h0.z = d > 2 ? cidx[b + 2] : 0xFFFFFFFFu;
+    h0.w = d > 3 ? cidx[b + 3] : 0xFFFFFFFFu;
+    h1.x = d > 4 ? cidx[b + 4] : 0xFFFFFFFFu;
+    h1.y = d > 5 ? cidx[b + 5] : 0xFFFFFFFFu;
+    h1.z = d > 6 ? cidx[b + 6] : 0xFFFFFFFFu;
+    h1.w = d > 7 ? cidx[b + 7] : 0xFFFFFFFFu;
     reinterpret_cast<uint4*>(head)[2 * v] = h0;
     reinterpret_cast<uint4*>(head)[2 * v + 1] = h1;
   }

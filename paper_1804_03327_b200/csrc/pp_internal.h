@@ -19,6 +19,16 @@ constexpr int kRing = 4;           // level-counter ring
 #define PP_SUM_WORDS 0
 #endif
 constexpr unsigned kSumWordsMax = PP_SUM_WORDS;  // visited summary words in shared memory (0 = off)
+#ifndef PP_SOLO_EDGES
+#define PP_SOLO_EDGES 0
+#endif
+constexpr unsigned kSoloEdges = PP_SOLO_EDGES;  // push levels expanding <= this many edges
+                                                // run in CTA 0 alone (0 = never)
+#ifndef PP_LOWLAT_EDGES
+#define PP_LOWLAT_EDGES 32768
+#endif
+constexpr unsigned long long kLowLatEdges = PP_LOWLAT_EDGES;  // push levels expanding <= this
+                                  // many edges: speculative offsets, no pre-test before atomicOr
 constexpr unsigned kBig = 1024;    // pull->push goes straight from the bitmap if no new
                                    // frontier vertex has out-degree >= kBig
 #ifndef PP_BFS_BLOCK
@@ -59,6 +69,10 @@ struct BfsStatus {
   int levels;  // levels executed
   long long reached;
   long long t_start, t_init;  // %globaltimer at kernel entry / after the init barrier
+  // level-loop state handed back by CTA 0 at the end of a solo run
+  int solo_d, solo_dir, solo_sel, solo_finished;
+  long long solo_c_old, solo_m_u, solo_reached, solo_mf;
+  unsigned solo_nL, solo_nH;
 };
 
 }  // namespace pp

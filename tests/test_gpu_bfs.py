@@ -206,3 +206,19 @@ def test_c4_grid_closed_form(ctx):
             assert st["levels"] == int(exp.max()) and not st["dir"].any()
             if par is not None:
                 oracle.validate_graph500(g, s, d, par)
+
+
+def test_debug_times_and_level_ns(ctx):
+    """pp_bfs_debug_times records per-level, per-CTA phase times; stats carry level ns."""
+    g = synth.rmat(14, 16, seed=2)
+    G = pp.Graph.from_csr(ctx, g)
+    nct = pp.pp_bfs_debug_times(G.handle, 16)
+    assert nct >= 1
+    d = torch.zeros(g.n, dtype=torch.int32, device="cuda")
+    s = int(synth.sources(g, 1, seed=8)[0])
+    st = pp.bfs(G, s, d, stats_capacity=64)
+    t = pp.pp_bfs_debug_times(G.handle, 16, fetch=True)
+    assert t.shape == (16, nct) and (t >= 0).all() and (t > 0).any()
+    assert (st["ns"][:st["levels"]] > 0).all() and st["init_ns"] > 0
+    exp, _ = oracle.bfs(g, s)
+    assert np.array_equal(d.cpu().numpy(), exp)
