@@ -215,6 +215,78 @@ __global__ void __launch_bounds__(kBlock) k_mxv_pull(
   }
 }
 
+// Row-based mxv WITHOUT early exit (Eq. 2 / Eq. 4 evaluated in full): every passing row's
+// ids must be read, so a warp streams its 32 rows' ids as one packed, warp-balanced sequence
+// (warp scan of the passing rows' degrees, 4 coalesced loads per lane per step) and ORs the
+// hits per row with a warp reduction.  Rows longer than kHubIds go to k_mxv_pull_hubs.
+template <typename Off>
+__global__ void __launch_bounds__(kBlock) k_mxv_pull_stream(
+    int64_t n, uint32_t nwords, const Off* __restrict__ roff, const uint32_t* __restrict__ ridx,
+    const uint32_t* __restrict__ ubits, const uint32_t* __restrict__ mask, int complement,
+    int accum, int replace, const uint32_t* win, uint32_t* out, uint4* hubq, unsigned* nhub) {
+  const unsigned lane = lane_id();
+  const unsigned nitems = (nwords + 31) / 32;  // warp item = 32 words; lane l owns word l
+  const unsigned wstride = gridDim.x * kWarps;
+  for (unsigned item = blockIdx.x * kWarps + (threadIdx.x >> 5); item < nitems; item += wstride) {
+    const uint32_t myw = item * 32u + lane;
+    const uint32_t mypass = myw < nwords ? pass_word(mask, complement, n, myw) : 0u;
+    uint32_t myt = 0;
+    unsigned todo = __ballot_sync(kFull, mypass != 0);
+    while (todo) {  // stream the words that have passing rows, one at a time
+      const unsigned wl = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t w = item * 32u + wl;
+      const uint32_t pass = __shfl_sync(kFull, mypass, wl);
+      const uint32_t i = w * 32u + lane;
+      const bool mine = (pass >> lane) & 1u;
+      Off b = 0, e = 0;
+      if (mine) {
+        b = roff[i];
+        e = roff[i + 1];
+      }
+      const bool hub = mine && (e - b) > (Off)kHubIds;
+      const unsigned hm = __ballot_sync(kFull, hub);
+      if (hm) {  // hub rows: chunks for the grid-wide kernel
+        const unsigned nch = hub ? (unsigned)((e - b + (Off)kHubIds - 1) / (Off)kHubIds) : 0u;
+        const unsigned incl = warp_incl_scan(nch);
+        const unsigned tot = __shfl_sync(kFull, incl, 31);
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(nhub, tot);
+        base = __shfl_sync(kFull, base, 0) + incl - nch;
+        for (unsigned c = 0; c < nch; ++c) {
+          const Off st = b + (Off)c * (Off)kHubIds;
+          const Off len = min((Off)kHubIds, e - st);
+          hubq[base + c] = make_uint4(i, (uint32_t)len, (uint32_t)st,
+                                      (uint32_t)((unsigned long long)st >> 32));
+        }
+      }
+      const unsigned deg = (mine && !hub) ? (unsigned)(e - b) : 0u;
+      const unsigned incl = warp_incl_scan(deg);
+      const unsigned excl = incl - deg;
+      const unsigned tot = __shfl_sync(kFull, incl, 31);
+      uint32_t t = 0;
+      for (unsigned base = 0; base < tot; base += 128) {
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) {
+          const unsigned q = base + (unsigned)s2 * 32u + lane;
+          const unsigned j = warp_owner(incl, q);
+          const Off bj = __shfl_sync(kFull, b, j);
+          const unsigned xj = __shfl_sync(kFull, excl, j);
+          const bool hit = q < tot && bit_test(ubits, ridx[bj + (Off)(q - xj)]);
+          t |= __reduce_or_sync(kFull, hit ? (1u << j) : 0u);
+        }
+      }
+      if (lane == wl) myt = t;
+    }
+    if (myw < nwords) {
+      const uint32_t wi = (accum || !replace) ? win[myw] : 0u;
+      const uint32_t z = accum ? (wi | myt) : myt;
+      const uint32_t keep = replace ? 0u : wi;
+      out[myw] = ((mypass & z) | (~mypass & keep)) & valid_bits(n, myw);
+    }
+  }
+}
+
 // Long rows of k_mxv_pull, kHubIds ids per chunk, spread over the whole grid (warp per chunk,
 // 128 ids per step, ballot early exit inside the chunk).
 template <typename Off>
@@ -428,9 +500,15 @@ static cudaError_t mxv_t(pp_graph g, const MxvPlan& p) {
       if (e0 != cudaSuccess) return e0;
     }
     g->ctx->launches += 1;
-    k_mxv_pull<Off><<<blocks, kBlock, 0, st>>>(g->n, g->nwords, roff, ridx, p.u_bits, p.mask_bits,
-                                               p.complement, p.accum, p.replace, p.early_exit,
-                                               p.win_bits, p.out_bits, g->hubq, nhub);
+    if (p.early_exit)
+      k_mxv_pull<Off><<<blocks, kBlock, 0, st>>>(g->n, g->nwords, roff, ridx, p.u_bits, p.mask_bits,
+                                                 p.complement, p.accum, p.replace, p.early_exit,
+                                                 p.win_bits, p.out_bits, g->hubq, nhub);
+    else
+      k_mxv_pull_stream<Off><<<blocks, kBlock, 0, st>>>(g->n, (uint32_t)((g->n + 31) / 32), roff,
+                                                        ridx, p.u_bits, p.mask_bits, p.complement,
+                                                        p.accum, p.replace, p.win_bits, p.out_bits,
+                                                        g->hubq, nhub);
     if (!p.early_exit) {
       g->ctx->launches += 1;
       k_mxv_pull_hubs<Off><<<blocks, kBlock, 0, st>>>(g->hubq, nhub, ridx, p.u_bits, p.early_exit,
