@@ -177,6 +177,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--model-sources", type=int, default=4)
     ap.add_argument("--mode", default="replicas", choices=["replicas", "partitioned"])
+    ap.add_argument("--no-relabel", action="store_true",
+                    help="upload without PP_GRAPH_RELABEL (caller vertex order)")
     args = ap.parse_args()
     rank, world, local = env_rank()
     if args.impl == "reference":
@@ -200,7 +202,8 @@ def main():
         ctx = pp.DistContext(local, rank, world, nid[0])
     else:
         ctx = pp.Context(local)
-    G = pp.Graph.from_csr(ctx, g)
+    relabel = not args.no_relabel and not partitioned
+    G = pp.Graph.from_csr(ctx, g, relabel=relabel)
     n, nnz = g.n, g.nnz
     lo, hi = G.partition() if partitioned else (0, n)
     off_bytes = 4 if nnz < 2**32 - 1 else 8
@@ -272,12 +275,25 @@ def main():
             idx_t = torch.from_numpy(g.idx.astype(np.int64)).to(dev)
             deg_t = off_t[1:] - off_t[:-1]
             rows_t = torch.repeat_interleave(torch.arange(n, device=dev), deg_t)
+            key_t = None
+            if relabel:  # the layout the kernel scans: internal ids, rows in that order
+                key_t = torch.from_numpy(synth.degree_order_key(g).astype(np.int64)).to(dev)
+                e = torch.sort(key_t[rows_t] * n + key_t[idx_t]).values
+                rows_t, idx_t = e // n, e % n
+                deg_t = torch.bincount(rows_t, minlength=n)
+                off_t = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+                off_t[1:] = torch.cumsum(deg_t, 0)
+                del e
             noniso = deg_t > 0
             gd = (off_t, idx_t, rows_t, deg_t, noniso)
             for k in range(nmod):
                 s = src(args.warmup + k)
                 st = pp.bfs(G, s, depth, heuristic=heur, stats_capacity=4096)
-                mb += byte_model(torch, gd, depth, list(st["dir"]), n, nnz, off_bytes)
+                dm = depth
+                if key_t is not None:
+                    dm = torch.empty_like(depth)
+                    dm[key_t] = depth
+                mb += byte_model(torch, gd, dm, list(st["dir"]), n, nnz, off_bytes)
                 mt += step_ms[k] * 1e-3
             del off_t, idx_t, rows_t, deg_t, noniso, gd
         achieved = mb / mt / 1e9 if mt > 0 else None
@@ -312,7 +328,8 @@ def main():
             "config": {"workload": f"{args.config}: {g.name} (Graph500 RMAT a,b,c=.57,.19,.19, "
                                    f"scrambled, symmetrised, dedup), n={n}, nnz={nnz}, one DO-BFS "
                                    f"per step from seeded sources",
-                       "heuristic": args.heuristic, "l2": "flushed between steps (256 MiB write, "
+                       "heuristic": args.heuristic, "relabel": relabel,
+                       "l2": "flushed between steps (256 MiB write, "
                        "not timed)",
                        "parallelism": (f"1D row partition x{world} (NCCL allgather per level)"
                                        if partitioned else f"replicas x{world}")},

@@ -76,6 +76,14 @@ pp_status pp_ctx_launch_count(pp_ctx ctx, uint64_t* out);
 #define PP_GRAPH_SYMMETRIC 1u
 #define PP_GRAPH_DEVICE 2u
 #define PP_GRAPH_VALIDATE 4u
+/* PP_GRAPH_RELABEL: renumber vertices internally in order of decreasing degree (out + in;
+ * ties by increasing id) and re-sort every row in that order (upload-time preprocessing,
+ * DESIGN.md §5.3).  Every result is still reported in the caller's ids; the only visible
+ * difference is which parent pp_bfs reports when several are valid: the in-neighbour at
+ * depth-1 that comes FIRST in the internal order (highest degree, then lowest id) instead
+ * of the lowest id.  Needs nnz, n < 2^31; single-GPU contexts only (else
+ * PP_ERR_UNSUPPORTED). */
+#define PP_GRAPH_RELABEL 8u
 pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr_off,
                           const uint32_t* csr_idx, const int64_t* csc_off,
                           const uint32_t* csc_idx, uint32_t flags, pp_graph* out);
@@ -138,8 +146,9 @@ pp_status pp_mxv(pp_graph g, pp_vector* w, const pp_descriptor* desc, const pp_v
  * depth: int32[n], device or host memory (detected); 0 = unreached, source = 1,
  *   level-k vertices = k (Alg. 1 convention, R1).  Host memory means the
  *   result is copied back inside the call (end-to-end path).
- * parent: int32[n] or NULL; canonical min-id parent at depth-1 (R14),
- *   parent[source] = source, unreached = -1.
+ * parent: int32[n] or NULL; canonical min-id parent at depth-1 (R14; on a
+ *   PP_GRAPH_RELABEL graph: first in the internal order), parent[source] = source,
+ *   unreached = -1.
  * Direction per level (Opt. 1): mode DO uses `heuristic`:
  *   PP_HEUR_EDGES   Beamer edge-count rule (P:366 first sentence; R11), alpha=15, beta=18;
  *   PP_HEUR_PAPER_R the paper's r = nnz(f)/M rule (R10), alpha=beta=0.01;

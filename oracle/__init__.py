@@ -51,6 +51,8 @@ def _load():
         lib.oracle_bfs.argtypes = [i64, vp, vp, i64, vp]
         lib.oracle_parents.restype = ctypes.c_int
         lib.oracle_parents.argtypes = [i64, vp, vp, vp, i64, vp]
+        lib.oracle_parents_ordered.restype = ctypes.c_int
+        lib.oracle_parents_ordered.argtypes = [i64, vp, vp, vp, i64, vp, vp]
         lib.oracle_mxv.restype = ctypes.c_int
         lib.oracle_mxv.argtypes = [i64, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                    vp, vp]
@@ -78,13 +80,22 @@ def bfs(g, s: int):
     return depth, int(L)
 
 
-def parents(gT, depth, s: int):
-    """O2: min-id parent at depth-1 (gT = CSC of A: row v lists in-neighbours)."""
+def parents(gT, depth, s: int, key=None):
+    """O2: min-id parent at depth-1 (gT = CSC of A: row v lists in-neighbours).  With
+    `key` (a permutation: key[u] = position of u in a vertex order) the valid parent with
+    the smallest key instead (the order of a PP_GRAPH_RELABEL graph)."""
     off, idx = _arr(gT.off, np.int64), _arr(gT.idx, np.uint32)
     depth = _arr(depth, np.int32)
     par = np.empty(gT.n, dtype=np.int32)
-    rc = _load().oracle_parents(gT.n, off.ctypes.data, idx.ctypes.data, depth.ctypes.data, int(s),
-                                par.ctypes.data)
+    if key is not None:
+        key = _arr(key, np.uint32)
+        assert key.shape == (gT.n,)
+        rc = _load().oracle_parents_ordered(gT.n, off.ctypes.data, idx.ctypes.data,
+                                            depth.ctypes.data, int(s), key.ctypes.data,
+                                            par.ctypes.data)
+    else:
+        rc = _load().oracle_parents(gT.n, off.ctypes.data, idx.ctypes.data, depth.ctypes.data,
+                                    int(s), par.ctypes.data)
     if rc != 0:
         raise ValueError("depth vector is not a BFS result")
     return par

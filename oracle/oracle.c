@@ -13,7 +13,8 @@
  * Functions (each is the plain definition, no blocking/fusion/reordering):
  *   O1 oracle_bfs        textbook FIFO-queue BFS; Alg. 1 depth convention
  *                        (source depth 1, unreached 0).
- *   O2 oracle_parents    canonical min-id parent at depth-1 (R14).
+ *   O2 oracle_parents    canonical min-id parent at depth-1 (R14);
+ *      oracle_parents_ordered  the same under a vertex order (first in the order).
  *   O3 oracle_mxv        definitional Boolean masked matvec, Eq. 2/4 (P:91-96,
  *                        123-125) with structural complement, accumulate
  *                        and replace (R5, R6).  No early exit, no
@@ -76,6 +77,27 @@ int oracle_parents(int64_t n, const int64_t* coff, const uint32_t* cidx, const i
       if (depth[u] == depth[v] - 1 && (best < 0 || (int64_t)u < best)) best = u;
     }
     if (best < 0) return -1; /* depth vector is not a BFS result */
+    parent[v] = (int32_t)best;
+  }
+  return 0;
+}
+
+/* O2 under a vertex order (PP_GRAPH_RELABEL, R14): the same set of valid
+ * parents { u in N-(v) : depth[u] = depth[v]-1 }, the canonical one being the u with the
+ * smallest key[u] (key = a permutation of 0..n-1: the position of u in the order).
+ * key[u] = u gives oracle_parents. */
+int oracle_parents_ordered(int64_t n, const int64_t* coff, const uint32_t* cidx,
+                           const int32_t* depth, int64_t s, const uint32_t* key, int32_t* parent) {
+  for (int64_t v = 0; v < n; ++v) {
+    parent[v] = -1;
+    if (depth[v] == 0) continue;
+    if (v == s) { parent[v] = (int32_t)s; continue; }
+    int64_t best = -1;
+    for (int64_t e = coff[v]; e < coff[v + 1]; ++e) {
+      uint32_t u = cidx[e];
+      if (depth[u] == depth[v] - 1 && (best < 0 || key[u] < key[best])) best = u;
+    }
+    if (best < 0) return -1;
     parent[v] = (int32_t)best;
   }
   return 0;

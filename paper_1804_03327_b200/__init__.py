@@ -30,7 +30,7 @@ PP_OK, PP_ERR_ARG, PP_ERR_RANGE, PP_ERR_DIM, PP_ERR_GRAPH, PP_ERR_UNSUPPORTED, P
 STATUS_NAMES = {0: "PP_OK", 1: "PP_ERR_ARG", 2: "PP_ERR_RANGE", 3: "PP_ERR_DIM", 4: "PP_ERR_GRAPH",
                 5: "PP_ERR_UNSUPPORTED", 6: "PP_ERR_CUDA", 7: "PP_ERR_NCCL", 8: "PP_ERR_OOM",
                 9: "PP_ERR_TIMEOUT"}
-PP_GRAPH_SYMMETRIC, PP_GRAPH_DEVICE, PP_GRAPH_VALIDATE = 1, 2, 4
+PP_GRAPH_SYMMETRIC, PP_GRAPH_DEVICE, PP_GRAPH_VALIDATE, PP_GRAPH_RELABEL = 1, 2, 4, 8
 PP_VEC_LIST, PP_VEC_BITMAP = 0, 1
 PP_SR_LOR_LAND = 0
 PP_DIR_AUTO, PP_DIR_PUSH, PP_DIR_PULL = 0, 1, 2
@@ -272,13 +272,14 @@ class Graph:
     """Device-resident graph (library-owned copy of CSR + CSC)."""
 
     def __init__(self, ctx: Context, n, off, idx, coff=None, cidx=None, symmetric=None,
-                 validate=False, device_ptrs=False):
+                 validate=False, device_ptrs=False, relabel=False):
         self.ctx = ctx
         self.n = int(n)
         nnz = int(off[-1]) if not device_ptrs else int(idx.numel())
         if symmetric is None:
             symmetric = coff is None
         flags = (PP_GRAPH_SYMMETRIC if symmetric else 0) | (PP_GRAPH_VALIDATE if validate else 0) | \
+            (PP_GRAPH_RELABEL if relabel else 0) | \
             (PP_GRAPH_DEVICE if device_ptrs else 0)
         if not device_ptrs:
             off = np.ascontiguousarray(off, dtype=np.int64)
@@ -287,6 +288,7 @@ class Graph:
                 coff = np.ascontiguousarray(coff, dtype=np.int64)
                 cidx = np.ascontiguousarray(cidx, dtype=np.uint32)
         self.nnz = nnz
+        self.relabel = bool(relabel)
         self._keep = (off, idx, coff, cidx)
         self.handle = pp_graph_upload(ctx.handle, self.n, nnz, _ptr(off), _ptr(idx) if nnz else None,
                                       _ptr(coff), _ptr(cidx) if (cidx is not None and nnz) else None,
@@ -294,11 +296,12 @@ class Graph:
         self._keep = None
 
     @classmethod
-    def from_csr(cls, ctx, csr, csc=None, validate=False):
+    def from_csr(cls, ctx, csr, csc=None, validate=False, relabel=False):
         if csc is None and not getattr(csr, "symmetric", True):
             raise ValueError("directed graph needs its CSC")
         return cls(ctx, csr.n, csr.off, csr.idx, None if csc is None else csc.off,
-                   None if csc is None else csc.idx, symmetric=csc is None, validate=validate)
+                   None if csc is None else csc.idx, symmetric=csc is None, validate=validate,
+                   relabel=relabel)
 
     def info(self):
         return pp_graph_info(self.handle)

@@ -47,14 +47,18 @@ struct BfsArgs {
   uint4* L1;
   uint2* H0;
   uint2* H1;
-  int32_t* depth;
-  uint32_t* parent;
+  unsigned hcap;  // entries of H0 / H1 (chunk descriptors grow up, hub blocks down)
+  int32_t* depth;       // caller ids (PP_GRAPH_RELABEL: index through perm)
+  uint32_t* parent;     // internal ids (the caller's array, or pint on a relabelled graph)
+  uint32_t* pout;       // relabelled graph with parents: the caller's parent array
+  const uint32_t* __restrict__ perm;  // internal -> caller id, nullptr = identity
+  const uint32_t* __restrict__ rank;  // caller -> internal id
   LevelCtr* ctr;
   LevelStat* stats;
   int stats_cap;
   GridBarrier* bar;
   BfsStatus* status;
-  uint32_t source;
+  uint32_t source;  // caller id
   int mode;  // 0 DO, 1 push only, 2 pull only
   int rule;  // 0 edges, 1 paper r
   double alpha, beta;
@@ -96,14 +100,8 @@ __device__ __forceinline__ bool grid_barrier(GridBarrier* b, BfsStatus* st, unsi
     unsigned long long v = atom_add_release_u64(cnt, 1ull) + 1ull;
     if (v < target) {
       unsigned long long t0 = global_timer_ns();
-      unsigned hb = ld_relaxed_u32(&b->gen);
       while ((v = ld_acquire_u64(cnt)) < target) {
         __nanosleep(16);
-        const unsigned hb2 = ld_relaxed_u32(&b->gen);  // solo-mode heartbeat (CTA 0)
-        if (hb2 != hb) {
-          hb = hb2;
-          t0 = global_timer_ns();
-        }
         if (global_timer_ns() - t0 > kWatchdogNs) {
           atomicExch(&st->error, (int)PP_ERR_TIMEOUT);
           atomicOr(cnt, kAbortBit);
@@ -165,15 +163,8 @@ __device__ __forceinline__ unsigned cta_grab(unsigned* sctr) {
   j = __shfl_sync(kFull, j, 0);
   return blockIdx.x + j * gridDim.x;
 }
-// Solo mode (one CTA runs a tiny level): every item of the phase belongs to this CTA.
-__device__ __forceinline__ unsigned cta_grab_all(unsigned* sctr) {
-  unsigned j = 0;
-  if (lane_id() == 0) j = atomicAdd(sctr, 1u);
-  return __shfl_sync(kFull, j, 0);
-}
 __device__ __forceinline__ unsigned nwarps() { return gridDim.x * kBfsWarps; }
 
-constexpr unsigned kSelfChunks = 64;  // hubs with more chunks are emitted warp-cooperatively
 
 // Light frontier entry: the discovering thread already loaded the row's offsets, so the
 // next push reads {v, deg, begin} in one 16-byte load instead of a list load followed by
@@ -187,11 +178,43 @@ __device__ __forceinline__ Off light_begin(const uint4& e) {
   return (Off)(((unsigned long long)e.w << 32) | e.z);
 }
 
+// Heavy frontier vertices (out-degree >= kHeavy) are expanded as kChunk-edge chunks.  A
+// vertex with <= kSelfChunks chunks gets one descriptor {v, k} per chunk (bottom of H); a
+// hub gets one descriptor {v, k0} per 32 chunks (top of H, growing down: H[hcap-1-j]), and
+// the next push maps its hub items (32 per block) back to chunks.  Descriptor writes are
+// O(degree / 4096) for a hub, so no warp stalls emitting them whichever hubs it discovers
+// (with PP_GRAPH_RELABEL the first chunk of a row holds the highest-degree neighbours).
+// cs / cb: this lane's chunk / block descriptor counts; warp-collective.
+__device__ __forceinline__ void heavy_counts(unsigned nch, unsigned& cs, unsigned& cb) {
+  const bool hub = nch > kSelfChunks;
+  cs = hub ? 0u : nch;
+  cb = hub ? (nch + 31u) / 32u : 0u;
+}
+__device__ __forceinline__ void heavy_bases(unsigned CS, unsigned CB, LevelCtr* out, unsigned& s0,
+                                            unsigned& b0) {
+  const unsigned is = warp_incl_scan(CS), ib = warp_incl_scan(CB);
+  const unsigned ts = __shfl_sync(kFull, is, 31), tb = __shfl_sync(kFull, ib, 31);
+  unsigned bs = 0, bb = 0;
+  if (lane_id() == 0) {
+    if (ts) bs = atomicAdd(&out->nH, ts);
+    if (tb) bb = atomicAdd(&out->nB, tb);
+  }
+  s0 = __shfl_sync(kFull, bs, 0) + is - CS;
+  b0 = __shfl_sync(kFull, bb, 0) + ib - CB;
+}
+__device__ __forceinline__ void heavy_write(uint32_t v, unsigned cs, unsigned cb, uint2* H,
+                                            unsigned hcap, unsigned& s0, unsigned& b0) {
+  for (unsigned k = 0; k < cs; ++k) H[s0 + k] = make_uint2(v, k);
+  for (unsigned j = 0; j < cb; ++j) H[hcap - 1u - (b0 + j)] = make_uint2(v, 32u * j);
+  s0 += cs;
+  b0 += cb;
+}
+
 // Append newly discovered vertex v (valid lanes) to the next frontier: light list if
-// 0 < deg < kHeavy, else ceil(deg/kChunk) heavy chunks.  Warp-collective.
+// 0 < deg < kHeavy, else heavy chunks.  Warp-collective.
 template <typename Off>
 __device__ __forceinline__ void append_frontier(bool valid, uint32_t v, Off deg, Off begin, uint4* Lout,
-                                                uint2* Hout, LevelCtr* out) {
+                                                uint2* Hout, unsigned hcap, LevelCtr* out) {
   const unsigned lane = lane_id();
   bool heavy = valid && deg >= (Off)kHeavy;
   bool light = valid && deg > 0 && !heavy;
@@ -202,26 +225,11 @@ __device__ __forceinline__ void append_frontier(bool valid, uint32_t v, Off deg,
     base = __shfl_sync(kFull, base, leader);
     if (light) Lout[base + __popc(lm & lanemask_lt())] = light_entry<Off>(v, deg, begin);
   }
-  unsigned hm = __ballot_sync(kFull, heavy);
-  if (hm) {
-    const unsigned nch = heavy ? (unsigned)((deg + (Off)kChunk - 1) / (Off)kChunk) : 0u;
-    const unsigned incl = warp_incl_scan(nch);
-    const unsigned excl = incl - nch;
-    const unsigned tot = __shfl_sync(kFull, incl, 31);
-    unsigned base = 0;
-    if (lane == 0) base = atomicAdd(&out->nH, tot);
-    base = __shfl_sync(kFull, base, 0);
-    if (nch <= kSelfChunks)
-      for (unsigned k = 0; k < nch; ++k) Hout[base + excl + k] = make_uint2(v, k);
-    unsigned hb = __ballot_sync(kFull, nch > kSelfChunks);
-    while (hb) {  // hubs: vertex by vertex, 32 descriptors per step
-      const unsigned l = __ffs(hb) - 1;
-      hb &= hb - 1;
-      const uint32_t vl = __shfl_sync(kFull, v, l);
-      const unsigned n = __shfl_sync(kFull, nch, l);
-      const unsigned st = base + __shfl_sync(kFull, excl, l);
-      for (unsigned c = lane; c < n; c += 32) Hout[st + c] = make_uint2(vl, c);
-    }
+  if (__any_sync(kFull, heavy)) {
+    unsigned cs, cb, s0, b0;
+    heavy_counts(heavy ? (unsigned)((deg + (Off)kChunk - 1) / (Off)kChunk) : 0u, cs, cb);
+    heavy_bases(cs, cb, out, s0, b0);
+    heavy_write(v, cs, cb, Hout, hcap, s0, b0);
   }
 }
 
@@ -231,7 +239,7 @@ constexpr int kU = 4;  // edges (push) in flight per lane
 template <typename Off>
 __device__ __forceinline__ void append_frontier4(const bool (&disc)[kU], const uint32_t (&w)[kU],
                                                  const Off (&deg)[kU], const Off (&beg)[kU],
-                                                 uint4* Lout, uint2* Hout,
+                                                 uint4* Lout, uint2* Hout, unsigned hcap,
                                                  LevelCtr* out) {
   const unsigned lane = lane_id();
   unsigned lm[kU], ltot = 0, hsum = 0;
@@ -254,38 +262,18 @@ __device__ __forceinline__ void append_frontier4(const bool (&disc)[kU], const u
     }
   }
   if (__any_sync(kFull, hsum != 0)) {
-    // heavy chunks: one atomic per warp, then vertex by vertex, 32 descriptors per step
-    const unsigned incl = warp_incl_scan(hsum);
-    const unsigned tot = __shfl_sync(kFull, incl, 31);
-    unsigned base = 0;
-    if (lane == 0) base = atomicAdd(&out->nH, tot);
-    const unsigned start0 = __shfl_sync(kFull, base, 0) + incl - hsum;
-    // Lanes write their own descriptors (all lanes in parallel); vertices with more than
-    // kSelfChunks chunks (hubs) are then written warp-cooperatively, 32 per step.
-    unsigned start = start0;
-    unsigned nch[kU];
+    unsigned cs[kU], cb[kU], CS = 0, CB = 0;
 #pragma unroll
     for (int t = 0; t < kU; ++t) {
-      nch[t] = (disc[t] && deg[t] >= (Off)kHeavy)
-                   ? (unsigned)((deg[t] + (Off)kChunk - 1) / (Off)kChunk) : 0u;
-      if (nch[t] <= kSelfChunks)
-        for (unsigned k = 0; k < nch[t]; ++k) Hout[start + k] = make_uint2(w[t], k);
-      start += nch[t];
+      heavy_counts((disc[t] && deg[t] >= (Off)kHeavy)
+                       ? (unsigned)((deg[t] + (Off)kChunk - 1) / (Off)kChunk) : 0u, cs[t], cb[t]);
+      CS += cs[t];
+      CB += cb[t];
     }
-    start = start0;
+    unsigned s0, b0;
+    heavy_bases(CS, CB, out, s0, b0);
 #pragma unroll
-    for (int t = 0; t < kU; ++t) {
-      unsigned hb = __ballot_sync(kFull, nch[t] > kSelfChunks);
-      while (hb) {
-        const unsigned l = __ffs(hb) - 1;
-        hb &= hb - 1;
-        const uint32_t v = __shfl_sync(kFull, w[t], l);
-        const unsigned n = __shfl_sync(kFull, nch[t], l);
-        const unsigned st = __shfl_sync(kFull, start, l);
-        for (unsigned c = lane; c < n; c += 32) Hout[st + c] = make_uint2(v, c);
-      }
-      start += nch[t];
-    }
+    for (int t = 0; t < kU; ++t) heavy_write(w[t], cs[t], cb[t], Hout, hcap, s0, b0);
   }
 }
 
@@ -331,12 +319,9 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
   }
 #pragma unroll
   for (int t = 0; t < kU; ++t) {
-    if (disc[t]) {
-      a.depth[w[t]] = newdepth;
-      if (kSumWordsMax) {
-        const uint32_t gi = w[t] >> a.sum_shift;
-        atomicOr(&a.sumv[gi >> 5], 1u << (gi & 31u));
-      }
+    if (disc[t] && kSumWordsMax) {
+      const uint32_t gi = w[t] >> a.sum_shift;
+      atomicOr(&a.sumv[gi >> 5], 1u << (gi & 31u));
     }
   }
   if (PARENTS) {
@@ -345,7 +330,7 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
       if (!valid[t]) continue;
       bool fresh = disc[t] || !((cur[t] >> (w[t] & 31u)) & 1u);
       if (!fresh) {
-        const int dw = ld_relaxed_s32(&a.depth[w[t]]);
+        const int dw = ld_relaxed_s32(&a.depth[a.perm ? a.perm[w[t]] : w[t]]);
         fresh = (dw == 0 || dw == newdepth);
       }
       if (fresh) atomicMin(&a.parent[w[t]], u[t]);
@@ -353,11 +338,14 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
   }
   if (!__any_sync(kFull, disc[0] || disc[1] || disc[2] || disc[3])) return;
   Off deg[kU], beg[kU];
+  uint32_t dpos[kU];  // where the discovery's depth goes (caller id)
 #pragma unroll
   for (int t = 0; t < kU; ++t) {
     deg[t] = 0;
     beg[t] = 0;
+    dpos[t] = w[t];
     if (disc[t]) {
+      if (a.perm) dpos[t] = a.perm[w[t]];  // loaded in the same batch as the offsets
       beg[t] = lowlat ? sb[t] : a.off[w[t]];
       deg[t] = (lowlat ? se[t] : a.off[w[t] + 1]) - beg[t];
       const Off degin = a.symmetric ? deg[t] : (Off)(a.coff[w[t] + 1] - a.coff[w[t]]);
@@ -366,7 +354,10 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
       acc.mfin += (unsigned long long)degin;
     }
   }
-  append_frontier4<Off>(disc, w, deg, beg, Lout, Hout, out);
+#pragma unroll
+  for (int t = 0; t < kU; ++t)
+    if (disc[t]) a.depth[dpos[t]] = newdepth;
+  append_frontier4<Off>(disc, w, deg, beg, Lout, Hout, a.hcap, out);
 }
 
 // Edges of up to 32 light frontier vertices (lane l holds v, row begin b, degree deg),
@@ -397,7 +388,7 @@ __device__ __forceinline__ void push_round(const BfsArgs<Off>& a, uint32_t v, Of
 }
 
 #ifndef PP_PULL_WORDS
-#define PP_PULL_WORDS 32
+#define PP_PULL_WORDS 8
 #endif
 constexpr unsigned kPW = PP_PULL_WORDS;  // bitmap words per warp item (32*kPW rows)
 
@@ -410,23 +401,31 @@ constexpr unsigned kPW = PP_PULL_WORDS;  // bitmap words per warp item (32*kPW r
 // every warp), their edges balanced over lanes by a warp scan of degrees.
 template <typename Off, bool PARENTS>
 __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
-                           const uint2* Hin, unsigned nH, const uint32_t* fr, uint4* Lout,
+                           const uint2* Hin, unsigned nH, unsigned nB, const uint32_t* fr,
+                           uint4* Lout,
                            uint2* Hout, LevelCtr* out, uint32_t* vis, int newdepth, Acc& acc,
-                           unsigned* sctr, bool solo, bool lowlat) {
+                           unsigned* sctr, bool lowlat) {
   const unsigned lane = lane_id();
-  const unsigned NW = solo ? (unsigned)kBfsWarps : nwarps();
+  const unsigned NW = nwarps();
   unsigned R = 32;
   while (R > 1 && (nL + R / 2 - 1) / (R / 2) <= NW) R >>= 1;
   const unsigned nRounds = fr ? a.nwords / kPW : (nL + R - 1) / R;
-  const unsigned total = nH + nRounds;
-  for (unsigned item = solo ? cta_grab_all(sctr) : cta_grab(sctr); item < total;
-       item = solo ? cta_grab_all(sctr) : cta_grab(sctr)) {
-    if (item < nH) {
+  const unsigned nHC = nH + 32u * nB;  // chunk items: descriptors, then 32 per hub block
+  const unsigned total = nHC + nRounds;
+  for (unsigned item = cta_grab(sctr); item < total; item = cta_grab(sctr)) {
+    if (item < nHC) {
       bool valid[kU];
       uint32_t u[kU], w[kU];
-      const uint2 h = Hin[item];
+      uint2 h;
+      if (item < nH) {
+        h = Hin[item];
+      } else {
+        const unsigned q = item - nH;
+        h = Hin[a.hcap - 1u - (q >> 5)];
+        h.y += q & 31u;
+      }
       const Off rb = a.off[h.x], re = a.off[h.x + 1];
-      const Off b = rb + (Off)h.y * (Off)kChunk;
+      const Off b = rb + (Off)h.y * (Off)kChunk;  // past the row end for a hub's last slots
       const Off e = min(re, b + (Off)kChunk);
 #pragma unroll
       for (int t = 0; t < kU; ++t) {
@@ -437,7 +436,7 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
       }
       push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat);
     } else if (!fr) {
-      const unsigned i = (item - nH) * R + lane;
+      const unsigned i = (item - nHC) * R + lane;
       uint32_t v = 0;
       Off b = 0;
       unsigned deg = 0;
@@ -449,7 +448,7 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
       }
       push_round<Off, PARENTS>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc, lowlat);
     } else {
-      const unsigned wbase = (item - nH) * kPW;
+      const unsigned wbase = (item - nHC) * kPW;
       const uint32_t fw = lane < kPW ? fr[wbase + lane] : 0u;
       const unsigned cnt = __popc(fw);
       const unsigned incl = warp_incl_scan(cnt);
@@ -531,7 +530,7 @@ struct PullCtx {
   // unvisited neighbours without a global access (false positives only: a set summary
   // bit is confirmed against the exact snapshot bitmap).
   __device__ __forceinline__ bool hit(uint32_t x) const {
-    if (no_reuse) return a.depth[x] == d;
+    if (no_reuse) return a.depth[a.perm ? a.perm[x] : x] == d;
     if (kSumWordsMax) {
       const uint32_t gi = x >> a.sum_shift;
       if (!((ssum[gi >> 5] >> (gi & 31u)) & 1u)) return false;
@@ -574,7 +573,7 @@ struct PullCtx {
   }
   // discovery of row i (found this level): Alg. 1 lines 7-8 fused
   __device__ __forceinline__ void commit(uint32_t i, uint32_t par, Off degin, unsigned wbase,
-                                         bool in_item) const {
+                                         bool in_item, uint32_t dpos) const {
     const uint32_t bit = 1u << (i & 31u);
     if (in_item) {
       atomicOr(&sfound[(i >> 5) - wbase], bit);
@@ -582,7 +581,7 @@ struct PullCtx {
       atomicOr(&vout[i >> 5], bit);
       atomicOr(&a.fr[i >> 5], bit);
     }
-    a.depth[i] = d + 1;
+    a.depth[dpos] = d + 1;  // caller id of i
     if (PARENTS) a.parent[i] = par;
     if (kSumWordsMax && !in_item) {  // in-item finds reach the summary at item close
       const uint32_t gi = i >> a.sum_shift;
@@ -693,7 +692,7 @@ struct PullCtx {
     }
     if (valid && found && !committed) {
       const bool in_item = item_open && (i >> 5) >= wbase && (i >> 5) < wbase + kPW;
-      commit(i, par, (Off)degin, wbase, in_item);
+      commit(i, par, (Off)degin, wbase, in_item, a.perm ? a.perm[i] : i);
     }
   }
 };
@@ -758,9 +757,12 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
       // stage: offsets and the row's head (first 8 in-neighbours = one 32-byte sector, one
       // 256-bit load from a row-contiguous array: dense items stream it), all in flight
       V8 hd[kC];
+      uint32_t dpos[kC];  // caller id of the row (relabelled graph: loaded with the head)
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
+        dpos[t] = i[t];
         if (valid[t]) {
+          if (a.perm) dpos[t] = a.perm[i[t]];
           rb[t] = a.coff[i[t]];
           e[t] = a.coff[i[t] + 1];
           hd[t] = ld_nc_v8(a.head + (size_t)i[t] * 8u);
@@ -794,7 +796,7 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
       }
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
-        if (found[t] && fresh[t]) C.commit(i[t], par[t], e[t] - rb[t], wbase, true);
+        if (found[t] && fresh[t]) C.commit(i[t], par[t], e[t] - rb[t], wbase, true, dpos[t]);
         // park undecided rows (and, without early exit, rows with ids left)
         const bool park = valid[t] && p[t] < e[t] && !(found[t] && C.early_exit) &&
                           (fresh[t] || !found[t]);
@@ -854,7 +856,7 @@ __device__ void convert_phase(const BfsArgs<Off>& a, const uint32_t* vnew, const
         beg = a.off[v];
         deg = a.off[v + 1] - beg;
       }
-      append_frontier<Off>(valid, v, deg, beg, Lout, Hout, out);
+      append_frontier<Off>(valid, v, deg, beg, Lout, Hout, a.hcap, out);
     }
   }
 }
@@ -876,7 +878,7 @@ template <typename Off>
 struct BfsShared {  // static part; the residual queues live in dynamic shared memory
   uint32_t sfound[kBfsWarps][32];
   unsigned long long red[kBfsWarps][4];
-  long long lvl[6];  // c, m_f, m_fin, nL, nH, nbig of the level just finished
+  long long lvl[7];  // c, m_f, m_fin, nL, nH, nbig, nB of the level just finished
   unsigned work;     // CTA-local work counter (cta_grab)
 };
 
@@ -890,6 +892,7 @@ __device__ __forceinline__ void read_level(const LevelCtr* out, BfsShared<Off>& 
     sh.lvl[3] = (long long)ld_relaxed_u32(&out->nL);
     sh.lvl[4] = (long long)ld_relaxed_u32(&out->nH);
     sh.lvl[5] = (long long)ld_relaxed_u64(&out->nbig);
+    sh.lvl[6] = (long long)ld_relaxed_u32(&out->nB);
     sh.work = 0u;
   }
   __syncthreads();
@@ -904,14 +907,14 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   const unsigned warp = threadIdx.x >> 5;
   const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned long long gsize = (unsigned long long)gridDim.x * blockDim.x;
-  const uint32_t s = a.source;
+  const uint32_t s = a.rank ? a.rank[a.source] : a.source;  // internal id of the source
   if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t_start = (long long)global_timer_ns();
   unsigned epoch = 0;  // grid barriers passed (thread 0)
 
   // ---- Alg. 1 lines 2-4: d <- 1, f <- e_s, v <- 0 (depth 0 = unvisited) ----
   for (unsigned long long v = gtid; v < (unsigned long long)a.n; v += gsize) {
-    a.depth[v] = (v == s) ? 1 : 0;
-    if (PARENTS) a.parent[v] = (v == s) ? s : 0xFFFFFFFFu;
+    a.depth[v] = (v == a.source) ? 1 : 0;                          // caller ids
+    if (PARENTS) a.parent[v] = (v == s) ? s : 0xFFFFFFFFu;         // internal ids
   }
   // visited starts as {s} plus the isolated / padding vertices, which no pull may
   // compute and no push can reach (they have no edges).
@@ -929,8 +932,15 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
     const Off deg = a.off[s + 1] - a.off[s];
     if (deg >= (Off)kHeavy) {
       const unsigned nch = (unsigned)((deg + (Off)kChunk - 1) / (Off)kChunk);
-      for (unsigned k = threadIdx.x; k < nch; k += blockDim.x) a.H0[k] = make_uint2(s, k);
-      if (threadIdx.x == 0) a.ctr[0].nH = nch;
+      if (nch <= kSelfChunks) {
+        for (unsigned k = threadIdx.x; k < nch; k += blockDim.x) a.H0[k] = make_uint2(s, k);
+        if (threadIdx.x == 0) a.ctr[0].nH = nch;
+      } else {
+        const unsigned nb = (nch + 31u) / 32u;
+        for (unsigned j = threadIdx.x; j < nb; j += blockDim.x)
+          a.H0[a.hcap - 1u - j] = make_uint2(s, 32u * j);
+        if (threadIdx.x == 0) a.ctr[0].nB = nb;
+      }
     } else if (deg > 0 && threadIdx.x == 0) {
       a.L0[0] = light_entry<Off>(s, deg, a.off[s]);
       a.ctr[0].nL = 1;
@@ -939,7 +949,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   if (!grid_barrier(a.bar, a.status, epoch)) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t_init = (long long)global_timer_ns();
   read_level(&a.ctr[0], sh);
-  unsigned nL = (unsigned)sh.lvl[3], nH = (unsigned)sh.lvl[4];
+  unsigned nL = (unsigned)sh.lvl[3], nH = (unsigned)sh.lvl[4], nB = (unsigned)sh.lvl[6];
 
   int dir = (a.mode == 2) ? 1 : 0;
   int cur = 0;  // visited bitmap in use
@@ -950,46 +960,9 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   long long reached = 1;
   Acc acc{0, 0, 0, 0};
   bool from_bits = false;  // next push reads the pull's frontier bitmap
-  // Solo mode: a push level expanding <= kSoloEdges edges runs in CTA 0 alone, with
-  // CTA-local synchronisation instead of grid barriers, for as many consecutive tiny push
-  // levels as follow; the other CTAs wait in one grid barrier and then reload the level
-  // state CTA 0 publishes.  Every CTA evaluates the same condition from the same counters.
-  bool solo = kSoloEdges && dir == 0 && (unsigned long long)(a.off[s + 1] - a.off[s]) <= kSoloEdges;
   long long mf_last = (long long)(a.off[s + 1] - a.off[s]);  // edges the next push expands
   int d = 1;
   for (;; ++d) {
-    if (solo && blockIdx.x != 0) {
-      if (!grid_barrier(a.bar, a.status, epoch)) return;
-      if (threadIdx.x == 0) {
-        sh.lvl[0] = ld_relaxed_s32(&a.status->solo_d);
-        sh.lvl[1] = ld_relaxed_s32(&a.status->solo_dir);
-        sh.lvl[2] = ld_relaxed_s32(&a.status->solo_sel);
-        sh.lvl[3] = ld_relaxed_s32(&a.status->solo_finished);
-        sh.lvl[4] = (long long)ld_relaxed_u64((const unsigned long long*)&a.status->solo_c_old);
-        sh.lvl[5] = (long long)ld_relaxed_u64((const unsigned long long*)&a.status->solo_m_u);
-        sh.red[0][0] = ld_relaxed_u64((const unsigned long long*)&a.status->solo_reached);
-        sh.red[0][1] = ld_relaxed_u32(&a.status->solo_nL);
-        sh.red[0][2] = ld_relaxed_u32(&a.status->solo_nH);
-        sh.red[0][3] = ld_relaxed_u64((const unsigned long long*)&a.status->solo_mf);
-        sh.work = 0u;
-      }
-      __syncthreads();
-      d = (int)sh.lvl[0];
-      dir = (int)sh.lvl[1];
-      sel = (int)sh.lvl[2];
-      c_old = sh.lvl[4];
-      m_u = sh.lvl[5];
-      reached = (long long)sh.red[0][0];
-      nL = (unsigned)sh.red[0][1];
-      nH = (unsigned)sh.red[0][2];
-      mf_last = (long long)sh.red[0][3];
-      const bool finished = sh.lvl[3] != 0;
-      __syncthreads();
-      solo = false;
-      if (finished) break;
-      --d;  // the loop increment brings d to the published next level
-      continue;
-    }
     const long long t_lvl = (a.dbg && threadIdx.x == 0) ? (long long)global_timer_ns() : 0;
     LevelCtr* out = &a.ctr[d & (kRing - 1)];
     if (blockIdx.x == 0 && threadIdx.x < sizeof(LevelCtr) / 4)
@@ -998,9 +971,9 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
     uint32_t* vis_other = cur ? a.vis0 : a.vis1;
     if (dir == 0) {
       push_phase<Off, PARENTS>(a, sel ? a.L1 : a.L0, from_bits ? 0u : nL, sel ? a.H1 : a.H0,
-                               from_bits ? 0u : nH, from_bits ? a.fr : nullptr,
+                               from_bits ? 0u : nH, from_bits ? 0u : nB, from_bits ? a.fr : nullptr,
                                sel ? a.L0 : a.L1, sel ? a.H0 : a.H1, out, vis, d + 1, acc,
-                               &sh.work, solo, (unsigned long long)mf_last <= kLowLatEdges);
+                               &sh.work, (unsigned long long)mf_last <= kLowLatEdges);
       from_bits = false;
     } else {
       if (kSumWordsMax) {
@@ -1011,19 +984,14 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
                                ssum, &sh.work);
     }
     flush_acc(acc, out, sh.red);
-    if (solo) {
-      __threadfence_block();
-      __syncthreads();
-      if (threadIdx.x == 0) st_release_gpu(&a.bar->gen, (unsigned)d);  // heartbeat
-    } else {
-      if (a.dbg && threadIdx.x == 0 && d - 1 < a.dbg_levels)
-        a.dbg[(size_t)(d - 1) * gridDim.x + blockIdx.x] = (long long)global_timer_ns() - t_lvl;
-      if (!grid_barrier(a.bar, a.status, epoch)) return;
-    }
+    if (a.dbg && threadIdx.x == 0 && d - 1 < a.dbg_levels)
+      a.dbg[(size_t)(d - 1) * gridDim.x + blockIdx.x] = (long long)global_timer_ns() - t_lvl;
+    if (!grid_barrier(a.bar, a.status, epoch)) return;
     read_level(out, sh);
     const long long c_new = sh.lvl[0], mf = sh.lvl[1], mfin = sh.lvl[2];
     nL = (unsigned)sh.lvl[3];
     nH = (unsigned)sh.lvl[4];
+    nB = (unsigned)sh.lvl[6];
     if (dir == 1) cur ^= 1;
     else sel ^= 1;
     m_u -= a.symmetric ? mf : mfin;
@@ -1042,27 +1010,6 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
     int next = dir;
     if (!done && a.mode == 0)
       next = decide(a.rule, dir, c_old, c_new, mf, m_u, a.n, a.alpha, a.beta);
-    const bool solo_next = kSoloEdges && !done && dir == 0 && next == 0 &&
-                           (unsigned long long)mf <= kSoloEdges;
-    if (solo && !solo_next) {
-      // CTA 0 ends its solo run: publish the loop state for level d+1, release the others
-      if (threadIdx.x == 0) {
-        a.status->solo_d = d + 1;
-        a.status->solo_dir = next;
-        a.status->solo_sel = sel;
-        a.status->solo_finished = done ? 1 : 0;
-        a.status->solo_c_old = c_new;
-        a.status->solo_m_u = m_u;
-        a.status->solo_reached = reached;
-        a.status->solo_nL = nL;
-        a.status->solo_nH = nH;
-        a.status->solo_mf = mf;
-      }
-      if (!grid_barrier(a.bar, a.status, epoch)) return;
-      solo = false;
-    } else if (!solo && solo_next) {
-      solo = true;
-    }
     if (done) break;
     if (dir == 1 && next == 0 && sh.lvl[5] == 0) {
       from_bits = true;  // every new frontier vertex is light: push straight from `fr`
@@ -1076,6 +1023,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       read_level(out, sh);
       nL = (unsigned)sh.lvl[3];
       nH = (unsigned)sh.lvl[4];
+      nB = (unsigned)sh.lvl[6];
     }
     dir = next;
     c_old = c_new;
@@ -1084,6 +1032,12 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.status->levels = d;
     a.status->reached = reached;
+  }
+  if (PARENTS && a.perm) {  // relabelled graph: internal parents -> caller ids (after the
+    for (unsigned long long i = gtid; i < (unsigned long long)a.n; i += gsize) {  // last barrier)
+      const uint32_t p = a.parent[i];
+      a.pout[a.perm[i]] = p == 0xFFFFFFFFu ? p : a.perm[p];
+    }
   }
 }
 
@@ -1148,8 +1102,12 @@ static cudaError_t launch_off(pp_graph g, uint32_t source, int mode, int rule, d
   a.L1 = reinterpret_cast<uint4*>(g->L[1]);
   a.H0 = g->H[0];
   a.H1 = g->H[1];
+  a.hcap = (unsigned)g->hcap;
   a.depth = depth;
-  a.parent = parent;
+  a.parent = (parent && g->perm) ? g->pint : parent;
+  a.pout = parent;
+  a.perm = g->perm;
+  a.rank = g->rank;
   a.ctr = g->ctr;
   a.stats = g->stats;
   a.stats_cap = g->stats_cap;

@@ -73,7 +73,8 @@ void free_graph(pp_graph g) {
                   g->symmetric ? nullptr : (void*)g->cidx, g->isolated, g->head, g->vis[0], g->vis[1], g->fr, g->sumv,
                   g->L[0], g->L[1], g->H[0], g->H[1], g->ctr, g->stats, g->bar,
                   g->sbits[0], g->sbits[1], g->sbits[2], g->sbits[3], g->sblock, g->hubq, g->scount,
-                  g->dtmp[0], g->dtmp[1], g->dbg,
+                  g->dtmp[0], g->dtmp[1], g->dbg, g->perm, g->rank, g->pint,
+                  g->rbits[0], g->rbits[1], g->rbits[2], g->rbits[3],
                   g->dvis, g->dfr, g->dnxt, g->diso, g->pbeg, g->pend, g->dcnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -274,6 +275,29 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr
                 "row is not strictly increasing)",
                 side ? "CSC" : "CSR", (unsigned long long)g->scount_host[0]);
     }
+  }
+
+  // optional degree-ordered relabelling (relabel.cu): rows renumbered and re-sorted; the
+  // prepare kernels below then see only internal ids
+  if (flags & PP_GRAPH_RELABEL) {
+    if (ctx->nranks > 0)
+      PP_FAIL(PP_ERR_UNSUPPORTED, "pp_graph_upload: PP_GRAPH_RELABEL is single-GPU only");
+    if (nnz >= (int64_t)0x7FFFFFFF || n >= (int64_t)0x7FFFFFFF)
+      PP_FAIL(PP_ERR_UNSUPPORTED, "pp_graph_upload: PP_GRAPH_RELABEL needs nnz, n < 2^31");
+    if ((s = dalloc(&g->perm, (size_t)n, &bytes, "relabel perm")) != PP_OK) return s;
+    if ((s = dalloc(&g->rank, (size_t)n, &bytes, "relabel rank")) != PP_OK) return s;
+    if ((s = dalloc(&g->pint, (size_t)n, &bytes, "internal parents")) != PP_OK) return s;
+    for (int k = 0; k < 4; ++k)
+      if ((s = dalloc(&g->rbits[k], g->nwords, &bytes, "relabel scratch bitmap")) != PP_OK) return s;
+    int64_t junk = 0;
+    int64_t* noff = nullptr;
+    if ((s = dalloc(&noff, (size_t)(n + 1) * 2, &junk, "relabel offsets")) != PP_OK) return s;
+    const cudaError_t e = launch_relabel(g, d_off64, d_coff64, noff, noff + (n + 1), &ctx->launches);
+    if (g->dtmp[0]) cudaFree(g->dtmp[0]);
+    g->dtmp[0] = noff;  // freed with the other staging below
+    if (e != cudaSuccess) return cuda_fail(e, "relabel");
+    d_off64 = noff;
+    d_coff64 = symmetric ? noff : noff + (n + 1);
   }
 
   // narrowed offsets, isolated bitmap, heavy-chunk capacities
@@ -503,7 +527,28 @@ pp_status pp_mxv(pp_graph g, pp_vector* w, const pp_descriptor* desc, const pp_v
     }
     p.win_bits = g->sbits[3];
   }
+  uint32_t* out_caller = p.out_bits;
+  if (g->perm) {
+    // relabelled graph: every operand as an internal-id bitmap, result mapped back
+    const uint32_t* ub = p.u_bits;
+    if (!ub) {
+      PP_CK(launch_list_to_bitmap(g, p.u_list, p.u_nnz, g->sbits[1], bad), "u list->bitmap");
+      ub = g->sbits[1];
+    }
+    PP_CK(launch_permute_bits(g, ub, true, g->rbits[0]), "permute u");
+    p.u_bits = g->rbits[0];
+    p.u_list = nullptr;
+    p.u_nnz = 0;
+    if (p.mask_bits) {
+      PP_CK(launch_permute_bits(g, p.mask_bits, true, g->rbits[1]), "permute mask");
+      p.mask_bits = g->rbits[1];
+    }
+    if (need_win) PP_CK(launch_permute_bits(g, p.win_bits, true, g->rbits[2]), "permute w_in");
+    p.win_bits = need_win ? g->rbits[2] : g->rbits[3];
+    p.out_bits = g->rbits[3];
+  }
   PP_CK(launch_mxv(g, p), "mxv kernels");
+  if (g->perm) PP_CK(launch_permute_bits(g, g->rbits[3], false, out_caller), "permute w");
 
   if (w->format == PP_VEC_LIST) {
     PP_CK(launch_bitmap_to_list(g, g->sbits[3], (uint32_t*)w->data, w->capacity, g->scount), "bitmap->list");

@@ -14,16 +14,13 @@ constexpr int kBlock = 256;        // threads per CTA of every kernel
 constexpr int kWarps = kBlock / 32;
 constexpr unsigned kHeavy = 128;   // out-degree >= kHeavy: expanded as kChunk-edge chunks
 constexpr unsigned kChunk = 128;   // edges per heavy chunk = one 4-deep warp iteration
+constexpr unsigned kSelfChunks = 32;  // heavy vertices with more chunks are hubs (block
+                                      // descriptors, one per 32 chunks)
 constexpr int kRing = 4;           // level-counter ring
 #ifndef PP_SUM_WORDS
 #define PP_SUM_WORDS 0
 #endif
 constexpr unsigned kSumWordsMax = PP_SUM_WORDS;  // visited summary words in shared memory (0 = off)
-#ifndef PP_SOLO_EDGES
-#define PP_SOLO_EDGES 0
-#endif
-constexpr unsigned kSoloEdges = PP_SOLO_EDGES;  // push levels expanding <= this many edges
-                                                // run in CTA 0 alone (0 = never)
 #ifndef PP_LOWLAT_EDGES
 #define PP_LOWLAT_EDGES 32768
 #endif
@@ -45,7 +42,8 @@ struct LevelCtr {
   unsigned int nL, nH;       // next frontier: light-list length, heavy-chunk count
   unsigned int work, work2;  // dynamic work counters (phase, convert phase)
   unsigned long long nbig;   // discoveries with out-degree >= kBig (pull levels)
-  unsigned int pad[4];
+  unsigned int nB;           // next frontier: hub block descriptors (32 chunks each)
+  unsigned int pad[3];
 };
 static_assert(sizeof(LevelCtr) == 64, "LevelCtr layout");
 
@@ -69,10 +67,6 @@ struct BfsStatus {
   int levels;  // levels executed
   long long reached;
   long long t_start, t_init;  // %globaltimer at kernel entry / after the init barrier
-  // level-loop state handed back by CTA 0 at the end of a solo run
-  int solo_d, solo_dir, solo_sel, solo_finished;
-  long long solo_c_old, solo_m_u, solo_reached, solo_mf;
-  unsigned solo_nL, solo_nH;
 };
 
 }  // namespace pp
@@ -99,6 +93,11 @@ struct pp_graph_s {
   uint32_t* cidx = nullptr;
   uint32_t* isolated = nullptr;  // nwords: bit = no in- and no out-edges, or padding
   uint32_t* head = nullptr;      // 8n: first 8 in-neighbours of every row (pull heads)
+  // PP_GRAPH_RELABEL: internal id = rank by decreasing degree (relabel.cu)
+  uint32_t* perm = nullptr;  // internal -> caller id (nullptr: ids are the caller's)
+  uint32_t* rank = nullptr;  // caller -> internal id
+  uint32_t* pint = nullptr;  // BFS parents in internal ids (atomicMin key space)
+  uint32_t* rbits[4] = {nullptr, nullptr, nullptr, nullptr};  // mxv: u, mask, w_in, w (internal)
   // BFS working set
   uint32_t* vis[2] = {nullptr, nullptr};
   uint32_t* fr = nullptr;  // frontier bitmap of the last pull level
@@ -157,6 +156,9 @@ struct MxvPlan {
   const uint32_t* win_bits;  // w_in as bitmap (may alias out_bits)
   uint32_t* out_bits;        // result bitmap
 };
+cudaError_t launch_relabel(pp_graph g, const int64_t* d_off64, const int64_t* d_coff64,
+                           int64_t* new_off64, int64_t* new_coff64, uint64_t* launches);
+cudaError_t launch_permute_bits(pp_graph g, const uint32_t* in, bool to_internal, uint32_t* out);
 cudaError_t launch_list_to_bitmap(pp_graph g, const uint32_t* list, int64_t m, uint32_t* bits,
                                   unsigned long long* d_bad);
 cudaError_t launch_mxv(pp_graph g, const MxvPlan& p);

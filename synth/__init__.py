@@ -145,6 +145,19 @@ def sources(g: CSR, count: int, seed: int = 2) -> np.ndarray:
     return np.array(out, dtype=np.int64)
 
 
+def degree_order_key(g: CSR, gT: CSR = None) -> np.ndarray:
+    """Position of every vertex in the PP_GRAPH_RELABEL vertex order: decreasing degree
+    (out + in for a directed graph; ties by increasing id).  A data-layout definition used
+    by tests to state the relabelled graph's canonical parents (oracle.parents(key=...))."""
+    deg = g.degrees().astype(np.int64)
+    if gT is not None and not getattr(g, "symmetric", True):
+        deg = deg + gT.degrees().astype(np.int64)
+    order = np.argsort(-deg, kind="stable")
+    key = np.empty(g.n, dtype=np.uint32)
+    key[order] = np.arange(g.n, dtype=np.uint32)
+    return key
+
+
 def random_subset(n: int, count: int, seed: int) -> np.ndarray:
     """Exactly `count` distinct ids from [0,n), seeded (C3 mask protocol)."""
     rng = np.random.Generator(np.random.PCG64(seed))

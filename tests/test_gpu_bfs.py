@@ -41,7 +41,9 @@ def check(ctx, g, gT, G, s, mode, rule, toggles=0, parents=True, exp=None):
     assert np.array_equal(d, ed), f"depth mismatch src={s} mode={mode} rule={rule} t={toggles}: " \
         f"{np.nonzero(d != ed)[0][:10]}"
     if parents:
-        ep = oracle.parents(gT, ed, s)
+        # relabelled graphs: the valid parent first in the degree order (R14)
+        key = synth.degree_order_key(g, gT) if getattr(G, "relabel", False) else None
+        ep = oracle.parents(gT, ed, s, key=key)
         assert np.array_equal(par, ep), f"parent mismatch at {np.nonzero(par != ep)[0][:10]}"
     t = oracle.trace(g, gT, ed, mode=ORACLE_MODE[mode], rule=rule)
     assert st["levels"] == t["levels"] == L
@@ -74,17 +76,18 @@ def small_graphs():
 SMALL = small_graphs()
 
 
-def upload(ctx, g):
+def upload(ctx, g, relabel=False):
     if g.symmetric:
-        return pp.Graph.from_csr(ctx, g, validate=True), g
+        return pp.Graph.from_csr(ctx, g, validate=True, relabel=relabel), g
     gT = synth.transpose(g)
-    return pp.Graph.from_csr(ctx, g, gT, validate=True), gT
+    return pp.Graph.from_csr(ctx, g, gT, validate=True, relabel=relabel), gT
 
 
+@pytest.mark.parametrize("relabel", [False, True])
 @pytest.mark.parametrize("name", sorted(SMALL))
-def test_small_graphs_all_modes(ctx, name):
+def test_small_graphs_all_modes(ctx, name, relabel):
     g = SMALL[name]
-    G, gT = upload(ctx, g)
+    G, gT = upload(ctx, g, relabel)
     deg = np.diff(g.off)
     srcs = sorted(set([0, g.n - 1, int(np.argmax(deg))] + list(range(0, g.n, max(1, g.n // 5)))))
     for s in srcs:
@@ -93,12 +96,13 @@ def test_small_graphs_all_modes(ctx, name):
             check(ctx, g, gT, G, s, mode, rule, exp=exp)
 
 
+@pytest.mark.parametrize("relabel", [False, True])
 @pytest.mark.parametrize("toggles", [pp.PP_OPT_NO_EARLYEXIT, pp.PP_OPT_NO_MASKING, pp.PP_OPT_NO_REUSE,
                                      7])
-def test_toggles_do_not_change_results(ctx, toggles):
+def test_toggles_do_not_change_results(ctx, toggles, relabel):
     for name in ("rmat_s12", "directed_random", "path", "paper_fig3"):
         g = SMALL[name]
-        G, gT = upload(ctx, g)
+        G, gT = upload(ctx, g, relabel)
         for s in synth.sources(g, 4, seed=9):
             exp = oracle.bfs(g, s)
             for mode, rule in MODES:
@@ -113,10 +117,11 @@ def test_isolated_source(ctx):
         assert st["levels"] == 1 and st["reached"] == 1
 
 
-def test_c1_rmat_s16_64_sources(ctx):
+@pytest.mark.parametrize("relabel", [False, True])
+def test_c1_rmat_s16_64_sources(ctx, relabel):
     """Config C1: RMAT s16 ef16, 64 seeded sources, 4 direction policies, bit-exact."""
     g = synth.make("C1")
-    G = pp.Graph.from_csr(ctx, g, validate=True)
+    G = pp.Graph.from_csr(ctx, g, validate=True, relabel=relabel)
     for s in synth.sources(g, 64, seed=2):
         exp = oracle.bfs(g, s)
         for mode, rule in MODES:
@@ -165,15 +170,16 @@ def test_errors(ctx):
 
 
 @pytest.fixture(scope="module")
-def c2(ctx):
-    g = synth.make("C2")
-    return g, pp.Graph.from_csr(ctx, g)
+def c2g():
+    return synth.make("C2")
 
 
-def test_c2_rmat_s22_sampled_sources(ctx, c2):
-    """Config C2 at full size (the bench's launch configuration): oracle on 3 sources,
-    Graph500 validation (O5) + stats vs O4 on 8 more."""
-    g, G = c2
+@pytest.mark.parametrize("relabel", [True, False])
+def test_c2_rmat_s22_sampled_sources(ctx, c2g, relabel):
+    """Config C2 at full size (relabel=True is the bench's launch configuration): oracle on
+    3 sources, Graph500 validation (O5) + stats vs O4 on 8 more."""
+    g = c2g
+    G = pp.Graph.from_csr(ctx, g, relabel=relabel)
     srcs = synth.sources(g, 11, seed=2)
     for k, s in enumerate(srcs):
         if k < 3:
@@ -189,6 +195,7 @@ def test_c2_rmat_s22_sampled_sources(ctx, c2):
     exp = oracle.bfs(g, s)
     for mode, rule in MODES[1:]:
         check(ctx, g, g, G, s, mode, rule, exp=exp)
+    G.close()
 
 
 def test_c4_grid_closed_form(ctx):

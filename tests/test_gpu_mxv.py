@@ -63,11 +63,12 @@ GRAPHS = {
 }
 
 
+@pytest.mark.parametrize("relabel", [False, True])
 @pytest.mark.parametrize("gname", sorted(GRAPHS))
-def test_mxv_all_descriptor_combinations(ctx, gname):
+def test_mxv_all_descriptor_combinations(ctx, gname, relabel):
     g = GRAPHS[gname]()
     gT = synth.transpose(g)
-    G = pp.Graph.from_csr(ctx, g, None if g.symmetric else gT, validate=True)
+    G = pp.Graph.from_csr(ctx, g, None if g.symmetric else gT, validate=True, relabel=relabel)
     n = g.n
     rng = np.random.default_rng(len(gname))
     for trial in range(2):

@@ -216,6 +216,35 @@ def test_o2_min_over_all_valid_bfs_trees(seed):
             assert par[v] == min(t[v] for t in valid)
 
 
+@pytest.mark.parametrize("seed", range(8))
+def test_o2_ordered_min_key_over_all_valid_bfs_trees(seed):
+    """Ordered O2 (relabelled graphs): the valid parent first in a random vertex order."""
+    rng = np.random.default_rng(300 + seed)
+    n = int(rng.integers(2, 6))
+    A = (rng.random((n, n)) < 0.5).astype(np.int64)
+    np.fill_diagonal(A, 0)
+    if seed % 2:
+        A = A | A.T
+    g, gT = csr_from_dense(A), csr_from_dense(A.T)
+    key = rng.permutation(n).astype(np.uint32)
+    for s in range(n):
+        d, _ = oracle.bfs(g, s)
+        par = oracle.parents(gT, d, s, key=key)
+        valid = all_valid_parent_vectors(A, s, d)
+        assert tuple(par.tolist()) in valid
+        for v in range(n):
+            if d[v] > 0 and v != s:
+                assert key[par[v]] == min(key[t[v]] for t in valid)
+
+
+def test_o2_ordered_identity_key_is_min_id():
+    g = synth.rmat(11, 8, seed=4)
+    ident = np.arange(g.n, dtype=np.uint32)
+    for s in synth.sources(g, 3, seed=6):
+        d, _ = oracle.bfs(g, s)
+        assert np.array_equal(oracle.parents(g, d, s, key=ident), oracle.parents(g, d, s))
+
+
 def test_o2_rmat_passes_graph500_validation():
     g = synth.rmat(12, 8, seed=3)
     for s in synth.sources(g, 4, seed=5):

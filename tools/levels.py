@@ -14,7 +14,7 @@ t0 = time.time()
 g = synth.make(cfg)
 print(f"{cfg}: n={g.n} nnz={g.nnz} gen {time.time()-t0:.1f}s", flush=True)
 ctx = pp.Context(0)
-G = pp.Graph.from_csr(ctx, g)
+G = pp.Graph.from_csr(ctx, g, relabel="norelabel" not in sys.argv)
 depth = torch.empty(g.n, dtype=torch.int32, device="cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for s in synth.sources(g, 3, seed=7):
