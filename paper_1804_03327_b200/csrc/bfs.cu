@@ -110,7 +110,11 @@ __device__ __forceinline__ bool grid_barrier(GridBarrier* b, BfsStatus* st, unsi
         }
       }
     }
+#if PP_BAR_FENCE_SC
     __threadfence();
+#else
+    asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
     s_ok = (v & kAbortBit) ? 0 : 1;
   }
   __syncthreads();
@@ -164,6 +168,25 @@ __device__ __forceinline__ unsigned cta_grab(unsigned* sctr) {
   return blockIdx.x + j * gridDim.x;
 }
 __device__ __forceinline__ unsigned nwarps() { return gridDim.x * kBfsWarps; }
+
+// Visited prefix: every CTA copies the first `pw` words of the visited bitmap into shared
+// memory at the start of a heavy level (coalesced 16-byte loads, L2-resident source).  With
+// PP_GRAPH_RELABEL the low ids are the highest-degree vertices, so most visited probes of
+// a level (pull: a row's first in-neighbours; push: hub targets) are answered from shared
+// memory instead of a scattered L2 access.  Returns the number of bits covered.
+__device__ __forceinline__ uint32_t load_vprefix(const uint32_t* vis, uint32_t* svis,
+                                                 unsigned long long nwords) {
+  if (!kVPrefixWords) return 0u;
+  const unsigned pw = (unsigned)min((unsigned long long)kVPrefixWords, nwords) & ~3u;
+  const uint4* src = reinterpret_cast<const uint4*>(vis);
+  uint4* dst = reinterpret_cast<uint4*>(svis);
+  for (unsigned t = threadIdx.x; t < pw / 4u; t += blockDim.x) dst[t] = ld_relaxed_u4(src + t);
+  __syncthreads();
+  return pw * 32u;
+}
+__device__ __forceinline__ bool vprefix_bit(const uint32_t* svis, uint32_t x) {
+  return (svis[x >> 5] >> (x & 31u)) & 1u;
+}
 
 
 // Light frontier entry: the discovering thread already loaded the row's offsets, so the
@@ -285,7 +308,8 @@ template <typename Off, bool PARENTS>
 __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&valid)[kU],
                                             const uint32_t (&u)[kU], const uint32_t (&w)[kU],
                                             uint32_t* vis, int newdepth, uint4* Lout,
-                                            uint2* Hout, LevelCtr* out, Acc& acc, bool lowlat) {
+                                            uint2* Hout, LevelCtr* out, Acc& acc, bool lowlat,
+                                            const uint32_t* svis, uint32_t pbits) {
   uint32_t cur[kU];
   bool disc[kU];
   Off sb[kU], se[kU];
@@ -306,7 +330,8 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
     for (int t = 0; t < kU; ++t) disc[t] = valid[t] && !((cur[t] >> (w[t] & 31u)) & 1u);
   } else {
 #pragma unroll
-    for (int t = 0; t < kU; ++t) cur[t] = valid[t] ? vis[w[t] >> 5] : 0xFFFFFFFFu;
+    for (int t = 0; t < kU; ++t)  // visited at level start (prefix) or now (global)
+      cur[t] = !valid[t] ? 0xFFFFFFFFu : (w[t] < pbits ? svis[w[t] >> 5] : vis[w[t] >> 5]);
 #pragma unroll
     for (int t = 0; t < kU; ++t) {
       const uint32_t bit = 1u << (w[t] & 31u);
@@ -365,7 +390,8 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
 template <typename Off, bool PARENTS>
 __device__ __forceinline__ void push_round(const BfsArgs<Off>& a, uint32_t v, Off b, unsigned deg,
                                            uint4* Lout, uint2* Hout, LevelCtr* out,
-                                           uint32_t* vis, int newdepth, Acc& acc, bool lowlat) {
+                                           uint32_t* vis, int newdepth, Acc& acc, bool lowlat,
+                                           const uint32_t* svis, uint32_t pbits) {
   const unsigned lane = lane_id();
   const unsigned incl = warp_incl_scan(deg);
   const unsigned excl = incl - deg;
@@ -383,7 +409,8 @@ __device__ __forceinline__ void push_round(const BfsArgs<Off>& a, uint32_t v, Of
       valid[t] = e < tot;
       w[t] = valid[t] ? a.idx[bj + (Off)(e - xj)] : 0u;
     }
-    push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat);
+    push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat,
+                              svis, pbits);
   }
 }
 
@@ -404,7 +431,7 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
                            const uint2* Hin, unsigned nH, unsigned nB, const uint32_t* fr,
                            uint4* Lout,
                            uint2* Hout, LevelCtr* out, uint32_t* vis, int newdepth, Acc& acc,
-                           unsigned* sctr, bool lowlat) {
+                           unsigned* sctr, bool lowlat, const uint32_t* svis, uint32_t pbits) {
   const unsigned lane = lane_id();
   const unsigned NW = nwarps();
   unsigned R = 32;
@@ -434,7 +461,8 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
         u[t] = h.x;
         w[t] = valid[t] ? a.idx[p] : 0u;
       }
-      push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat);
+      push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat,
+                                svis, pbits);
     } else if (!fr) {
       const unsigned i = (item - nHC) * R + lane;
       uint32_t v = 0;
@@ -446,7 +474,8 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
         deg = le.y;
         b = light_begin<Off>(le);
       }
-      push_round<Off, PARENTS>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc, lowlat);
+      push_round<Off, PARENTS>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc, lowlat, svis,
+                               pbits);
     } else {
       const unsigned wbase = (item - nHC) * kPW;
       const uint32_t fw = lane < kPW ? fr[wbase + lane] : 0u;
@@ -467,7 +496,8 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
           b = a.off[v];
           deg = (unsigned)(a.off[v + 1] - b);
         }
-        push_round<Off, PARENTS>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc, lowlat);
+        push_round<Off, PARENTS>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc, lowlat, svis,
+                               pbits);
       }
     }
   }
@@ -479,7 +509,7 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
 constexpr int kC = PP_PULL_KC;  // candidates in flight per lane
 constexpr int kLaneMax = 16;    // residual rows with <= this many ids left: one lane each
 constexpr int kGroupMax = 512;   // <= this many: 8-lane groups; longer: the whole warp
-constexpr int kQ = 96;        // residual-queue entries per warp (31 + 32*kC fits)
+constexpr int kQ = 32 * kC + 64;  // residual-queue entries per warp (31 + 32*kC fits)
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 // Rows whose first sector did not decide them, parked per warp in shared memory and
@@ -525,12 +555,15 @@ struct PullCtx {
   uint32_t* sfound;
   ResidualQ<Off>& q;
   const uint32_t* ssum;  // shared-memory copy of the visited summary (snapshot)
+  const uint32_t* svis;  // shared-memory copy of the snapshot's first pbits bits
+  uint32_t pbits;
 
   // Visited test of a probed neighbour.  The summary in shared memory rejects most
   // unvisited neighbours without a global access (false positives only: a set summary
   // bit is confirmed against the exact snapshot bitmap).
   __device__ __forceinline__ bool hit(uint32_t x) const {
     if (no_reuse) return a.depth[a.perm ? a.perm[x] : x] == d;
+    if (x < pbits) return vprefix_bit(svis, x);
     if (kSumWordsMax) {
       const uint32_t gi = x >> a.sum_shift;
       if (!((ssum[gi >> 5] >> (gi & 31u)) & 1u)) return false;
@@ -594,7 +627,7 @@ struct PullCtx {
     acc.big += deg >= (Off)kBig ? 1u : 0u;
   }
   // process the top `cnt` (<= 32) residual rows, one per lane
-  __device__ void residual_batch(int& qn, int cnt, unsigned wbase, bool item_open) const {
+  __device__ void residual_batch(int& qn, int cnt, unsigned wbase, unsigned pw) const {
     const unsigned lane = lane_id();
     const int slot = qn - cnt + (int)lane;
     const bool valid = (int)lane < cnt;
@@ -691,7 +724,7 @@ struct PullCtx {
       }
     }
     if (valid && found && !committed) {
-      const bool in_item = item_open && (i >> 5) >= wbase && (i >> 5) < wbase + kPW;
+      const bool in_item = (i >> 5) >= wbase && (i >> 5) < wbase + pw;
       commit(i, par, (Off)degin, wbase, in_item, a.perm ? a.perm[i] : i);
     }
   }
@@ -712,18 +745,50 @@ template <typename Off, bool PARENTS>
 __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
                            uint32_t* __restrict__ vout, LevelCtr* out, int d, Acc& acc,
                            uint32_t* sfound, ResidualQ<Off>& rq, const uint32_t* ssum,
-                           unsigned* sctr) {
+                           unsigned* sctr, const uint32_t* svis, uint32_t pbits) {
   const unsigned lane = lane_id();
   const unsigned nitems = a.nwords / kPW;
   const bool no_mask = (a.toggles & PP_OPT_NO_MASKING) != 0;
   PullCtx<Off, PARENTS> C{a, vin, vout, d, !(a.toggles & PP_OPT_NO_EARLYEXIT),
-                          (a.toggles & PP_OPT_NO_REUSE) != 0, acc, sfound, rq, ssum};
+                          (a.toggles & PP_OPT_NO_REUSE) != 0, acc, sfound, rq, ssum,
+                          svis, pbits};
   int qn = 0;
   unsigned wbase = 0;
-  for (unsigned item = cta_grab(sctr); item < nitems; item = cta_grab(sctr)) {
-    wbase = item * kPW;
-    const bool own = lane < kPW;
-    const uint32_t vw = own ? vin[wbase + lane] : 0xFFFFFFFFu;
+  // Guided schedule.  CTA b owns items b, b+G, ... (G = grid); its warps grab them in order
+  // through the shared-memory counter.  A kPW-word item is a chain of ~kPW*16/32 dependent
+  // candidate rounds, so a whole item as the last work of a phase leaves the CTA's other
+  // warps idle at the level barrier: the CTA's last kPullTail items are therefore handed
+  // out one bitmap word (32 rows) at a time.  The warp also grabs one step ahead and loads
+  // the next item's visited words while this one is processed.
+  const unsigned G = gridDim.x;
+  const unsigned J = nitems > blockIdx.x ? (nitems - blockIdx.x + G - 1) / G : 0u;
+  const unsigned T = min(J, kPullTail), JH = J - T, K = JH + T * kPW;
+  auto map = [&](unsigned k, unsigned& w0, unsigned& pw) {
+    if (k < JH) {
+      w0 = (blockIdx.x + k * G) * kPW;
+      pw = kPW;
+    } else {
+      const unsigned kk = k - JH;
+      w0 = (blockIdx.x + (JH + kk / kPW) * G) * kPW + kk % kPW;
+      pw = 1u;
+    }
+  };
+  auto grab = [&]() {
+    unsigned j = 0;
+    if (lane == 0) j = atomicAdd(sctr, 1u);
+    return __shfl_sync(kFull, j, 0);
+  };
+  unsigned k = grab(), w0n = 0, pwn = 0;
+  if (k < K) map(k, w0n, pwn);
+  uint32_t vw_next = (k < K && lane < pwn) ? vin[w0n + lane] : 0xFFFFFFFFu;
+  while (k < K) {
+    wbase = w0n;
+    const unsigned pw = pwn;
+    const bool own = lane < pw;
+    const uint32_t vw = vw_next;
+    k = grab();
+    if (k < K) map(k, w0n, pwn);
+    vw_next = (k < K && lane < pwn) ? vin[w0n + lane] : 0xFFFFFFFFu;
     const uint32_t unvisited = ~vw;
     // Masking (Opt. 2): only rows with !v(i) are computed.  Without it every
     // non-isolated row is computed and the result filtered afterwards.
@@ -812,9 +877,15 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
         qn += __popc(pm);
       }
       __syncwarp();
-      while (qn >= 32) C.residual_batch(qn, 32, wbase, true);
+      while (qn >= 32) C.residual_batch(qn, 32, wbase, pw);
     }
-    if (qn > 0) C.residual_batch(qn, qn, wbase, true);
+#if PP_PULL_CARRY
+    // residual rows (< 32) carry over into the next item and are committed with atomicOr
+    // once their item has closed, so a partial batch (one more dependent chain) is paid
+    // once per phase instead of once per item
+#else
+    if (qn > 0) C.residual_batch(qn, qn, wbase, pw);
+#endif
     __syncwarp();
     const uint32_t fw = own ? sfound[lane] : 0u;
     if (own) {
@@ -834,6 +905,7 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
     }
     __syncwarp();
   }
+  if (qn > 0) C.residual_batch(qn, qn, wbase, 0u);  // items closed: atomicOr commits
 }
 
 // Dense2sparse of the new frontier v' & !v after a pull level (pull->push switch).
@@ -904,6 +976,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   ResidualQ<Off>* rqs = reinterpret_cast<ResidualQ<Off>*>(dyn_smem);
   uint32_t* ssum = reinterpret_cast<uint32_t*>(dyn_smem + sizeof(ResidualQ<Off>) * kBfsWarps);
+  uint32_t* svis = ssum + kSumWordsMax;
   const unsigned warp = threadIdx.x >> 5;
   const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned long long gsize = (unsigned long long)gridDim.x * blockDim.x;
@@ -969,11 +1042,14 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       reinterpret_cast<unsigned*>(&a.ctr[(d + 1) & (kRing - 1)])[threadIdx.x] = 0u;
     uint32_t* vis = cur ? a.vis1 : a.vis0;
     uint32_t* vis_other = cur ? a.vis0 : a.vis1;
+    const bool heavy_level = dir == 0 ? (unsigned long long)mf_last >= kVPrefixMinEdges
+                                      : (unsigned long long)m_u >= kVPrefixMinEdges;
+    const uint32_t pbits = (heavy_level && a.perm) ? load_vprefix(vis, svis, a.nwords) : 0u;
     if (dir == 0) {
       push_phase<Off, PARENTS>(a, sel ? a.L1 : a.L0, from_bits ? 0u : nL, sel ? a.H1 : a.H0,
                                from_bits ? 0u : nH, from_bits ? 0u : nB, from_bits ? a.fr : nullptr,
                                sel ? a.L0 : a.L1, sel ? a.H0 : a.H1, out, vis, d + 1, acc,
-                               &sh.work, (unsigned long long)mf_last <= kLowLatEdges);
+                               &sh.work, (unsigned long long)mf_last <= kLowLatEdges, svis, pbits);
       from_bits = false;
     } else {
       if (kSumWordsMax) {
@@ -981,7 +1057,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
         __syncthreads();
       }
       pull_phase<Off, PARENTS>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp],
-                               ssum, &sh.work);
+                               ssum, &sh.work, svis, pbits);
     }
     flush_acc(acc, out, sh.red);
     if (a.dbg && threadIdx.x == 0 && d - 1 < a.dbg_levels)
@@ -1043,7 +1119,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
 
 template <typename Off>
 constexpr size_t dyn_smem_bytes() {
-  return sizeof(ResidualQ<Off>) * kBfsWarps + sizeof(uint32_t) * kSumWordsMax;
+  return sizeof(ResidualQ<Off>) * kBfsWarps + sizeof(uint32_t) * (kSumWordsMax + kVPrefixWords);
 }
 
 template <typename Off, bool PARENTS>

@@ -33,6 +33,29 @@ constexpr unsigned kBig = 1024;    // pull->push goes straight from the bitmap i
 #endif
 constexpr int kBfsBlock = PP_BFS_BLOCK;  // persistent BFS: one CTA per SM
 constexpr int kBfsWarps = kBfsBlock / 32;
+#ifndef PP_PULL_TAIL
+#define PP_PULL_TAIL 0
+#endif
+constexpr unsigned kPullTail = PP_PULL_TAIL;  // pull: a CTA's last kPullTail items are handed
+                                              // out one bitmap word at a time (guided schedule)
+#ifndef PP_PULL_CARRY
+#define PP_PULL_CARRY 0
+#endif
+#ifndef PP_VPREFIX_WORDS
+#define PP_VPREFIX_WORDS 0
+#endif
+constexpr unsigned kVPrefixWords = PP_VPREFIX_WORDS;  // BFS: shared-memory copy of the first
+                                  // 32*kVPrefixWords bits of the visited bitmap at level start
+                                  // (with PP_GRAPH_RELABEL: the highest-degree vertices, the
+                                  // targets of most probes); 0 = off
+#ifndef PP_VPREFIX_MIN_EDGES
+#define PP_VPREFIX_MIN_EDGES 262144
+#endif
+constexpr unsigned long long kVPrefixMinEdges = PP_VPREFIX_MIN_EDGES;  // ... only for levels
+                                  // whose work (push: m_f; pull: m_u) is at least this
+#ifndef PP_BAR_FENCE_SC
+#define PP_BAR_FENCE_SC 1
+#endif
 
 // Per-level counters, written with atomics during a level, read after the grid barrier.
 struct LevelCtr {

@@ -10,7 +10,7 @@ src = int(sys.argv[2]) if len(sys.argv) > 2 else 2764614
 W = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 g = synth.make(cfg)
 ctx = pp.Context(0)
-G = pp.Graph.from_csr(ctx, g)
+G = pp.Graph.from_csr(ctx, g, relabel="norelabel" not in sys.argv)
 depth = torch.empty(g.n, dtype=torch.int32, device="cuda")
 for _ in range(W):
     pp.bfs(G, src, depth)
