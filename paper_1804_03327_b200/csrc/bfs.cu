@@ -121,6 +121,10 @@ __device__ __forceinline__ bool grid_barrier(GridBarrier* b, BfsStatus* st, unsi
   return s_ok != 0;
 }
 
+// This CTA's contributions to the next frontier's list lengths in the current phase
+// (light entries, heavy chunk descriptors, hub block descriptors), published by level_sync.
+__shared__ unsigned s_app[3];
+
 // Per-lane accumulators of a level's counters, flushed once per phase.
 struct Acc {
   unsigned long long c, mf, mfin, big;
@@ -219,8 +223,14 @@ __device__ __forceinline__ void heavy_bases(unsigned CS, unsigned CB, LevelCtr* 
   const unsigned ts = __shfl_sync(kFull, is, 31), tb = __shfl_sync(kFull, ib, 31);
   unsigned bs = 0, bb = 0;
   if (lane_id() == 0) {
-    if (ts) bs = atomicAdd(&out->nH, ts);
-    if (tb) bb = atomicAdd(&out->nB, tb);
+    if (ts) {
+      bs = atomicAdd(&out->nH, ts);
+      if (kCountingSync) atomicAdd(&s_app[1], ts);
+    }
+    if (tb) {
+      bb = atomicAdd(&out->nB, tb);
+      if (kCountingSync) atomicAdd(&s_app[2], tb);
+    }
   }
   s0 = __shfl_sync(kFull, bs, 0) + is - CS;
   b0 = __shfl_sync(kFull, bb, 0) + ib - CB;
@@ -244,7 +254,10 @@ __device__ __forceinline__ void append_frontier(bool valid, uint32_t v, Off deg,
   unsigned lm = __ballot_sync(kFull, light);
   if (lm) {
     unsigned leader = __ffs(lm) - 1, base = 0;
-    if (lane == leader) base = atomicAdd(&out->nL, (unsigned)__popc(lm));
+    if (lane == leader) {
+      base = atomicAdd(&out->nL, (unsigned)__popc(lm));
+      if (kCountingSync) atomicAdd(&s_app[0], (unsigned)__popc(lm));
+    }
     base = __shfl_sync(kFull, base, leader);
     if (light) Lout[base + __popc(lm & lanemask_lt())] = light_entry<Off>(v, deg, begin);
   }
@@ -275,7 +288,10 @@ __device__ __forceinline__ void append_frontier4(const bool (&disc)[kU], const u
   }
   if (ltot) {
     unsigned base = 0;
-    if (lane == 0) base = atomicAdd(&out->nL, ltot);
+    if (lane == 0) {
+      base = atomicAdd(&out->nL, ltot);
+      if (kCountingSync) atomicAdd(&s_app[0], ltot);
+    }
     base = __shfl_sync(kFull, base, 0);
 #pragma unroll
     for (int t = 0; t < kU; ++t) {
@@ -557,6 +573,8 @@ struct PullCtx {
   const uint32_t* ssum;  // shared-memory copy of the visited summary (snapshot)
   const uint32_t* svis;  // shared-memory copy of the snapshot's first pbits bits
   uint32_t pbits;
+  uint2* hubs;           // no early exit: long-row chunk descriptors (2 uint2 each) ...
+  unsigned* hub_count;   // ... and their count
 
   // Visited test of a probed neighbour.  The summary in shared memory rejects most
   // unvisited neighbours without a global access (false positives only: a set summary
@@ -698,12 +716,37 @@ struct PullCtx {
         p = rp;
       }
     }
-    // tier 2: long remainders, whole warp (256 ids per step: 8 per lane), ballot early exit
+    // tier 2: long remainders, whole warp (256 ids per step: 8 per lane), ballot early exit.
+    // Without early exit (the Table-2 ablation arms) a remainder longer than kHubSplit is
+    // not scanned here: it becomes kHubSplit-id chunk descriptors that every warp of the
+    // grid processes after the item loop (pull_hub_chunks), so the relabelled hubs, which
+    // share the first items, do not serialise in one warp.
     unsigned dm = __ballot_sync(kFull, valid && p < e && !(found && early_exit));
     while (dm) {
       const unsigned l = __ffs(dm) - 1;
       dm &= dm - 1;
       const Off pb = __shfl_sync(kFull, p, l), pe = __shfl_sync(kFull, e, l);
+      if (!early_exit && pe - pb > (Off)kHubSplit) {
+        const unsigned nch = (unsigned)((pe - pb + (Off)kHubSplit - 1) / (Off)kHubSplit);
+        unsigned base = 0;
+        // capacity: 3*ceil(rem/2048) <= deg/128 for deg > 2048, and hcap >= sum ceil(deg/128)
+        if (lane == 0) base = atomicAdd(hub_count, nch);
+        base = __shfl_sync(kFull, base, 0);
+        // row id (valid only when the row may still commit: unvisited, not yet found)
+        const uint32_t ri = __shfl_sync(kFull, i, l);
+        const bool may = __shfl_sync(kFull, (i < kNone - 1u && !committed) ? 1 : 0, l) != 0;
+        const uint32_t flags = __shfl_sync(kFull, degin & 0x7FFFFFFFu, l) | (may ? 0x80000000u : 0u);
+        for (unsigned j = lane; j < nch; j += 32) {
+          const Off q0 = pb + (Off)j * (Off)kHubSplit;
+          const unsigned len = (unsigned)min((Off)kHubSplit, pe - q0);
+          uint2* h = hubs + 3u * (base + j);
+          h[0] = make_uint2(ri, flags);
+          h[1] = make_uint2((uint32_t)q0, (uint32_t)((unsigned long long)q0 >> 32));
+          h[2] = make_uint2(len, 0u);
+        }
+        if (lane == l) p = e;  // handed over; `found` stays as it was (committed rows only)
+        continue;
+      }
       bool f = __shfl_sync(kFull, found ? 1 : 0, l) != 0;
       uint32_t fx = __shfl_sync(kFull, par, l);
       for (Off q0 = pb & ~(Off)7; q0 < pe; q0 += 256) {
@@ -751,7 +794,7 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
   const bool no_mask = (a.toggles & PP_OPT_NO_MASKING) != 0;
   PullCtx<Off, PARENTS> C{a, vin, vout, d, !(a.toggles & PP_OPT_NO_EARLYEXIT),
                           (a.toggles & PP_OPT_NO_REUSE) != 0, acc, sfound, rq, ssum,
-                          svis, pbits};
+                          svis, pbits, a.H0, &out->work2};
   int qn = 0;
   unsigned wbase = 0;
   // Guided schedule.  CTA b owns items b, b+G, ... (G = grid); its warps grab them in order
@@ -908,6 +951,60 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
   if (qn > 0) C.residual_batch(qn, qn, wbase, 0u);  // items closed: atomicOr commits
 }
 
+// No-early-exit pull, second part: the long-row chunks emitted by tier 2, grabbed by every
+// warp of the grid (global counter: few chunks).  A chunk scans its ids in full (no early
+// exit), takes its first hit in sorted order, and the row's commit happens once, by the
+// chunk whose atomicOr on v' flips the bit (the item owning the row has closed); the
+// min-id parent is the atomicMin of the chunks' first hits (R14).
+template <typename Off, bool PARENTS>
+__device__ void pull_hub_chunks(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
+                                uint32_t* __restrict__ vout, LevelCtr* out, unsigned nch, int d,
+                                Acc& acc, ResidualQ<Off>& rq, const uint32_t* svis,
+                                uint32_t pbits) {
+  const unsigned lane = lane_id();
+  PullCtx<Off, PARENTS> C{a, vin, vout, d, false, (a.toggles & PP_OPT_NO_REUSE) != 0, acc,
+                          nullptr, rq, nullptr, svis, pbits, a.H0, nullptr};
+  while (true) {
+    unsigned j = 0;
+    if (lane == 0) j = atomicAdd(&out->work, 1u);
+    j = __shfl_sync(kFull, j, 0);
+    if (j >= nch) break;
+    const uint2 h0 = a.H0[3u * j], h1 = a.H0[3u * j + 1u], h2 = a.H0[3u * j + 2u];
+    const uint32_t i = h0.x;
+    const bool may = (h0.y >> 31) != 0;  // row unvisited and not found yet (else: scan only)
+    const Off degin = (Off)(h0.y & 0x7FFFFFFFu);
+    const Off q0 = (Off)(((unsigned long long)h1.y << 32) | h1.x);
+    const Off e = q0 + (Off)h2.x;
+    bool f = false;
+    uint32_t fx = 0;
+    for (Off qb = q0 & ~(Off)7; qb < e; qb += 256) {
+      bool lf = false;
+      uint32_t lx = 0;
+      const Off qq = qb + (Off)(lane * 8u);
+      if (qq < e) C.probe8(qq, q0, e, lf, lx);
+      const unsigned bm = __ballot_sync(kFull, lf);
+      if (bm && !f) {
+        f = true;
+        fx = __shfl_sync(kFull, lx, __ffs(bm) - 1);
+      }
+    }
+    if (f && may && lane == 0) {
+      if (PARENTS) atomicMin(&a.parent[i], fx);
+      const uint32_t bit = 1u << (i & 31u);
+      const uint32_t old = atomicOr(&vout[i >> 5], bit);
+      if (!(old & bit)) {
+        atomicOr(&a.fr[i >> 5], bit);
+        a.depth[a.perm ? a.perm[i] : i] = d + 1;
+        const Off deg = a.symmetric ? degin : (Off)(a.off[i + 1] - a.off[i]);
+        acc.c += 1;
+        acc.mf += (unsigned long long)deg;
+        acc.mfin += (unsigned long long)degin;
+        acc.big += deg >= (Off)kBig ? 1u : 0u;
+      }
+    }
+  }
+}
+
 // Dense2sparse of the new frontier v' & !v after a pull level (pull->push switch).
 template <typename Off>
 __device__ void convert_phase(const BfsArgs<Off>& a, const uint32_t* vnew, const uint32_t* vold,
@@ -951,7 +1048,9 @@ struct BfsShared {  // static part; the residual queues live in dynamic shared m
   uint32_t sfound[kBfsWarps][32];
   unsigned long long red[kBfsWarps][4];
   long long lvl[7];  // c, m_f, m_fin, nL, nH, nbig, nB of the level just finished
+  unsigned long long vprev[2][7];  // level_sync: running sums of each slot at its last use
   unsigned work;     // CTA-local work counter (cta_grab)
+  int ok;
 };
 
 // thread 0 reads a level's counters once (post-barrier) and broadcasts them via smem
@@ -970,6 +1069,111 @@ __device__ __forceinline__ void read_level(const LevelCtr* out, BfsShared<Off>& 
   __syncthreads();
 }
 
+// Counting level sync: the end of every phase (init, level, Dense2sparse) in ONE exchange.
+// The CTA's counters (c, m_f, m_fin, nbig from the lanes; nL, nH, nB from s_app) are reduced
+// warp -> CTA; thread 0 then issues a release fence and adds (value << 24) + 1 to each of
+// the 8 words of slot (phase & 1) with fire-and-forget reductions, and polls the slot until
+// every word's low 24 bits show all G arrivals of this phase (mod 2^24: the arrival total
+// after u uses of a slot is u*G exactly, and a CTA is at most one phase ahead, hence two
+// slots).  The polled words themselves carry the level's totals, so the old sequence
+// (counter atomics, a release atomic that waits for them, the barrier poll, then a
+// separate load of the counters) loses one arrival round trip and the counter-read round
+// trip.  Fence-then-relaxed-add / relaxed-poll-then-fence is the release/acquire pattern
+// that publishes the phase's data writes (depths, bitmaps, lists) to every CTA.
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ ulonglong2 ld_relaxed_u64x2(const unsigned long long* p) {
+  ulonglong2 v;
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0,%1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
+  return v;
+}
+
+template <typename Off>
+__device__ __forceinline__ bool level_sync(Acc& acc, BfsShared<Off>& sh, GridBarrier* bar,
+                                           BfsStatus* st, unsigned& ph) {
+  const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+  const bool any = __any_sync(kFull, (acc.c | acc.mf | acc.mfin | acc.big) != 0ull);
+  unsigned long long c = 0, mf = 0, mfin = 0, big = 0;
+  if (any) {
+    c = warp_sum(acc.c);
+    mf = warp_sum(acc.mf);
+    mfin = warp_sum(acc.mfin);
+    big = warp_sum(acc.big);
+  }
+  if (lane == 0) {
+    sh.red[warp][0] = c;
+    sh.red[warp][1] = mf;
+    sh.red[warp][2] = mfin;
+    sh.red[warp][3] = big;
+  }
+  acc.c = acc.mf = acc.mfin = acc.big = 0;
+  __syncthreads();
+  if (warp == 0) {
+    const bool in = lane < (unsigned)kBfsWarps;
+    unsigned long long v[4];
+#pragma unroll
+    for (int f = 0; f < 4; ++f) v[f] = in ? sh.red[lane][f] : 0ull;
+    if (__any_sync(kFull, (v[0] | v[1] | v[2] | v[3]) != 0ull)) {
+#pragma unroll
+      for (int f = 0; f < 4; ++f) v[f] = warp_sum(v[f]);
+    }
+    if (lane == 0) {
+      const unsigned slot = ph & 1u;
+      unsigned long long* pk = &bar->pk[slot][0][0];  // word f at pk[f * kSyncStride]
+      const unsigned long long expect = (unsigned long long)(ph / 2u + 1u) * gridDim.x;
+      const unsigned long long vals[8] = {v[0], v[1], v[2], s_app[0], s_app[1], v[3], s_app[2], 0ull};
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");  // release this CTA's phase writes
+#pragma unroll
+      for (int f = 0; f < 8; ++f) red_add_u64(pk + f * kSyncStride, (vals[f] << 24) + 1ull);
+      unsigned long long w[8];
+      bool ok = true;
+      const unsigned long long t0 = global_timer_ns();
+      while (true) {
+        if (kSyncStride == 1) {
+#pragma unroll
+          for (int f = 0; f < 8; f += 2) {
+            const ulonglong2 x = ld_relaxed_u64x2(pk + f);
+            w[f] = x.x;
+            w[f + 1] = x.y;
+          }
+        } else {
+#pragma unroll
+          for (int f = 0; f < 8; ++f) w[f] = ld_relaxed_u64(pk + f * kSyncStride);
+        }
+        bool done = true;
+#pragma unroll
+        for (int f = 0; f < 8; ++f) done &= ((w[f] - expect) & 0xFFFFFFull) == 0ull;
+        if (done) break;
+        if (ld_relaxed_u64(&bar->count) & kAbortBit) {
+          ok = false;
+          break;
+        }
+        if (global_timer_ns() - t0 > kWatchdogNs) {
+          atomicExch(&st->error, (int)PP_ERR_TIMEOUT);
+          atomicOr(reinterpret_cast<unsigned long long*>(&bar->count), kAbortBit);
+          ok = false;
+          break;
+        }
+        __nanosleep(16);
+      }
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire every CTA's phase writes
+#pragma unroll
+      for (int f = 0; f < 7; ++f) {
+        const unsigned long long tot = (w[f] - expect) >> 24;  // running sum over this slot
+        sh.lvl[f] = (long long)(tot - sh.vprev[slot][f]);
+        sh.vprev[slot][f] = tot;
+      }
+      s_app[0] = s_app[1] = s_app[2] = 0u;
+      sh.work = 0u;
+      sh.ok = ok ? 1 : 0;
+      ++ph;
+    }
+  }
+  __syncthreads();
+  return sh.ok != 0;
+}
+
 template <typename Off, bool PARENTS>
 __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   __shared__ BfsShared<Off> sh;
@@ -983,6 +1187,11 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   const uint32_t s = a.rank ? a.rank[a.source] : a.source;  // internal id of the source
   if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t_start = (long long)global_timer_ns();
   unsigned epoch = 0;  // grid barriers passed (thread 0)
+  unsigned ph = 0;     // level_sync phases passed (thread 0)
+  if (kCountingSync && threadIdx.x == 0) {
+    for (int f = 0; f < 7; ++f) sh.vprev[0][f] = sh.vprev[1][f] = 0ull;
+    s_app[0] = s_app[1] = s_app[2] = 0u;
+  }
 
   // ---- Alg. 1 lines 2-4: d <- 1, f <- e_s, v <- 0 (depth 0 = unvisited) ----
   for (unsigned long long v = gtid; v < (unsigned long long)a.n; v += gsize) {
@@ -1007,21 +1216,26 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       const unsigned nch = (unsigned)((deg + (Off)kChunk - 1) / (Off)kChunk);
       if (nch <= kSelfChunks) {
         for (unsigned k = threadIdx.x; k < nch; k += blockDim.x) a.H0[k] = make_uint2(s, k);
-        if (threadIdx.x == 0) a.ctr[0].nH = nch;
+        if (threadIdx.x == 0) a.ctr[0].nH = s_app[1] = nch;
       } else {
         const unsigned nb = (nch + 31u) / 32u;
         for (unsigned j = threadIdx.x; j < nb; j += blockDim.x)
           a.H0[a.hcap - 1u - j] = make_uint2(s, 32u * j);
-        if (threadIdx.x == 0) a.ctr[0].nB = nb;
+        if (threadIdx.x == 0) a.ctr[0].nB = s_app[2] = nb;
       }
     } else if (deg > 0 && threadIdx.x == 0) {
       a.L0[0] = light_entry<Off>(s, deg, a.off[s]);
-      a.ctr[0].nL = 1;
+      a.ctr[0].nL = s_app[0] = 1;
     }
   }
-  if (!grid_barrier(a.bar, a.status, epoch)) return;
+  if (kCountingSync) {
+    Acc acc0{0, 0, 0, 0};
+    if (!level_sync<Off>(acc0, sh, a.bar, a.status, ph)) return;
+  } else {
+    if (!grid_barrier(a.bar, a.status, epoch)) return;
+    read_level(&a.ctr[0], sh);
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t_init = (long long)global_timer_ns();
-  read_level(&a.ctr[0], sh);
   unsigned nL = (unsigned)sh.lvl[3], nH = (unsigned)sh.lvl[4], nB = (unsigned)sh.lvl[6];
 
   int dir = (a.mode == 2) ? 1 : 0;
@@ -1058,12 +1272,22 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       }
       pull_phase<Off, PARENTS>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp],
                                ssum, &sh.work, svis, pbits);
+      if (a.toggles & PP_OPT_NO_EARLYEXIT) {  // ablation arms: long rows grid-wide
+        if (!grid_barrier(a.bar, a.status, epoch)) return;
+        const unsigned nch = ld_relaxed_u32(&out->work2);
+        if (nch) pull_hub_chunks<Off, PARENTS>(a, vis, vis_other, out, nch, d, acc, rqs[warp], svis,
+                                                pbits);
+      }
     }
-    flush_acc(acc, out, sh.red);
     if (a.dbg && threadIdx.x == 0 && d - 1 < a.dbg_levels)
       a.dbg[(size_t)(d - 1) * gridDim.x + blockIdx.x] = (long long)global_timer_ns() - t_lvl;
-    if (!grid_barrier(a.bar, a.status, epoch)) return;
-    read_level(out, sh);
+    if (kCountingSync) {
+      if (!level_sync<Off>(acc, sh, a.bar, a.status, ph)) return;
+    } else {
+      flush_acc(acc, out, sh.red);
+      if (!grid_barrier(a.bar, a.status, epoch)) return;
+      read_level(out, sh);
+    }
     const long long c_new = sh.lvl[0], mf = sh.lvl[1], mfin = sh.lvl[2];
     nL = (unsigned)sh.lvl[3];
     nH = (unsigned)sh.lvl[4];
@@ -1095,8 +1319,12 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       uint32_t* vnew = cur ? a.vis1 : a.vis0;
       uint32_t* vold = cur ? a.vis0 : a.vis1;
       convert_phase<Off>(a, vnew, vold, sel ? a.L1 : a.L0, sel ? a.H1 : a.H0, out, &sh.work);
-      if (!grid_barrier(a.bar, a.status, epoch)) return;
-      read_level(out, sh);
+      if (kCountingSync) {
+        if (!level_sync<Off>(acc, sh, a.bar, a.status, ph)) return;
+      } else {
+        if (!grid_barrier(a.bar, a.status, epoch)) return;
+        read_level(out, sh);
+      }
       nL = (unsigned)sh.lvl[3];
       nH = (unsigned)sh.lvl[4];
       nB = (unsigned)sh.lvl[6];

@@ -26,6 +26,8 @@ constexpr unsigned kSumWordsMax = PP_SUM_WORDS;  // visited summary words in sha
 #endif
 constexpr unsigned long long kLowLatEdges = PP_LOWLAT_EDGES;  // push levels expanding <= this
                                   // many edges: speculative offsets, no pre-test before atomicOr
+constexpr unsigned kHubSplit = 2048;  // no-early-exit pull: longer row remainders are
+                                      // processed grid-wide in chunks of this many ids
 constexpr unsigned kBig = 1024;    // pull->push goes straight from the bitmap if no new
                                    // frontier vertex has out-degree >= kBig
 #ifndef PP_BFS_BLOCK
@@ -53,6 +55,11 @@ constexpr unsigned kVPrefixWords = PP_VPREFIX_WORDS;  // BFS: shared-memory copy
 #endif
 constexpr unsigned long long kVPrefixMinEdges = PP_VPREFIX_MIN_EDGES;  // ... only for levels
                                   // whose work (push: m_f; pull: m_u) is at least this
+#ifndef PP_COUNTING_SYNC
+#define PP_COUNTING_SYNC 0
+#endif
+constexpr bool kCountingSync = PP_COUNTING_SYNC != 0;  // bfs: level_sync instead of
+                                  // counter atomics + grid barrier + counter read
 #ifndef PP_BAR_FENCE_SC
 #define PP_BAR_FENCE_SC 1
 #endif
@@ -77,11 +84,20 @@ struct LevelStat {
   long long t_ns;  // %globaltimer when the level's barrier released (block 0)
 };
 
+#ifndef PP_SYNC_STRIDE
+#define PP_SYNC_STRIDE 32
+#endif
+constexpr int kSyncStride = PP_SYNC_STRIDE;
 struct GridBarrier {
   unsigned long long count;  // monotone arrival counter (bit 63: abort), zeroed per launch
   unsigned int pad0[30];
   unsigned int gen;
   unsigned int pad1[31];
+  // counting level sync (bfs.cu level_sync): two alternating slots of 8 words; every CTA
+  // adds (value << 24) + 1 to each word once per phase, so a word carries its own arrival
+  // count (low 24 bits) next to the running sum of the per-CTA values (zeroed per launch)
+  unsigned long long pk[2][8][kSyncStride];  // word f of slot s at pk[s][f][0]: one word per
+                                             // kSyncStride*8 bytes, spread over L2 slices
 };
 
 // Device-side BFS status words.

@@ -23,7 +23,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
         tmp = _SO + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O3", "-march=x86-64-v2", "-fopenmp", "-fPIC", "-shared",
-                               "-o", tmp, _SRC])
+                               "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _SO)
     return _SO
 
@@ -49,6 +49,8 @@ def _load():
         lib.synth_percolated_grid.restype = GP
         lib.synth_percolated_grid.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_double,
                                               ctypes.c_uint64]
+        lib.synth_rgg.restype = GP
+        lib.synth_rgg.argtypes = [ctypes.c_int, ctypes.c_double, ctypes.c_uint64]
         lib.synth_from_edges.restype = GP
         lib.synth_from_edges.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_void_p,
                                          ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
@@ -103,6 +105,12 @@ def grid(rows: int, cols: int) -> CSR:
 def percolated_grid(rows: int, cols: int, p: float = 0.6, seed: int = 1) -> CSR:
     return _take(_load().synth_percolated_grid(rows, cols, p, seed), True,
                  f"pgrid_{rows}x{cols}_p{p}")
+
+
+def rgg(scale: int, factor: float = 0.55, seed: int = 1) -> CSR:
+    """Random geometric graph: 2^scale uniform points in the unit square, edges at distance
+    <= factor*sqrt(ln n / n) (rgg_n_2_24_s0 shape)."""
+    return _take(_load().synth_rgg(scale, factor, seed), True, f"rgg_s{scale}_f{factor}")
 
 
 def from_edges(n: int, src, dst, symmetrize: bool = True, keep_self_loops: bool = False) -> CSR:
@@ -190,6 +198,10 @@ CONFIGS = {
     "C4": dict(kind="grid", rows=4096, cols=4096, sources=8),
     "C4_road": dict(kind="pgrid", rows=4096, cols=4096, p=0.6, seed=1, sources=8),
     "C5": dict(kind="rmat", scale=26, edgefactor=16, seed=1, sources=16),
+    # kron_g500-logn21 analog (Table 3; nnz within 0.5%): Table-2 ablation
+    "K21": dict(kind="rmat", scale=21, edgefactor=48, seed=1, sources=16),
+    # rgg_n_2_24_s0 shape: high-diameter second workload
+    "RGG24": dict(kind="rgg", scale=24, factor=0.55, seed=1, sources=8),
 }
 
 
@@ -197,6 +209,8 @@ def make(config: str) -> CSR:
     c = CONFIGS[config]
     if c["kind"] == "rmat":
         g = rmat(c["scale"], c["edgefactor"], c["seed"])
+    elif c["kind"] == "rgg":
+        g = rgg(c["scale"], c["factor"], c["seed"])
     elif c["kind"] == "grid":
         g = grid(c["rows"], c["cols"])
     else:

@@ -22,6 +22,7 @@
  * Output: CSR with int64 row offsets (n+1) and uint32 column ids (sorted,
  * unique within each row).  For the symmetric graphs generated here CSR == CSC.
  */
+#include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -204,6 +205,91 @@ synth_graph* synth_grid(int64_t rows, int64_t cols) {
     if (x + 1 < cols) g->idx[p++] = (uint32_t)(v + 1);
     if (y + 1 < rows) g->idx[p++] = (uint32_t)(v + cols);
   }
+  return g;
+}
+
+/* Random geometric graph (rgg_n_2_24_s0 shape, Table 3): 2^scale points
+ * uniform in the unit square, an edge between every pair at Euclidean distance <= r with
+ * r = factor * sqrt(ln n / n).  Point k's coordinates come from the splitmix64 stream keyed by
+ * (seed, 2k) and (seed, 2k+1).  Vertex ids are assigned in cell-major order over a grid of
+ * cells of side >= r (row-major cells, points of a cell by generation index), so every
+ * neighbour lies in the 3x3 surrounding cells and scanning those cells in order emits each
+ * row already sorted.  Symmetric by construction (the distance test is symmetric). */
+synth_graph* synth_rgg(int scale, double factor, uint64_t seed) {
+  const int64_t n = (int64_t)1 << scale;
+  const double r = factor * sqrt(log((double)n) / (double)n), r2 = r * r;
+  int64_t C = (int64_t)floor(1.0 / r);
+  if (C < 1) C = 1;
+  const int64_t ncell = C * C;
+  double* x0 = (double*)malloc(sizeof(double) * (size_t)n);
+  double* y0 = (double*)malloc(sizeof(double) * (size_t)n);
+  int64_t* cell = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+  int64_t* cstart = (int64_t*)calloc((size_t)ncell + 1, sizeof(int64_t));
+  const uint64_t key = seed * 0x100000001B3ull;
+#pragma omp parallel for schedule(static)
+  for (int64_t k = 0; k < n; ++k) {
+    x0[k] = u01(sm64(key ^ (uint64_t)(2 * k)));
+    y0[k] = u01(sm64(key ^ (uint64_t)(2 * k + 1)));
+    int64_t cx = (int64_t)(x0[k] * (double)C), cy = (int64_t)(y0[k] * (double)C);
+    if (cx >= C) cx = C - 1;
+    if (cy >= C) cy = C - 1;
+    cell[k] = cy * C + cx;
+  }
+  for (int64_t k = 0; k < n; ++k) cstart[cell[k] + 1]++;
+  for (int64_t c = 0; c < ncell; ++c) cstart[c + 1] += cstart[c];
+  double* px = (double*)malloc(sizeof(double) * (size_t)n);
+  double* py = (double*)malloc(sizeof(double) * (size_t)n);
+  {
+    int64_t* fillc = (int64_t*)malloc(sizeof(int64_t) * (size_t)ncell);
+    memcpy(fillc, cstart, sizeof(int64_t) * (size_t)ncell);
+    for (int64_t k = 0; k < n; ++k) {  /* stable: generation order inside a cell */
+      const int64_t id = fillc[cell[k]]++;
+      px[id] = x0[k];
+      py[id] = y0[k];
+    }
+    free(fillc);
+  }
+  free(x0);
+  free(y0);
+  free(cell);
+  synth_graph* g = (synth_graph*)calloc(1, sizeof(synth_graph));
+  g->n = n;
+  g->off = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n + 1));
+  int64_t* deg = (int64_t*)calloc((size_t)n, sizeof(int64_t));
+  for (int pass = 0; pass < 2; ++pass) {
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t cy = 0; cy < C; ++cy)
+      for (int64_t cx = 0; cx < C; ++cx)
+        for (int64_t i = cstart[cy * C + cx]; i < cstart[cy * C + cx + 1]; ++i) {
+          int64_t cntv = 0, p = pass ? g->off[i] : 0;
+          for (int64_t ny = cy - 1; ny <= cy + 1; ++ny) {
+            if (ny < 0 || ny >= C) continue;
+            for (int64_t nx = cx - 1; nx <= cx + 1; ++nx) {
+              if (nx < 0 || nx >= C) continue;
+              const int64_t c = ny * C + nx;
+              for (int64_t j = cstart[c]; j < cstart[c + 1]; ++j) {
+                if (j == i) continue;
+                const double dx = px[i] - px[j], dy = py[i] - py[j];
+                if (dx * dx + dy * dy <= r2) {
+                  if (pass) g->idx[p++] = (uint32_t)j;
+                  else ++cntv;
+                }
+              }
+            }
+          }
+          if (!pass) deg[i] = cntv;
+        }
+    if (!pass) {
+      g->off[0] = 0;
+      for (int64_t i = 0; i < n; ++i) g->off[i + 1] = g->off[i] + deg[i];
+      g->nnz = g->off[n];
+      g->idx = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)(g->nnz > 0 ? g->nnz : 1));
+    }
+  }
+  free(deg);
+  free(px);
+  free(py);
+  free(cstart);
   return g;
 }
 

@@ -109,6 +109,20 @@ def test_toggles_do_not_change_results(ctx, toggles, relabel):
                 check(ctx, g, gT, G, s, mode, rule, toggles=toggles, exp=exp)
 
 
+@pytest.mark.parametrize("relabel", [False, True])
+@pytest.mark.parametrize("toggles", [pp.PP_OPT_NO_EARLYEXIT, 7])
+def test_no_early_exit_long_rows_grid_wide(ctx, toggles, relabel):
+    """C1 has rows up to 9,722 ids: without early exit the pull hands remainders longer than
+    2,048 ids to grid-wide chunks (pull_hub_chunks); depths, min-id parents and the
+    direction trace must stay bit-exact."""
+    g = synth.make("C1")
+    G, gT = upload(ctx, g, relabel)
+    for s in synth.sources(g, 6, seed=4):
+        exp = oracle.bfs(g, s)
+        for mode, rule in ((pp.PP_MODE_DO, pp.PP_HEUR_EDGES), (pp.PP_MODE_PULL_ONLY, pp.PP_HEUR_EDGES)):
+            check(ctx, g, gT, G, s, mode, rule, toggles=toggles, exp=exp)
+
+
 def test_isolated_source(ctx):
     g = SMALL["disconnected"]
     G, gT = upload(ctx, g)

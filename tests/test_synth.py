@@ -58,3 +58,35 @@ def test_p1_table3_kron21_shape():
     g = synth.rmat(21, 48, seed=1)
     assert abs(g.nnz - 182.1e6) / 182.1e6 < 0.01
     assert abs(g.degrees().max() - 213904) / 213904 < 0.15
+
+
+def test_rgg_matches_brute_force_pairs():
+    """RGG (NEXT-2 workload): edge set = all point pairs within r, recomputed here by brute
+    force from the same counter-based coordinates (ids are the cell-major order)."""
+    import math
+    scale, factor, seed = 11, 0.55, 3
+    g = synth.rgg(scale, factor, seed)
+    rows = check_csr(g)
+    assert not np.any(rows == g.idx)
+    t = synth.transpose(g)
+    assert np.array_equal(t.off, g.off) and np.array_equal(t.idx, g.idx)
+    n = 1 << scale
+    r = factor * math.sqrt(math.log(n) / n)
+    key = (seed * 0x100000001B3) & (2**64 - 1)
+    u = lambda x: (synth.splitmix64(x) >> 11) * (1.0 / 9007199254740992.0)
+    x = np.array([u(key ^ (2 * k)) for k in range(n)])
+    y = np.array([u(key ^ (2 * k + 1)) for k in range(n)])
+    d2 = (x[:, None] - x[None, :]) ** 2 + (y[:, None] - y[None, :]) ** 2
+    np.fill_diagonal(d2, np.inf)
+    assert len(g.idx) == int((d2 <= r * r).sum())
+    # degree multiset is id-order independent
+    assert np.array_equal(np.sort(np.diff(g.off)), np.sort((d2 <= r * r).sum(1)))
+
+
+def test_rgg24_reproduces_table3_shape():
+    """Pin (Table 3): rgg_n_24 has 16.8M vertices, 265.1M edges, max degree
+    40.  radius 0.55*sqrt(ln n / n) gives nnz within 0.5% and max degree within 15%."""
+    g = synth.make("RGG24")
+    assert g.n == 1 << 24
+    assert abs(len(g.idx) - 265.1e6) / 265.1e6 < 0.005
+    assert abs(int(np.diff(g.off).max()) - 40) <= 6
