@@ -252,6 +252,8 @@ def main():
 
     # ---- end to end through the public API: host output buffer, D2H inside the call ----
     host_depth = torch.empty(max(hi - lo, 1), dtype=torch.int32).pin_memory().numpy()
+    for k in range(args.warmup):  # untimed: first call allocates the device staging buffer
+        pp.bfs(G, src(k), host_depth, heuristic=heur)
     e2e_t = []
     for k in range(args.steps):
         flush.zero_()
