@@ -1,3 +1,4 @@
+#include <cstdlib>
 // bfs.cu — persistent, device-resident direction-optimised BFS (Algorithm 1).
 //
 // One cooperative launch runs the whole traversal: every level is one phase
@@ -58,6 +59,8 @@ struct BfsArgs {
   int stats_cap;
   GridBarrier* bar;
   BfsStatus* status;
+  int narrow;  // 1: this launch is one thread-block cluster running the small levels
+  int resume;  // 1: continue the loop state a narrow launch handed over (bar->rs)
   uint32_t source;  // caller id
   int mode;  // 0 DO, 1 push only, 2 pull only
   int rule;  // 0 edges, 1 paper r
@@ -124,6 +127,23 @@ __device__ __forceinline__ bool grid_barrier(GridBarrier* b, BfsStatus* st, unsi
 // This CTA's contributions to the next frontier's list lengths in the current phase
 // (light entries, heavy chunk descriptors, hub block descriptors), published by level_sync.
 __shared__ unsigned s_app[3];
+
+// Narrow mode: the whole launch is ONE thread-block cluster, so the level barrier is the
+// hardware cluster barrier (release/acquire at cluster scope, which also orders the
+// global-memory writes of the level) instead of the software grid barrier.
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n"
+               "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ bool level_barrier(bool narrow, GridBarrier* b, BfsStatus* st,
+                                              unsigned& epoch) {
+  if (narrow) {
+    __syncthreads();
+    cluster_barrier();
+    return true;
+  }
+  return grid_barrier(b, st, epoch);
+}
 
 // Per-lane accumulators of a level's counters, flushed once per phase.
 struct Acc {
@@ -888,10 +908,26 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
         const Off deg = e[t] - rb[t];
+#if PP_PULL_PROBE_SPLIT
+        // second id alone first (most rows the first id misses are decided by it): fewer
+        // scattered probes per candidate, one more dependent step for the rest
+        if (valid[t] && deg > 1 && !(found[t] && C.early_exit) && C.hit(hd[t].x[1])) {
+          if (!found[t]) {
+            found[t] = true;
+            par[t] = hd[t].x[1];
+          }
+        }
+        if (valid[t] && deg > 2 && !(found[t] && C.early_exit)) {
+          bool h[8];
+          h[1] = false;
+#pragma unroll
+          for (int q = 2; q < 8; ++q) h[q] = deg > (Off)q && C.hit(hd[t].x[q]);
+#else
         if (valid[t] && deg > 1 && !(found[t] && C.early_exit)) {
           bool h[8];
 #pragma unroll
           for (int q = 1; q < 8; ++q) h[q] = deg > (Off)q && C.hit(hd[t].x[q]);
+#endif
 #pragma unroll
           for (int q = 1; q < 8; ++q) {
             if (h[q] && !found[t]) {
@@ -1185,7 +1221,9 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned long long gsize = (unsigned long long)gridDim.x * blockDim.x;
   const uint32_t s = a.rank ? a.rank[a.source] : a.source;  // internal id of the source
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t_start = (long long)global_timer_ns();
+  if (a.resume && a.bar->rs.done) return;  // the narrow launch finished the BFS
+  if (!a.resume && blockIdx.x == 0 && threadIdx.x == 0)
+    a.status->t_start = (long long)global_timer_ns();
   unsigned epoch = 0;  // grid barriers passed (thread 0)
   unsigned ph = 0;     // level_sync phases passed (thread 0)
   if (kCountingSync && threadIdx.x == 0) {
@@ -1193,6 +1231,35 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
     s_app[0] = s_app[1] = s_app[2] = 0u;
   }
 
+  int dir = (a.mode == 2) ? 1 : 0;
+  int cur = 0;  // visited bitmap in use
+  int sel = 0;  // frontier list / chunk buffers holding the current frontier
+  long long c_old = 1;
+  const Off indeg_s = a.coff[s + 1] - a.coff[s];
+  long long m_u = a.nnz - (long long)indeg_s;
+  long long reached = 1;
+  Acc acc{0, 0, 0, 0};
+  bool from_bits = false;  // next push reads the pull's frontier bitmap
+  long long mf_last = (long long)(a.off[s + 1] - a.off[s]);  // edges the next push expands
+  int d = 1;
+  unsigned nL = 0, nH = 0, nB = 0;
+  if (a.resume) {  // continue where the narrow cluster stopped (stream-ordered after it)
+    const BfsResume& r = a.bar->rs;
+    d = r.d;
+    dir = r.dir;
+    cur = r.cur;
+    sel = r.sel;
+    from_bits = r.from_bits != 0;
+    nL = r.nL;
+    nH = r.nH;
+    nB = r.nB;
+    c_old = r.c_old;
+    m_u = r.m_u;
+    reached = r.reached;
+    mf_last = r.mf_last;
+    if (threadIdx.x == 0) sh.work = 0u;
+    __syncthreads();
+  } else {
   // ---- Alg. 1 lines 2-4: d <- 1, f <- e_s, v <- 0 (depth 0 = unvisited) ----
   for (unsigned long long v = gtid; v < (unsigned long long)a.n; v += gsize) {
     a.depth[v] = (v == a.source) ? 1 : 0;                          // caller ids
@@ -1232,24 +1299,35 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
     Acc acc0{0, 0, 0, 0};
     if (!level_sync<Off>(acc0, sh, a.bar, a.status, ph)) return;
   } else {
-    if (!grid_barrier(a.bar, a.status, epoch)) return;
+    if (!level_barrier(a.narrow, a.bar, a.status, epoch)) return;
     read_level(&a.ctr[0], sh);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t_init = (long long)global_timer_ns();
-  unsigned nL = (unsigned)sh.lvl[3], nH = (unsigned)sh.lvl[4], nB = (unsigned)sh.lvl[6];
-
-  int dir = (a.mode == 2) ? 1 : 0;
-  int cur = 0;  // visited bitmap in use
-  int sel = 0;  // frontier list / chunk buffers holding the current frontier
-  long long c_old = 1;
-  const Off indeg_s = a.coff[s + 1] - a.coff[s];
-  long long m_u = a.nnz - (long long)indeg_s;
-  long long reached = 1;
-  Acc acc{0, 0, 0, 0};
-  bool from_bits = false;  // next push reads the pull's frontier bitmap
-  long long mf_last = (long long)(a.off[s + 1] - a.off[s]);  // edges the next push expands
-  int d = 1;
+  nL = (unsigned)sh.lvl[3];
+  nH = (unsigned)sh.lvl[4];
+  nB = (unsigned)sh.lvl[6];
+  }
   for (;; ++d) {
+    if (a.narrow && (dir == 1 || (unsigned long long)mf_last > kNarrowMaxEdges)) {
+      // this level is too wide for one cluster: hand the loop to the whole grid
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        BfsResume& r = a.bar->rs;
+        r.d = d;
+        r.dir = dir;
+        r.cur = cur;
+        r.sel = sel;
+        r.from_bits = from_bits ? 1 : 0;
+        r.nL = nL;
+        r.nH = nH;
+        r.nB = nB;
+        r.c_old = c_old;
+        r.m_u = m_u;
+        r.reached = reached;
+        r.mf_last = mf_last;
+        r.valid = 1;
+      }
+      return;
+    }
     const long long t_lvl = (a.dbg && threadIdx.x == 0) ? (long long)global_timer_ns() : 0;
     LevelCtr* out = &a.ctr[d & (kRing - 1)];
     if (blockIdx.x == 0 && threadIdx.x < sizeof(LevelCtr) / 4)
@@ -1273,7 +1351,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       pull_phase<Off, PARENTS>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp],
                                ssum, &sh.work, svis, pbits);
       if (a.toggles & PP_OPT_NO_EARLYEXIT) {  // ablation arms: long rows grid-wide
-        if (!grid_barrier(a.bar, a.status, epoch)) return;
+        if (!level_barrier(a.narrow, a.bar, a.status, epoch)) return;
         const unsigned nch = ld_relaxed_u32(&out->work2);
         if (nch) pull_hub_chunks<Off, PARENTS>(a, vis, vis_other, out, nch, d, acc, rqs[warp], svis,
                                                 pbits);
@@ -1285,7 +1363,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       if (!level_sync<Off>(acc, sh, a.bar, a.status, ph)) return;
     } else {
       flush_acc(acc, out, sh.red);
-      if (!grid_barrier(a.bar, a.status, epoch)) return;
+      if (!level_barrier(a.narrow, a.bar, a.status, epoch)) return;
       read_level(out, sh);
     }
     const long long c_new = sh.lvl[0], mf = sh.lvl[1], mfin = sh.lvl[2];
@@ -1322,7 +1400,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       if (kCountingSync) {
         if (!level_sync<Off>(acc, sh, a.bar, a.status, ph)) return;
       } else {
-        if (!grid_barrier(a.bar, a.status, epoch)) return;
+        if (!level_barrier(a.narrow, a.bar, a.status, epoch)) return;
         read_level(out, sh);
       }
       nL = (unsigned)sh.lvl[3];
@@ -1333,6 +1411,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
     c_old = c_new;
     mf_last = mf;
   }
+  if (a.narrow && blockIdx.x == 0 && threadIdx.x == 0) a.bar->rs.done = 1;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     a.status->levels = d;
     a.status->reached = reached;
@@ -1381,6 +1460,39 @@ static cudaError_t launch_t(pp_graph g, const BfsArgs<Off>& args) {
                                      g->ctx->stream);
 }
 
+// Narrow launch: ONE thread-block cluster of kNarrowCtas CTAs runs init and the levels while
+// they stay small, then hands the loop state to the cooperative whole-grid launch queued
+// right behind it on the stream (which returns at once if the cluster finished the BFS).
+template <typename Off, bool PARENTS>
+static cudaError_t launch_narrow(pp_graph g, const BfsArgs<Off>& args) {
+  (void)grid_for<Off, PARENTS>();  // sets the dynamic shared memory attribute
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(kNarrowCtas);
+  cfg.blockDim = dim3(kBfsBlock);
+  cfg.dynamicSmemBytes = dyn_smem_bytes<Off>();
+  cfg.stream = g->ctx->stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kNarrowCtas;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  g->ctx->launches += 1;
+  return cudaLaunchKernelEx(&cfg, bfs_persistent<Off, PARENTS>, args);
+}
+
+// PP_NARROW unset or 0: never; 1: always (tests of the hand-over on any graph);
+// 2: for graphs with max out-degree <= kNarrowMaxDeg.
+static bool use_narrow(pp_graph g, int mode) {
+  if (kCountingSync || mode == 2) return false;
+  // Measured slower than the whole grid on C4 and RGG24, so opt-in only.
+  const char* e = getenv("PP_NARROW");
+  if (e && e[0] == '1') return true;
+  if (e && e[0] == '2') return g->max_out_deg <= kNarrowMaxDeg;
+  return false;
+}
+
 template <typename Off>
 static cudaError_t launch_off(pp_graph g, uint32_t source, int mode, int rule, double alpha,
                               double beta, uint32_t toggles, int32_t* depth, uint32_t* parent,
@@ -1426,6 +1538,15 @@ static cudaError_t launch_off(pp_graph g, uint32_t source, int mode, int rule, d
   a.max_levels = max_levels;
   a.dbg = g->dbg;
   a.dbg_levels = g->dbg_levels;
+  a.narrow = 0;
+  a.resume = 0;
+  if (use_narrow(g, mode)) {
+    a.narrow = 1;
+    const cudaError_t e = parent ? launch_narrow<Off, true>(g, a) : launch_narrow<Off, false>(g, a);
+    if (e != cudaSuccess) return e;
+    a.narrow = 0;
+    a.resume = 1;
+  }
   if (parent) return launch_t<Off, true>(g, a);
   return launch_t<Off, false>(g, a);
 }

@@ -322,11 +322,12 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr
   }
   if ((s = dalloc(&g->isolated, g->nwords, &bytes, "isolated")) != PP_OK) return s;
   if ((s = dalloc(&g->head, (size_t)n * 8, &bytes, "row heads")) != PP_OK) return s;
-  PP_CK(cudaMemsetAsync(g->scount, 0, 2 * sizeof(unsigned long long), st), "memset");
+  PP_CK(cudaMemsetAsync(g->scount, 0, 4 * sizeof(unsigned long long), st), "memset");
   PP_CK(launch_graph_prepare(g, d_off64, d_coff64, g->scount, &ctx->launches), "prepare kernels");
-  PP_CK(cudaMemcpyAsync(g->scount_host, g->scount, 16, cudaMemcpyDeviceToHost, st), "copy");
+  PP_CK(cudaMemcpyAsync(g->scount_host, g->scount, 32, cudaMemcpyDeviceToHost, st), "copy");
   PP_CK(cudaStreamSynchronize(st), "sync");
   g->hcap = (int64_t)std::max(g->scount_host[0], g->scount_host[1]);
+  g->max_out_deg = (int64_t)g->scount_host[2];
 
   // BFS / mxv working set
   for (int k = 0; k < 2; ++k) {

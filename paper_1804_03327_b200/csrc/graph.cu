@@ -50,15 +50,19 @@ __global__ void k_head(const int64_t* __restrict__ coff, const uint32_t* __restr
 }
 
 // Heavy-chunk capacity: sum over rows with degree >= kHeavy of ceil(deg / kChunk).
-__global__ void k_hcap(const int64_t* __restrict__ off, int64_t n, unsigned long long* out) {
-  unsigned long long c = 0;
+__global__ void k_hcap(const int64_t* __restrict__ off, int64_t n, unsigned long long* out,
+                       unsigned long long* maxdeg) {
+  unsigned long long c = 0, m = 0;
   for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (int64_t)gridDim.x * blockDim.x) {
     const int64_t d = off[v + 1] - off[v];
     if (d >= (int64_t)kHeavy) c += (unsigned long long)((d + kChunk - 1) / kChunk);
+    m = max(m, (unsigned long long)d);
   }
   c = warp_sum(c);
+  for (int o = 16; o >= 1; o >>= 1) m = max(m, __shfl_xor_sync(kFull, m, o));
   if (lane_id() == 0 && c) atomicAdd(out, c);
+  if (lane_id() == 0 && m) atomicMax(maxdeg, m);
 }
 
 // First offending row (or n+1 if none): non-monotone offsets, id >= n, unsorted / duplicate.
@@ -107,8 +111,8 @@ cudaError_t launch_graph_prepare(pp_graph g, const int64_t* d_off64, const int64
   *launches += 4;
   k_head<<<blocks, kBlock, 0, st>>>(d_coff64, g->cidx, g->n, g->head);
   k_isolated<<<blocks, kBlock, 0, st>>>(d_off64, d_coff64, g->n, g->nwords, g->isolated);
-  k_hcap<<<blocks, kBlock, 0, st>>>(d_off64, g->n, d_scratch + 0);
-  k_hcap<<<blocks, kBlock, 0, st>>>(d_coff64, g->n, d_scratch + 1);
+  k_hcap<<<blocks, kBlock, 0, st>>>(d_off64, g->n, d_scratch + 0, d_scratch + 2);
+  k_hcap<<<blocks, kBlock, 0, st>>>(d_coff64, g->n, d_scratch + 1, d_scratch + 3);
   return cudaGetLastError();
 }
 

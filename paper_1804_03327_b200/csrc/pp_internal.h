@@ -43,6 +43,9 @@ constexpr unsigned kPullTail = PP_PULL_TAIL;  // pull: a CTA's last kPullTail it
 #ifndef PP_PULL_CARRY
 #define PP_PULL_CARRY 0
 #endif
+#ifndef PP_PULL_PROBE_SPLIT
+#define PP_PULL_PROBE_SPLIT 0
+#endif
 #ifndef PP_VPREFIX_WORDS
 #define PP_VPREFIX_WORDS 0
 #endif
@@ -88,6 +91,24 @@ struct LevelStat {
 #define PP_SYNC_STRIDE 32
 #endif
 constexpr int kSyncStride = PP_SYNC_STRIDE;
+// Narrow -> wide hand-over of the BFS loop state (bfs.cu, narrow mode).
+struct BfsResume {
+  int valid, done;  // valid: the wide kernel continues at level d; done: BFS finished
+  int d, dir, cur, sel, from_bits, pad;
+  unsigned nL, nH, nB, pad2;
+  long long c_old, m_u, reached, mf_last;
+};
+constexpr int kNarrowCtas = 8;  // narrow mode: one thread-block cluster of this many CTAs
+#ifndef PP_NARROW_MAX_EDGES
+#define PP_NARROW_MAX_EDGES 131072
+#endif
+constexpr unsigned long long kNarrowMaxEdges = PP_NARROW_MAX_EDGES;  // hand over to the whole
+                                  // grid before a push expanding more edges, or a pull
+#ifndef PP_NARROW_MAX_DEG
+#define PP_NARROW_MAX_DEG 64
+#endif
+constexpr int64_t kNarrowMaxDeg = PP_NARROW_MAX_DEG;  // auto: narrow start for graphs whose max
+                                  // out-degree is at most this (mesh / road / geometric graphs)
 struct GridBarrier {
   unsigned long long count;  // monotone arrival counter (bit 63: abort), zeroed per launch
   unsigned int pad0[30];
@@ -98,6 +119,7 @@ struct GridBarrier {
   // count (low 24 bits) next to the running sum of the per-CTA values (zeroed per launch)
   unsigned long long pk[2][8][kSyncStride];  // word f of slot s at pk[s][f][0]: one word per
                                              // kSyncStride*8 bytes, spread over L2 slices
+  BfsResume rs;
 };
 
 // Device-side BFS status words.
@@ -158,6 +180,7 @@ struct pp_graph_s {
   uint4* hubq = nullptr;             // row-mxv long-row chunks {row, len, start}
   unsigned long long* scount = nullptr;  // device counters (mxv)
   unsigned long long* scount_host = nullptr;
+  int64_t max_out_deg = 0;       // max CSR row length (narrow-mode auto decision)
   int64_t* dtmp[2] = {nullptr, nullptr};  // upload staging / host-output staging
   int bfs_grid = 0;
   long long* dbg = nullptr;  // pp_bfs_debug_times: per level x CTA phase durations

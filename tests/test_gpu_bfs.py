@@ -123,6 +123,24 @@ def test_no_early_exit_long_rows_grid_wide(ctx, toggles, relabel):
             check(ctx, g, gT, G, s, mode, rule, toggles=toggles, exp=exp)
 
 
+@pytest.mark.parametrize("narrow", ["1", "0"])
+def test_narrow_cluster_start_and_handover(ctx, narrow, monkeypatch):
+    """Narrow mode (one 8-CTA thread-block cluster runs init and the small levels, then hands
+    the loop state to the whole-grid launch): PP_NARROW=1 forces it on every graph, so RMAT
+    sources hand over after 1-3 levels and the grid / path run narrow to the end; results
+    must be bit-exact either way (depths, min-id parents, direction trace)."""
+    monkeypatch.setenv("PP_NARROW", narrow)
+    graphs = [synth.make("C1"), synth.grid(64, 64), SMALL["path"], SMALL["disconnected"],
+              SMALL["directed_random"]]
+    for g in graphs:
+        for relabel in (False, True):
+            G, gT = upload(ctx, g, relabel)
+            for s in list(synth.sources(g, 3, seed=5)) + [0]:
+                exp = oracle.bfs(g, s)
+                for mode, rule in MODES:
+                    check(ctx, g, gT, G, s, mode, rule, exp=exp)
+
+
 def test_isolated_source(ctx):
     g = SMALL["disconnected"]
     G, gT = upload(ctx, g)
