@@ -200,6 +200,9 @@ CONFIGS = {
     "C5": dict(kind="rmat", scale=26, edgefactor=16, seed=1, sources=16),
     # kron_g500-logn21 analog (Table 3; nnz within 0.5%): Table-2 ablation
     "K21": dict(kind="rmat", scale=21, edgefactor=48, seed=1, sources=16),
+    # the paper's generated RMAT graphs (Table 3; Fig. 7)
+    "S23E32": dict(kind="rmat", scale=23, edgefactor=32, seed=1, sources=16),
+    "S24E16": dict(kind="rmat", scale=24, edgefactor=16, seed=1, sources=16),
     # rgg_n_2_24_s0 shape: high-diameter second workload
     "RGG24": dict(kind="rgg", scale=24, factor=0.55, seed=1, sources=8),
 }

@@ -16,7 +16,7 @@ g = synth.make(cfg)
 print(f"{cfg}: n={g.n} nnz={g.nnz} maxdeg={int(np.diff(g.off).max())} gen {time.time()-t0:.1f}s", flush=True)
 ctx = pp.Context(0)
 t0 = time.time()
-G = pp.Graph.from_csr(ctx, g)
+G = pp.Graph.from_csr(ctx, g, relabel="norelabel" not in sys.argv)
 print(f"upload {time.time()-t0:.1f}s device bytes {G.info()[2]/1e9:.2f} GB", flush=True)
 depth = torch.empty(g.n, dtype=torch.int32, device="cuda")
 parent = torch.empty(g.n, dtype=torch.int32, device="cuda")
