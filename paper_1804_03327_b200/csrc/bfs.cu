@@ -54,6 +54,7 @@ struct BfsArgs {
   uint32_t* pout;       // relabelled graph with parents: the caller's parent array
   const uint32_t* __restrict__ perm;  // internal -> caller id, nullptr = identity
   const uint32_t* __restrict__ rank;  // caller -> internal id
+  const uint4* __restrict__ vrec;     // relabelled: {begin lo, hi, out-degree, caller id}
   LevelCtr* ctr;
   LevelStat* stats;
   int stats_cap;
@@ -406,9 +407,16 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
     beg[t] = 0;
     dpos[t] = w[t];
     if (disc[t]) {
-      if (a.perm) dpos[t] = a.perm[w[t]];  // loaded in the same batch as the offsets
-      beg[t] = lowlat ? sb[t] : a.off[w[t]];
-      deg[t] = (lowlat ? se[t] : a.off[w[t] + 1]) - beg[t];
+      if (a.vrec && !lowlat) {  // one 16-byte record: offsets + caller id
+        const uint4 r = __ldg(a.vrec + w[t]);
+        beg[t] = (Off)(((unsigned long long)r.y << 32) | r.x);
+        deg[t] = (Off)r.z;
+        dpos[t] = r.w;
+      } else {
+        if (a.perm) dpos[t] = a.perm[w[t]];  // loaded in the same batch as the offsets
+        beg[t] = lowlat ? sb[t] : a.off[w[t]];
+        deg[t] = (lowlat ? se[t] : a.off[w[t] + 1]) - beg[t];
+      }
       const Off degin = a.symmetric ? deg[t] : (Off)(a.coff[w[t] + 1] - a.coff[w[t]]);
       acc.c += 1;
       acc.mf += (unsigned long long)deg[t];
@@ -1524,6 +1532,7 @@ static cudaError_t launch_off(pp_graph g, uint32_t source, int mode, int rule, d
   a.pout = parent;
   a.perm = g->perm;
   a.rank = g->rank;
+  a.vrec = g->vrec;
   a.ctr = g->ctr;
   a.stats = g->stats;
   a.stats_cap = g->stats_cap;

@@ -73,7 +73,7 @@ void free_graph(pp_graph g) {
                   g->symmetric ? nullptr : (void*)g->cidx, g->isolated, g->head, g->vis[0], g->vis[1], g->fr, g->sumv,
                   g->L[0], g->L[1], g->H[0], g->H[1], g->ctr, g->stats, g->bar,
                   g->sbits[0], g->sbits[1], g->sbits[2], g->sbits[3], g->sblock, g->hubq, g->scount,
-                  g->dtmp[0], g->dtmp[1], g->dbg, g->perm, g->rank, g->pint,
+                  g->dtmp[0], g->dtmp[1], g->dbg, g->perm, g->rank, g->pint, g->vrec,
                   g->rbits[0], g->rbits[1], g->rbits[2], g->rbits[3],
                   g->dvis, g->dfr, g->dnxt, g->diso, g->pbeg, g->pend, g->dcnt};
   for (void* p : ptrs)
@@ -287,6 +287,7 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr
     if ((s = dalloc(&g->perm, (size_t)n, &bytes, "relabel perm")) != PP_OK) return s;
     if ((s = dalloc(&g->rank, (size_t)n, &bytes, "relabel rank")) != PP_OK) return s;
     if ((s = dalloc(&g->pint, (size_t)n, &bytes, "internal parents")) != PP_OK) return s;
+    if (kVrec && (s = dalloc(&g->vrec, (size_t)n, &bytes, "vertex records")) != PP_OK) return s;
     for (int k = 0; k < 4; ++k)
       if ((s = dalloc(&g->rbits[k], g->nwords, &bytes, "relabel scratch bitmap")) != PP_OK) return s;
     int64_t junk = 0;

@@ -89,6 +89,18 @@ cudaError_t launch_graph_validate(pp_graph g, const int64_t* d_off64, const uint
   return cudaGetLastError();
 }
 
+// Relabelled graph: one 16-byte record per vertex {row begin lo, hi, out-degree, caller id}
+// so a push discovery gets its offsets and the caller id of its depth slot in ONE scattered
+// access instead of two (offsets, perm).
+__global__ void k_vrec(const int64_t* __restrict__ off, const uint32_t* __restrict__ perm, int64_t n,
+                       uint4* __restrict__ vrec) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = off[v];
+    vrec[v] = make_uint4((uint32_t)b, (uint32_t)((uint64_t)b >> 32), (uint32_t)(off[v + 1] - b), perm[v]);
+  }
+}
+
 cudaError_t launch_graph_prepare(pp_graph g, const int64_t* d_off64, const int64_t* d_coff64,
                                  unsigned long long* d_scratch, uint64_t* launches) {
   cudaStream_t st = g->ctx->stream;
@@ -107,6 +119,10 @@ cudaError_t launch_graph_prepare(pp_graph g, const int64_t* d_off64, const int64
       *launches += 1;
       k_off_narrow<uint32_t><<<blocks, kBlock, 0, st>>>(d_coff64, (uint32_t*)g->coff, g->n + 1);
     }
+  }
+  if (g->vrec) {
+    *launches += 1;
+    k_vrec<<<blocks, kBlock, 0, st>>>(d_off64, g->perm, g->n, g->vrec);
   }
   *launches += 4;
   k_head<<<blocks, kBlock, 0, st>>>(d_coff64, g->cidx, g->n, g->head);

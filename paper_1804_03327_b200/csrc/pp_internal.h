@@ -46,6 +46,10 @@ constexpr unsigned kPullTail = PP_PULL_TAIL;  // pull: a CTA's last kPullTail it
 #ifndef PP_PULL_PROBE_SPLIT
 #define PP_PULL_PROBE_SPLIT 0
 #endif
+#ifndef PP_VREC
+#define PP_VREC 1
+#endif
+constexpr bool kVrec = PP_VREC != 0;  // relabelled graphs: per-vertex {begin, deg, caller id}
 #ifndef PP_VPREFIX_WORDS
 #define PP_VPREFIX_WORDS 0
 #endif
@@ -180,7 +184,8 @@ struct pp_graph_s {
   uint4* hubq = nullptr;             // row-mxv long-row chunks {row, len, start}
   unsigned long long* scount = nullptr;  // device counters (mxv)
   unsigned long long* scount_host = nullptr;
-  int64_t max_out_deg = 0;       // max CSR row length (narrow-mode auto decision)
+  int64_t max_out_deg = 0;
+  uint4* vrec = nullptr;         // relabelled graph: {begin lo, hi, out-degree, caller id} per vertex       // max CSR row length (narrow-mode auto decision)
   int64_t* dtmp[2] = {nullptr, nullptr};  // upload staging / host-output staging
   int bfs_grid = 0;
   long long* dbg = nullptr;  // pp_bfs_debug_times: per level x CTA phase durations
