@@ -588,6 +588,23 @@ __device__ __forceinline__ V8 ld_nc_v8(const uint32_t* p) {
   return v;
 }
 
+// Row-head load (32 B) with an L2 prefetch-size hint: candidates of a dense item have
+// adjacent heads, so an L2 miss may fetch the surrounding 128/256 B from HBM at once.
+__device__ __forceinline__ V8 ld_head_v8(const uint32_t* p) {
+  V8 v;
+#if PP_HEAD_L2PF == 256
+  asm volatile("ld.global.nc.L2::256B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+#elif PP_HEAD_L2PF == 128
+  asm volatile("ld.global.nc.L2::128B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+#else
+  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+#endif
+               : "=r"(v.x[0]), "=r"(v.x[1]), "=r"(v.x[2]), "=r"(v.x[3]), "=r"(v.x[4]),
+                 "=r"(v.x[5]), "=r"(v.x[6]), "=r"(v.x[7])
+               : "l"(p));
+  return v;
+}
+
 template <typename Off, bool PARENTS>
 struct PullCtx {
   const BfsArgs<Off>& a;
@@ -652,9 +669,11 @@ struct PullCtx {
   }
   // discovery of row i (found this level): Alg. 1 lines 7-8 fused
   __device__ __forceinline__ void commit(uint32_t i, uint32_t par, Off degin, unsigned wbase,
-                                         bool in_item, uint32_t dpos) const {
+                                         bool in_item, uint32_t dpos, bool bit_by_caller = false) const {
     const uint32_t bit = 1u << (i & 31u);
-    if (in_item) {
+    if (bit_by_caller) {
+      // the caller ORs the bit into its item word with a warp reduction
+    } else if (in_item) {
       atomicOr(&sfound[(i >> 5) - wbase], bit);
     } else {
       atomicOr(&vout[i >> 5], bit);
@@ -865,6 +884,7 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
     // non-isolated row is computed and the result filtered afterwards.
     const uint32_t cand = no_mask ? (own ? ~a.isolated[wbase + lane] : 0u) : unvisited;
     sfound[lane] = 0u;
+    uint32_t fw_acc = 0u;  // kPullWarpOr: this lane's item word's found bits (lane < pw)
     const unsigned cnt = __popc(cand);
     const unsigned incl = warp_incl_scan(cnt);
     const unsigned excl = incl - cnt;
@@ -901,7 +921,7 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
           if (a.perm) dpos[t] = a.perm[i[t]];
           rb[t] = a.coff[i[t]];
           e[t] = a.coff[i[t] + 1];
-          hd[t] = ld_nc_v8(a.head + (size_t)i[t] * 8u);
+          hd[t] = ld_head_v8(a.head + (size_t)i[t] * 8u);
         }
       }
       // stage: probe the first neighbour, then the other head ids of rows that missed
@@ -948,7 +968,22 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
       }
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
-        if (found[t] && fresh[t]) C.commit(i[t], par[t], e[t] - rb[t], wbase, true, dpos[t]);
+        if (found[t] && fresh[t])
+          C.commit(i[t], par[t], e[t] - rb[t], wbase, true, dpos[t], kPullWarpOr);
+        if (kPullWarpOr) {
+          // the round's rows are consecutive candidates, so their found bits fall in 1-3
+          // item words: one redux.sync OR per word instead of 32 same-word smem atomics
+          const bool fb = found[t] && fresh[t];
+          const unsigned wj = fb ? (i[t] >> 5) - wbase : 0xFFFFFFFFu;
+          const unsigned lo = __reduce_min_sync(kFull, wj);
+          if (lo != 0xFFFFFFFFu) {
+            const unsigned hi = __reduce_max_sync(kFull, fb ? wj : 0u);
+            for (unsigned j = lo; j <= hi; ++j) {
+              const uint32_t bits = __reduce_or_sync(kFull, wj == j ? (1u << (i[t] & 31u)) : 0u);
+              if (lane == j) fw_acc |= bits;
+            }
+          }
+        }
         // park undecided rows (and, without early exit, rows with ids left)
         const bool park = valid[t] && p[t] < e[t] && !(found[t] && C.early_exit) &&
                           (fresh[t] || !found[t]);
@@ -974,7 +1009,7 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
     if (qn > 0) C.residual_batch(qn, qn, wbase, pw);
 #endif
     __syncwarp();
-    const uint32_t fw = own ? sfound[lane] : 0u;
+    const uint32_t fw = own ? (sfound[lane] | fw_acc) : 0u;
     if (own) {
       vout[wbase + lane] = vw | fw;
       a.fr[wbase + lane] = fw;
@@ -1269,9 +1304,21 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
     __syncthreads();
   } else {
   // ---- Alg. 1 lines 2-4: d <- 1, f <- e_s, v <- 0 (depth 0 = unvisited) ----
-  for (unsigned long long v = gtid; v < (unsigned long long)a.n; v += gsize) {
-    a.depth[v] = (v == a.source) ? 1 : 0;                          // caller ids
-    if (PARENTS) a.parent[v] = (v == s) ? s : 0xFFFFFFFFu;         // internal ids
+  if (kInitVec && !PARENTS && (reinterpret_cast<uintptr_t>(a.depth) & 15u) == 0) {
+    // 16-byte stores: a quarter of the store instructions of the scalar loop
+    const unsigned long long n4 = (unsigned long long)a.n / 4u;
+    int4* d4 = reinterpret_cast<int4*>(a.depth);
+    for (unsigned long long q = gtid; q < n4; q += gsize) {
+      const unsigned long long v0 = q * 4u;
+      d4[q] = make_int4(v0 == a.source, v0 + 1 == a.source, v0 + 2 == a.source, v0 + 3 == a.source);
+    }
+    for (unsigned long long v = n4 * 4u + gtid; v < (unsigned long long)a.n; v += gsize)
+      a.depth[v] = (v == a.source) ? 1 : 0;
+  } else {
+    for (unsigned long long v = gtid; v < (unsigned long long)a.n; v += gsize) {
+      a.depth[v] = (v == a.source) ? 1 : 0;                          // caller ids
+      if (PARENTS) a.parent[v] = (v == s) ? s : 0xFFFFFFFFu;         // internal ids
+    }
   }
   // visited starts as {s} plus the isolated / padding vertices, which no pull may
   // compute and no push can reach (they have no edges).

@@ -46,6 +46,17 @@ constexpr unsigned kPullTail = PP_PULL_TAIL;  // pull: a CTA's last kPullTail it
 #ifndef PP_PULL_PROBE_SPLIT
 #define PP_PULL_PROBE_SPLIT 0
 #endif
+#ifndef PP_PULL_WARPOR
+#define PP_PULL_WARPOR 0
+#endif
+constexpr bool kPullWarpOr = PP_PULL_WARPOR != 0;  // pull: found bits by warp reduction
+#ifndef PP_HEAD_L2PF
+#define PP_HEAD_L2PF 0
+#endif
+#ifndef PP_INIT_VEC
+#define PP_INIT_VEC 1
+#endif
+constexpr bool kInitVec = PP_INIT_VEC != 0;  // BFS init: 16-byte depth stores
 #ifndef PP_VREC
 #define PP_VREC 1
 #endif
