@@ -106,7 +106,7 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def byte_model(torch, g_dev, depth, dirs, n, nnz, off_bytes):
+def byte_model(torch, g_dev, depth, dirs, n, nnz, off_bytes, per_level=False):
     """Algorithmic HBM bytes of one BFS under DESIGN.md §6's model (byte-exact; the
     visited-bitmap probes are L2-resident and excluded).  Computed from the result
     (depth vector) and the level directions with torch ops on the graph's CSR."""
@@ -115,10 +115,12 @@ def byte_model(torch, g_dev, depth, dirs, n, nnz, off_bytes):
     d = depth.to(torch.int64)
     L = len(dirs)
     total = 4 * n + 2 * (n // 8)                       # init: depth, visited <- isolated
+    parts = [total]                                      # per_level: [init, level 1, ...]
     cnt = torch.bincount(d, minlength=L + 2)
     outdeg_sum = torch.zeros(L + 2, dtype=torch.int64, device=d.device).index_add_(0, d, deg)
     dj = d[idx]                                          # depth of each edge's head
     for k in range(1, L + 1):                            # level k expands depth-k frontier
+        before = total
         F = int(cnt[k])
         Fn = int(cnt[k + 1]) if k + 1 <= L + 1 else 0
         if dirs[k - 1] == 0:  # push
@@ -136,7 +138,8 @@ def byte_model(torch, g_dev, depth, dirs, n, nnz, off_bytes):
             total += 2 * (n // 8) + C * 2 * O + 4 * S + 4 * Fn
             if k < L and dirs[k] == 0:                 # pull -> push: convert
                 total += 2 * (n // 8) + Fn * (4 + 2 * O)
-    return total
+        parts.append(total - before)
+    return parts if per_level else total
 
 
 def run_reference(args, rank, world):

@@ -114,20 +114,12 @@ __device__ __forceinline__ bool grid_barrier(GridBarrier* b, BfsStatus* st, unsi
         }
       }
     }
-#if PP_BAR_FENCE_SC
     __threadfence();
-#else
-    asm volatile("fence.acq_rel.gpu;" ::: "memory");
-#endif
     s_ok = (v & kAbortBit) ? 0 : 1;
   }
   __syncthreads();
   return s_ok != 0;
 }
-
-// This CTA's contributions to the next frontier's list lengths in the current phase
-// (light entries, heavy chunk descriptors, hub block descriptors), published by level_sync.
-__shared__ unsigned s_app[3];
 
 // Narrow mode: the whole launch is ONE thread-block cluster, so the level barrier is the
 // hardware cluster barrier (release/acquire at cluster scope, which also orders the
@@ -194,24 +186,6 @@ __device__ __forceinline__ unsigned cta_grab(unsigned* sctr) {
 }
 __device__ __forceinline__ unsigned nwarps() { return gridDim.x * kBfsWarps; }
 
-// Visited prefix: every CTA copies the first `pw` words of the visited bitmap into shared
-// memory at the start of a heavy level (coalesced 16-byte loads, L2-resident source).  With
-// PP_GRAPH_RELABEL the low ids are the highest-degree vertices, so most visited probes of
-// a level (pull: a row's first in-neighbours; push: hub targets) are answered from shared
-// memory instead of a scattered L2 access.  Returns the number of bits covered.
-__device__ __forceinline__ uint32_t load_vprefix(const uint32_t* vis, uint32_t* svis,
-                                                 unsigned long long nwords) {
-  if (!kVPrefixWords) return 0u;
-  const unsigned pw = (unsigned)min((unsigned long long)kVPrefixWords, nwords) & ~3u;
-  const uint4* src = reinterpret_cast<const uint4*>(vis);
-  uint4* dst = reinterpret_cast<uint4*>(svis);
-  for (unsigned t = threadIdx.x; t < pw / 4u; t += blockDim.x) dst[t] = ld_relaxed_u4(src + t);
-  __syncthreads();
-  return pw * 32u;
-}
-__device__ __forceinline__ bool vprefix_bit(const uint32_t* svis, uint32_t x) {
-  return (svis[x >> 5] >> (x & 31u)) & 1u;
-}
 
 
 // Light frontier entry: the discovering thread already loaded the row's offsets, so the
@@ -244,14 +218,8 @@ __device__ __forceinline__ void heavy_bases(unsigned CS, unsigned CB, LevelCtr* 
   const unsigned ts = __shfl_sync(kFull, is, 31), tb = __shfl_sync(kFull, ib, 31);
   unsigned bs = 0, bb = 0;
   if (lane_id() == 0) {
-    if (ts) {
-      bs = atomicAdd(&out->nH, ts);
-      if (kCountingSync) atomicAdd(&s_app[1], ts);
-    }
-    if (tb) {
-      bb = atomicAdd(&out->nB, tb);
-      if (kCountingSync) atomicAdd(&s_app[2], tb);
-    }
+    if (ts) bs = atomicAdd(&out->nH, ts);
+    if (tb) bb = atomicAdd(&out->nB, tb);
   }
   s0 = __shfl_sync(kFull, bs, 0) + is - CS;
   b0 = __shfl_sync(kFull, bb, 0) + ib - CB;
@@ -275,10 +243,7 @@ __device__ __forceinline__ void append_frontier(bool valid, uint32_t v, Off deg,
   unsigned lm = __ballot_sync(kFull, light);
   if (lm) {
     unsigned leader = __ffs(lm) - 1, base = 0;
-    if (lane == leader) {
-      base = atomicAdd(&out->nL, (unsigned)__popc(lm));
-      if (kCountingSync) atomicAdd(&s_app[0], (unsigned)__popc(lm));
-    }
+    if (lane == leader) base = atomicAdd(&out->nL, (unsigned)__popc(lm));
     base = __shfl_sync(kFull, base, leader);
     if (light) Lout[base + __popc(lm & lanemask_lt())] = light_entry<Off>(v, deg, begin);
   }
@@ -309,10 +274,7 @@ __device__ __forceinline__ void append_frontier4(const bool (&disc)[kU], const u
   }
   if (ltot) {
     unsigned base = 0;
-    if (lane == 0) {
-      base = atomicAdd(&out->nL, ltot);
-      if (kCountingSync) atomicAdd(&s_app[0], ltot);
-    }
+    if (lane == 0) base = atomicAdd(&out->nL, ltot);
     base = __shfl_sync(kFull, base, 0);
 #pragma unroll
     for (int t = 0; t < kU; ++t) {
@@ -345,8 +307,7 @@ template <typename Off, bool PARENTS>
 __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&valid)[kU],
                                             const uint32_t (&u)[kU], const uint32_t (&w)[kU],
                                             uint32_t* vis, int newdepth, uint4* Lout,
-                                            uint2* Hout, LevelCtr* out, Acc& acc, bool lowlat,
-                                            const uint32_t* svis, uint32_t pbits) {
+                                            uint2* Hout, LevelCtr* out, Acc& acc, bool lowlat) {
   uint32_t cur[kU];
   bool disc[kU];
   Off sb[kU], se[kU];
@@ -367,8 +328,7 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
     for (int t = 0; t < kU; ++t) disc[t] = valid[t] && !((cur[t] >> (w[t] & 31u)) & 1u);
   } else {
 #pragma unroll
-    for (int t = 0; t < kU; ++t)  // visited at level start (prefix) or now (global)
-      cur[t] = !valid[t] ? 0xFFFFFFFFu : (w[t] < pbits ? svis[w[t] >> 5] : vis[w[t] >> 5]);
+    for (int t = 0; t < kU; ++t) cur[t] = valid[t] ? vis[w[t] >> 5] : 0xFFFFFFFFu;
 #pragma unroll
     for (int t = 0; t < kU; ++t) {
       const uint32_t bit = 1u << (w[t] & 31u);
@@ -434,8 +394,7 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
 template <typename Off, bool PARENTS>
 __device__ __forceinline__ void push_round(const BfsArgs<Off>& a, uint32_t v, Off b, unsigned deg,
                                            uint4* Lout, uint2* Hout, LevelCtr* out,
-                                           uint32_t* vis, int newdepth, Acc& acc, bool lowlat,
-                                           const uint32_t* svis, uint32_t pbits) {
+                                           uint32_t* vis, int newdepth, Acc& acc, bool lowlat) {
   const unsigned lane = lane_id();
   const unsigned incl = warp_incl_scan(deg);
   const unsigned excl = incl - deg;
@@ -453,8 +412,7 @@ __device__ __forceinline__ void push_round(const BfsArgs<Off>& a, uint32_t v, Of
       valid[t] = e < tot;
       w[t] = valid[t] ? a.idx[bj + (Off)(e - xj)] : 0u;
     }
-    push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat,
-                              svis, pbits);
+    push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat);
   }
 }
 
@@ -475,7 +433,7 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
                            const uint2* Hin, unsigned nH, unsigned nB, const uint32_t* fr,
                            uint4* Lout,
                            uint2* Hout, LevelCtr* out, uint32_t* vis, int newdepth, Acc& acc,
-                           unsigned* sctr, bool lowlat, const uint32_t* svis, uint32_t pbits) {
+                           unsigned* sctr, bool lowlat) {
   const unsigned lane = lane_id();
   const unsigned NW = nwarps();
   unsigned R = 32;
@@ -505,8 +463,7 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
         u[t] = h.x;
         w[t] = valid[t] ? a.idx[p] : 0u;
       }
-      push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat,
-                                svis, pbits);
+      push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat);
     } else if (!fr) {
       const unsigned i = (item - nHC) * R + lane;
       uint32_t v = 0;
@@ -518,8 +475,7 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
         deg = le.y;
         b = light_begin<Off>(le);
       }
-      push_round<Off, PARENTS>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc, lowlat, svis,
-                               pbits);
+      push_round<Off, PARENTS>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc, lowlat);
     } else {
       const unsigned wbase = (item - nHC) * kPW;
       const uint32_t fw = lane < kPW ? fr[wbase + lane] : 0u;
@@ -540,8 +496,7 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
           b = a.off[v];
           deg = (unsigned)(a.off[v + 1] - b);
         }
-        push_round<Off, PARENTS>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc, lowlat, svis,
-                               pbits);
+        push_round<Off, PARENTS>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc, lowlat);
       }
     }
   }
@@ -588,23 +543,6 @@ __device__ __forceinline__ V8 ld_nc_v8(const uint32_t* p) {
   return v;
 }
 
-// Row-head load (32 B) with an L2 prefetch-size hint: candidates of a dense item have
-// adjacent heads, so an L2 miss may fetch the surrounding 128/256 B from HBM at once.
-__device__ __forceinline__ V8 ld_head_v8(const uint32_t* p) {
-  V8 v;
-#if PP_HEAD_L2PF == 256
-  asm volatile("ld.global.nc.L2::256B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-#elif PP_HEAD_L2PF == 128
-  asm volatile("ld.global.nc.L2::128B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-#else
-  asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-#endif
-               : "=r"(v.x[0]), "=r"(v.x[1]), "=r"(v.x[2]), "=r"(v.x[3]), "=r"(v.x[4]),
-                 "=r"(v.x[5]), "=r"(v.x[6]), "=r"(v.x[7])
-               : "l"(p));
-  return v;
-}
-
 template <typename Off, bool PARENTS>
 struct PullCtx {
   const BfsArgs<Off>& a;
@@ -616,8 +554,6 @@ struct PullCtx {
   uint32_t* sfound;
   ResidualQ<Off>& q;
   const uint32_t* ssum;  // shared-memory copy of the visited summary (snapshot)
-  const uint32_t* svis;  // shared-memory copy of the snapshot's first pbits bits
-  uint32_t pbits;
   uint2* hubs;           // no early exit: long-row chunk descriptors (2 uint2 each) ...
   unsigned* hub_count;   // ... and their count
 
@@ -626,7 +562,6 @@ struct PullCtx {
   // bit is confirmed against the exact snapshot bitmap).
   __device__ __forceinline__ bool hit(uint32_t x) const {
     if (no_reuse) return a.depth[a.perm ? a.perm[x] : x] == d;
-    if (x < pbits) return vprefix_bit(svis, x);
     if (kSumWordsMax) {
       const uint32_t gi = x >> a.sum_shift;
       if (!((ssum[gi >> 5] >> (gi & 31u)) & 1u)) return false;
@@ -669,11 +604,9 @@ struct PullCtx {
   }
   // discovery of row i (found this level): Alg. 1 lines 7-8 fused
   __device__ __forceinline__ void commit(uint32_t i, uint32_t par, Off degin, unsigned wbase,
-                                         bool in_item, uint32_t dpos, bool bit_by_caller = false) const {
+                                         bool in_item, uint32_t dpos) const {
     const uint32_t bit = 1u << (i & 31u);
-    if (bit_by_caller) {
-      // the caller ORs the bit into its item word with a warp reduction
-    } else if (in_item) {
+    if (in_item) {
       atomicOr(&sfound[(i >> 5) - wbase], bit);
     } else {
       atomicOr(&vout[i >> 5], bit);
@@ -835,33 +768,25 @@ template <typename Off, bool PARENTS>
 __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
                            uint32_t* __restrict__ vout, LevelCtr* out, int d, Acc& acc,
                            uint32_t* sfound, ResidualQ<Off>& rq, const uint32_t* ssum,
-                           unsigned* sctr, const uint32_t* svis, uint32_t pbits) {
+                           unsigned* sctr) {
   const unsigned lane = lane_id();
   const unsigned nitems = a.nwords / kPW;
   const bool no_mask = (a.toggles & PP_OPT_NO_MASKING) != 0;
   PullCtx<Off, PARENTS> C{a, vin, vout, d, !(a.toggles & PP_OPT_NO_EARLYEXIT),
                           (a.toggles & PP_OPT_NO_REUSE) != 0, acc, sfound, rq, ssum,
-                          svis, pbits, a.H0, &out->work2};
+                          a.H0, &out->work2};
   int qn = 0;
   unsigned wbase = 0;
-  // Guided schedule.  CTA b owns items b, b+G, ... (G = grid); its warps grab them in order
-  // through the shared-memory counter.  A kPW-word item is a chain of ~kPW*16/32 dependent
-  // candidate rounds, so a whole item as the last work of a phase leaves the CTA's other
-  // warps idle at the level barrier: the CTA's last kPullTail items are therefore handed
-  // out one bitmap word (32 rows) at a time.  The warp also grabs one step ahead and loads
-  // the next item's visited words while this one is processed.
+  // CTA b owns items b, b+G, ... (G = grid, interleaved so every CTA sees the same mix of
+  // heavy and light items); its warps grab them in order through the shared-memory counter.
+  // The warp grabs one step ahead and loads the next item's visited words meanwhile.
+  // (Handing a CTA's last items out one word at a time, or smaller items, measured slower:
+  // DESIGN.md §11.)
   const unsigned G = gridDim.x;
-  const unsigned J = nitems > blockIdx.x ? (nitems - blockIdx.x + G - 1) / G : 0u;
-  const unsigned T = min(J, kPullTail), JH = J - T, K = JH + T * kPW;
+  const unsigned K = nitems > blockIdx.x ? (nitems - blockIdx.x + G - 1) / G : 0u;
   auto map = [&](unsigned k, unsigned& w0, unsigned& pw) {
-    if (k < JH) {
-      w0 = (blockIdx.x + k * G) * kPW;
-      pw = kPW;
-    } else {
-      const unsigned kk = k - JH;
-      w0 = (blockIdx.x + (JH + kk / kPW) * G) * kPW + kk % kPW;
-      pw = 1u;
-    }
+    w0 = (blockIdx.x + k * G) * kPW;
+    pw = kPW;
   };
   auto grab = [&]() {
     unsigned j = 0;
@@ -884,7 +809,6 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
     // non-isolated row is computed and the result filtered afterwards.
     const uint32_t cand = no_mask ? (own ? ~a.isolated[wbase + lane] : 0u) : unvisited;
     sfound[lane] = 0u;
-    uint32_t fw_acc = 0u;  // kPullWarpOr: this lane's item word's found bits (lane < pw)
     const unsigned cnt = __popc(cand);
     const unsigned incl = warp_incl_scan(cnt);
     const unsigned excl = incl - cnt;
@@ -921,7 +845,7 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
           if (a.perm) dpos[t] = a.perm[i[t]];
           rb[t] = a.coff[i[t]];
           e[t] = a.coff[i[t] + 1];
-          hd[t] = ld_head_v8(a.head + (size_t)i[t] * 8u);
+          hd[t] = ld_nc_v8(a.head + (size_t)i[t] * 8u);
         }
       }
       // stage: probe the first neighbour, then the other head ids of rows that missed
@@ -936,26 +860,10 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
         const Off deg = e[t] - rb[t];
-#if PP_PULL_PROBE_SPLIT
-        // second id alone first (most rows the first id misses are decided by it): fewer
-        // scattered probes per candidate, one more dependent step for the rest
-        if (valid[t] && deg > 1 && !(found[t] && C.early_exit) && C.hit(hd[t].x[1])) {
-          if (!found[t]) {
-            found[t] = true;
-            par[t] = hd[t].x[1];
-          }
-        }
-        if (valid[t] && deg > 2 && !(found[t] && C.early_exit)) {
-          bool h[8];
-          h[1] = false;
-#pragma unroll
-          for (int q = 2; q < 8; ++q) h[q] = deg > (Off)q && C.hit(hd[t].x[q]);
-#else
         if (valid[t] && deg > 1 && !(found[t] && C.early_exit)) {
           bool h[8];
 #pragma unroll
           for (int q = 1; q < 8; ++q) h[q] = deg > (Off)q && C.hit(hd[t].x[q]);
-#endif
 #pragma unroll
           for (int q = 1; q < 8; ++q) {
             if (h[q] && !found[t]) {
@@ -968,22 +876,7 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
       }
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
-        if (found[t] && fresh[t])
-          C.commit(i[t], par[t], e[t] - rb[t], wbase, true, dpos[t], kPullWarpOr);
-        if (kPullWarpOr) {
-          // the round's rows are consecutive candidates, so their found bits fall in 1-3
-          // item words: one redux.sync OR per word instead of 32 same-word smem atomics
-          const bool fb = found[t] && fresh[t];
-          const unsigned wj = fb ? (i[t] >> 5) - wbase : 0xFFFFFFFFu;
-          const unsigned lo = __reduce_min_sync(kFull, wj);
-          if (lo != 0xFFFFFFFFu) {
-            const unsigned hi = __reduce_max_sync(kFull, fb ? wj : 0u);
-            for (unsigned j = lo; j <= hi; ++j) {
-              const uint32_t bits = __reduce_or_sync(kFull, wj == j ? (1u << (i[t] & 31u)) : 0u);
-              if (lane == j) fw_acc |= bits;
-            }
-          }
-        }
+        if (found[t] && fresh[t]) C.commit(i[t], par[t], e[t] - rb[t], wbase, true, dpos[t]);
         // park undecided rows (and, without early exit, rows with ids left)
         const bool park = valid[t] && p[t] < e[t] && !(found[t] && C.early_exit) &&
                           (fresh[t] || !found[t]);
@@ -1001,15 +894,9 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
       __syncwarp();
       while (qn >= 32) C.residual_batch(qn, 32, wbase, pw);
     }
-#if PP_PULL_CARRY
-    // residual rows (< 32) carry over into the next item and are committed with atomicOr
-    // once their item has closed, so a partial batch (one more dependent chain) is paid
-    // once per phase instead of once per item
-#else
     if (qn > 0) C.residual_batch(qn, qn, wbase, pw);
-#endif
     __syncwarp();
-    const uint32_t fw = own ? (sfound[lane] | fw_acc) : 0u;
+    const uint32_t fw = own ? sfound[lane] : 0u;
     if (own) {
       vout[wbase + lane] = vw | fw;
       a.fr[wbase + lane] = fw;
@@ -1027,7 +914,6 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
     }
     __syncwarp();
   }
-  if (qn > 0) C.residual_batch(qn, qn, wbase, 0u);  // items closed: atomicOr commits
 }
 
 // No-early-exit pull, second part: the long-row chunks emitted by tier 2, grabbed by every
@@ -1038,11 +924,10 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
 template <typename Off, bool PARENTS>
 __device__ void pull_hub_chunks(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
                                 uint32_t* __restrict__ vout, LevelCtr* out, unsigned nch, int d,
-                                Acc& acc, ResidualQ<Off>& rq, const uint32_t* svis,
-                                uint32_t pbits) {
+                                Acc& acc, ResidualQ<Off>& rq) {
   const unsigned lane = lane_id();
   PullCtx<Off, PARENTS> C{a, vin, vout, d, false, (a.toggles & PP_OPT_NO_REUSE) != 0, acc,
-                          nullptr, rq, nullptr, svis, pbits, a.H0, nullptr};
+                          nullptr, rq, nullptr, a.H0, nullptr};
   while (true) {
     unsigned j = 0;
     if (lane == 0) j = atomicAdd(&out->work, 1u);
@@ -1127,9 +1012,7 @@ struct BfsShared {  // static part; the residual queues live in dynamic shared m
   uint32_t sfound[kBfsWarps][32];
   unsigned long long red[kBfsWarps][4];
   long long lvl[7];  // c, m_f, m_fin, nL, nH, nbig, nB of the level just finished
-  unsigned long long vprev[2][7];  // level_sync: running sums of each slot at its last use
   unsigned work;     // CTA-local work counter (cta_grab)
-  int ok;
 };
 
 // thread 0 reads a level's counters once (post-barrier) and broadcasts them via smem
@@ -1148,118 +1031,12 @@ __device__ __forceinline__ void read_level(const LevelCtr* out, BfsShared<Off>& 
   __syncthreads();
 }
 
-// Counting level sync: the end of every phase (init, level, Dense2sparse) in ONE exchange.
-// The CTA's counters (c, m_f, m_fin, nbig from the lanes; nL, nH, nB from s_app) are reduced
-// warp -> CTA; thread 0 then issues a release fence and adds (value << 24) + 1 to each of
-// the 8 words of slot (phase & 1) with fire-and-forget reductions, and polls the slot until
-// every word's low 24 bits show all G arrivals of this phase (mod 2^24: the arrival total
-// after u uses of a slot is u*G exactly, and a CTA is at most one phase ahead, hence two
-// slots).  The polled words themselves carry the level's totals, so the old sequence
-// (counter atomics, a release atomic that waits for them, the barrier poll, then a
-// separate load of the counters) loses one arrival round trip and the counter-read round
-// trip.  Fence-then-relaxed-add / relaxed-poll-then-fence is the release/acquire pattern
-// that publishes the phase's data writes (depths, bitmaps, lists) to every CTA.
-__device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ ulonglong2 ld_relaxed_u64x2(const unsigned long long* p) {
-  ulonglong2 v;
-  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0,%1}, [%2];" : "=l"(v.x), "=l"(v.y) : "l"(p) : "memory");
-  return v;
-}
-
-template <typename Off>
-__device__ __forceinline__ bool level_sync(Acc& acc, BfsShared<Off>& sh, GridBarrier* bar,
-                                           BfsStatus* st, unsigned& ph) {
-  const unsigned warp = threadIdx.x >> 5, lane = lane_id();
-  const bool any = __any_sync(kFull, (acc.c | acc.mf | acc.mfin | acc.big) != 0ull);
-  unsigned long long c = 0, mf = 0, mfin = 0, big = 0;
-  if (any) {
-    c = warp_sum(acc.c);
-    mf = warp_sum(acc.mf);
-    mfin = warp_sum(acc.mfin);
-    big = warp_sum(acc.big);
-  }
-  if (lane == 0) {
-    sh.red[warp][0] = c;
-    sh.red[warp][1] = mf;
-    sh.red[warp][2] = mfin;
-    sh.red[warp][3] = big;
-  }
-  acc.c = acc.mf = acc.mfin = acc.big = 0;
-  __syncthreads();
-  if (warp == 0) {
-    const bool in = lane < (unsigned)kBfsWarps;
-    unsigned long long v[4];
-#pragma unroll
-    for (int f = 0; f < 4; ++f) v[f] = in ? sh.red[lane][f] : 0ull;
-    if (__any_sync(kFull, (v[0] | v[1] | v[2] | v[3]) != 0ull)) {
-#pragma unroll
-      for (int f = 0; f < 4; ++f) v[f] = warp_sum(v[f]);
-    }
-    if (lane == 0) {
-      const unsigned slot = ph & 1u;
-      unsigned long long* pk = &bar->pk[slot][0][0];  // word f at pk[f * kSyncStride]
-      const unsigned long long expect = (unsigned long long)(ph / 2u + 1u) * gridDim.x;
-      const unsigned long long vals[8] = {v[0], v[1], v[2], s_app[0], s_app[1], v[3], s_app[2], 0ull};
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");  // release this CTA's phase writes
-#pragma unroll
-      for (int f = 0; f < 8; ++f) red_add_u64(pk + f * kSyncStride, (vals[f] << 24) + 1ull);
-      unsigned long long w[8];
-      bool ok = true;
-      const unsigned long long t0 = global_timer_ns();
-      while (true) {
-        if (kSyncStride == 1) {
-#pragma unroll
-          for (int f = 0; f < 8; f += 2) {
-            const ulonglong2 x = ld_relaxed_u64x2(pk + f);
-            w[f] = x.x;
-            w[f + 1] = x.y;
-          }
-        } else {
-#pragma unroll
-          for (int f = 0; f < 8; ++f) w[f] = ld_relaxed_u64(pk + f * kSyncStride);
-        }
-        bool done = true;
-#pragma unroll
-        for (int f = 0; f < 8; ++f) done &= ((w[f] - expect) & 0xFFFFFFull) == 0ull;
-        if (done) break;
-        if (ld_relaxed_u64(&bar->count) & kAbortBit) {
-          ok = false;
-          break;
-        }
-        if (global_timer_ns() - t0 > kWatchdogNs) {
-          atomicExch(&st->error, (int)PP_ERR_TIMEOUT);
-          atomicOr(reinterpret_cast<unsigned long long*>(&bar->count), kAbortBit);
-          ok = false;
-          break;
-        }
-        __nanosleep(16);
-      }
-      asm volatile("fence.acq_rel.gpu;" ::: "memory");  // acquire every CTA's phase writes
-#pragma unroll
-      for (int f = 0; f < 7; ++f) {
-        const unsigned long long tot = (w[f] - expect) >> 24;  // running sum over this slot
-        sh.lvl[f] = (long long)(tot - sh.vprev[slot][f]);
-        sh.vprev[slot][f] = tot;
-      }
-      s_app[0] = s_app[1] = s_app[2] = 0u;
-      sh.work = 0u;
-      sh.ok = ok ? 1 : 0;
-      ++ph;
-    }
-  }
-  __syncthreads();
-  return sh.ok != 0;
-}
-
 template <typename Off, bool PARENTS>
 __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   __shared__ BfsShared<Off> sh;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   ResidualQ<Off>* rqs = reinterpret_cast<ResidualQ<Off>*>(dyn_smem);
   uint32_t* ssum = reinterpret_cast<uint32_t*>(dyn_smem + sizeof(ResidualQ<Off>) * kBfsWarps);
-  uint32_t* svis = ssum + kSumWordsMax;
   const unsigned warp = threadIdx.x >> 5;
   const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   const unsigned long long gsize = (unsigned long long)gridDim.x * blockDim.x;
@@ -1268,11 +1045,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   if (!a.resume && blockIdx.x == 0 && threadIdx.x == 0)
     a.status->t_start = (long long)global_timer_ns();
   unsigned epoch = 0;  // grid barriers passed (thread 0)
-  unsigned ph = 0;     // level_sync phases passed (thread 0)
-  if (kCountingSync && threadIdx.x == 0) {
-    for (int f = 0; f < 7; ++f) sh.vprev[0][f] = sh.vprev[1][f] = 0ull;
-    s_app[0] = s_app[1] = s_app[2] = 0u;
-  }
+
 
   int dir = (a.mode == 2) ? 1 : 0;
   int cur = 0;  // visited bitmap in use
@@ -1338,25 +1111,20 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       const unsigned nch = (unsigned)((deg + (Off)kChunk - 1) / (Off)kChunk);
       if (nch <= kSelfChunks) {
         for (unsigned k = threadIdx.x; k < nch; k += blockDim.x) a.H0[k] = make_uint2(s, k);
-        if (threadIdx.x == 0) a.ctr[0].nH = s_app[1] = nch;
+        if (threadIdx.x == 0) a.ctr[0].nH = nch;
       } else {
         const unsigned nb = (nch + 31u) / 32u;
         for (unsigned j = threadIdx.x; j < nb; j += blockDim.x)
           a.H0[a.hcap - 1u - j] = make_uint2(s, 32u * j);
-        if (threadIdx.x == 0) a.ctr[0].nB = s_app[2] = nb;
+        if (threadIdx.x == 0) a.ctr[0].nB = nb;
       }
     } else if (deg > 0 && threadIdx.x == 0) {
       a.L0[0] = light_entry<Off>(s, deg, a.off[s]);
-      a.ctr[0].nL = s_app[0] = 1;
+      a.ctr[0].nL = 1;
     }
   }
-  if (kCountingSync) {
-    Acc acc0{0, 0, 0, 0};
-    if (!level_sync<Off>(acc0, sh, a.bar, a.status, ph)) return;
-  } else {
-    if (!level_barrier(a.narrow, a.bar, a.status, epoch)) return;
-    read_level(&a.ctr[0], sh);
-  }
+  if (!level_barrier(a.narrow, a.bar, a.status, epoch)) return;
+  read_level(&a.ctr[0], sh);
   if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t_init = (long long)global_timer_ns();
   nL = (unsigned)sh.lvl[3];
   nH = (unsigned)sh.lvl[4];
@@ -1389,14 +1157,11 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       reinterpret_cast<unsigned*>(&a.ctr[(d + 1) & (kRing - 1)])[threadIdx.x] = 0u;
     uint32_t* vis = cur ? a.vis1 : a.vis0;
     uint32_t* vis_other = cur ? a.vis0 : a.vis1;
-    const bool heavy_level = dir == 0 ? (unsigned long long)mf_last >= kVPrefixMinEdges
-                                      : (unsigned long long)m_u >= kVPrefixMinEdges;
-    const uint32_t pbits = (heavy_level && a.perm) ? load_vprefix(vis, svis, a.nwords) : 0u;
     if (dir == 0) {
       push_phase<Off, PARENTS>(a, sel ? a.L1 : a.L0, from_bits ? 0u : nL, sel ? a.H1 : a.H0,
                                from_bits ? 0u : nH, from_bits ? 0u : nB, from_bits ? a.fr : nullptr,
                                sel ? a.L0 : a.L1, sel ? a.H0 : a.H1, out, vis, d + 1, acc,
-                               &sh.work, (unsigned long long)mf_last <= kLowLatEdges, svis, pbits);
+                               &sh.work, (unsigned long long)mf_last <= kLowLatEdges);
       from_bits = false;
     } else {
       if (kSumWordsMax) {
@@ -1404,23 +1169,18 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
         __syncthreads();
       }
       pull_phase<Off, PARENTS>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp],
-                               ssum, &sh.work, svis, pbits);
+                               ssum, &sh.work);
       if (a.toggles & PP_OPT_NO_EARLYEXIT) {  // ablation arms: long rows grid-wide
         if (!level_barrier(a.narrow, a.bar, a.status, epoch)) return;
         const unsigned nch = ld_relaxed_u32(&out->work2);
-        if (nch) pull_hub_chunks<Off, PARENTS>(a, vis, vis_other, out, nch, d, acc, rqs[warp], svis,
-                                                pbits);
+        if (nch) pull_hub_chunks<Off, PARENTS>(a, vis, vis_other, out, nch, d, acc, rqs[warp]);
       }
     }
     if (a.dbg && threadIdx.x == 0 && d - 1 < a.dbg_levels)
       a.dbg[(size_t)(d - 1) * gridDim.x + blockIdx.x] = (long long)global_timer_ns() - t_lvl;
-    if (kCountingSync) {
-      if (!level_sync<Off>(acc, sh, a.bar, a.status, ph)) return;
-    } else {
-      flush_acc(acc, out, sh.red);
-      if (!level_barrier(a.narrow, a.bar, a.status, epoch)) return;
-      read_level(out, sh);
-    }
+    flush_acc(acc, out, sh.red);
+    if (!level_barrier(a.narrow, a.bar, a.status, epoch)) return;
+    read_level(out, sh);
     const long long c_new = sh.lvl[0], mf = sh.lvl[1], mfin = sh.lvl[2];
     nL = (unsigned)sh.lvl[3];
     nH = (unsigned)sh.lvl[4];
@@ -1452,12 +1212,8 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       uint32_t* vnew = cur ? a.vis1 : a.vis0;
       uint32_t* vold = cur ? a.vis0 : a.vis1;
       convert_phase<Off>(a, vnew, vold, sel ? a.L1 : a.L0, sel ? a.H1 : a.H0, out, &sh.work);
-      if (kCountingSync) {
-        if (!level_sync<Off>(acc, sh, a.bar, a.status, ph)) return;
-      } else {
-        if (!level_barrier(a.narrow, a.bar, a.status, epoch)) return;
-        read_level(out, sh);
-      }
+      if (!level_barrier(a.narrow, a.bar, a.status, epoch)) return;
+      read_level(out, sh);
       nL = (unsigned)sh.lvl[3];
       nH = (unsigned)sh.lvl[4];
       nB = (unsigned)sh.lvl[6];
@@ -1481,7 +1237,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
 
 template <typename Off>
 constexpr size_t dyn_smem_bytes() {
-  return sizeof(ResidualQ<Off>) * kBfsWarps + sizeof(uint32_t) * (kSumWordsMax + kVPrefixWords);
+  return sizeof(ResidualQ<Off>) * kBfsWarps + sizeof(uint32_t) * kSumWordsMax;
 }
 
 template <typename Off, bool PARENTS>
@@ -1540,7 +1296,7 @@ static cudaError_t launch_narrow(pp_graph g, const BfsArgs<Off>& args) {
 // PP_NARROW unset or 0: never; 1: always (tests of the hand-over on any graph);
 // 2: for graphs with max out-degree <= kNarrowMaxDeg.
 static bool use_narrow(pp_graph g, int mode) {
-  if (kCountingSync || mode == 2) return false;
+  if (mode == 2) return false;
   // Measured slower than the whole grid on C4 and RGG24, so opt-in only.
   const char* e = getenv("PP_NARROW");
   if (e && e[0] == '1') return true;

@@ -35,24 +35,6 @@ constexpr unsigned kBig = 1024;    // pull->push goes straight from the bitmap i
 #endif
 constexpr int kBfsBlock = PP_BFS_BLOCK;  // persistent BFS: one CTA per SM
 constexpr int kBfsWarps = kBfsBlock / 32;
-#ifndef PP_PULL_TAIL
-#define PP_PULL_TAIL 0
-#endif
-constexpr unsigned kPullTail = PP_PULL_TAIL;  // pull: a CTA's last kPullTail items are handed
-                                              // out one bitmap word at a time (guided schedule)
-#ifndef PP_PULL_CARRY
-#define PP_PULL_CARRY 0
-#endif
-#ifndef PP_PULL_PROBE_SPLIT
-#define PP_PULL_PROBE_SPLIT 0
-#endif
-#ifndef PP_PULL_WARPOR
-#define PP_PULL_WARPOR 0
-#endif
-constexpr bool kPullWarpOr = PP_PULL_WARPOR != 0;  // pull: found bits by warp reduction
-#ifndef PP_HEAD_L2PF
-#define PP_HEAD_L2PF 0
-#endif
 #ifndef PP_INIT_VEC
 #define PP_INIT_VEC 1
 #endif
@@ -61,26 +43,6 @@ constexpr bool kInitVec = PP_INIT_VEC != 0;  // BFS init: 16-byte depth stores
 #define PP_VREC 1
 #endif
 constexpr bool kVrec = PP_VREC != 0;  // relabelled graphs: per-vertex {begin, deg, caller id}
-#ifndef PP_VPREFIX_WORDS
-#define PP_VPREFIX_WORDS 0
-#endif
-constexpr unsigned kVPrefixWords = PP_VPREFIX_WORDS;  // BFS: shared-memory copy of the first
-                                  // 32*kVPrefixWords bits of the visited bitmap at level start
-                                  // (with PP_GRAPH_RELABEL: the highest-degree vertices, the
-                                  // targets of most probes); 0 = off
-#ifndef PP_VPREFIX_MIN_EDGES
-#define PP_VPREFIX_MIN_EDGES 262144
-#endif
-constexpr unsigned long long kVPrefixMinEdges = PP_VPREFIX_MIN_EDGES;  // ... only for levels
-                                  // whose work (push: m_f; pull: m_u) is at least this
-#ifndef PP_COUNTING_SYNC
-#define PP_COUNTING_SYNC 0
-#endif
-constexpr bool kCountingSync = PP_COUNTING_SYNC != 0;  // bfs: level_sync instead of
-                                  // counter atomics + grid barrier + counter read
-#ifndef PP_BAR_FENCE_SC
-#define PP_BAR_FENCE_SC 1
-#endif
 
 // Per-level counters, written with atomics during a level, read after the grid barrier.
 struct LevelCtr {
@@ -102,10 +64,6 @@ struct LevelStat {
   long long t_ns;  // %globaltimer when the level's barrier released (block 0)
 };
 
-#ifndef PP_SYNC_STRIDE
-#define PP_SYNC_STRIDE 32
-#endif
-constexpr int kSyncStride = PP_SYNC_STRIDE;
 // Narrow -> wide hand-over of the BFS loop state (bfs.cu, narrow mode).
 struct BfsResume {
   int valid, done;  // valid: the wide kernel continues at level d; done: BFS finished
@@ -129,11 +87,6 @@ struct GridBarrier {
   unsigned int pad0[30];
   unsigned int gen;
   unsigned int pad1[31];
-  // counting level sync (bfs.cu level_sync): two alternating slots of 8 words; every CTA
-  // adds (value << 24) + 1 to each word once per phase, so a word carries its own arrival
-  // count (low 24 bits) next to the running sum of the per-CTA values (zeroed per launch)
-  unsigned long long pk[2][8][kSyncStride];  // word f of slot s at pk[s][f][0]: one word per
-                                             // kSyncStride*8 bytes, spread over L2 slices
   BfsResume rs;
 };
 

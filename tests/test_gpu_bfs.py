@@ -70,6 +70,7 @@ def small_graphs():
     out["directed_random"] = synth.random_graph(2500, 9000, seed=3, symmetrize=False)
     out["rmat_s12"] = synth.rmat(12, 8, seed=5)
     out["pgrid"] = synth.percolated_grid(60, 60, 0.6, seed=2)
+    out["rgg_s13"] = synth.rgg(13, 0.55, seed=4)  # random geometric graph (NEXT-2 shape)
     return out
 
 
