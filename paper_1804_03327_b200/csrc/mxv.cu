@@ -15,6 +15,10 @@
 namespace pp {
 
 constexpr int kGridPerSM = 4;
+#ifndef PP_STREAM_U
+#define PP_STREAM_U 8
+#endif
+constexpr int kStreamU = PP_STREAM_U;  // row mxv without early exit: id loads in flight per lane
 constexpr unsigned kHubIds = 1024;  // row-mxv rows with more ids left go to k_mxv_pull_hubs
 
 static int grid_blocks(pp_graph g) { return g->ctx->num_sms * kGridPerSM; }
@@ -265,15 +269,25 @@ __global__ void __launch_bounds__(kBlock) k_mxv_pull_stream(
       const unsigned excl = incl - deg;
       const unsigned tot = __shfl_sync(kFull, incl, 31);
       uint32_t t = 0;
-      for (unsigned base = 0; base < tot; base += 128) {
+      // kStreamU coalesced id loads per lane in flight per step, then their probes
+      for (unsigned base = 0; base < tot; base += 32u * kStreamU) {
+        uint32_t x[kStreamU];
+        unsigned jj[kStreamU];
+        bool ok[kStreamU];
 #pragma unroll
-        for (int s2 = 0; s2 < 4; ++s2) {
+        for (int s2 = 0; s2 < kStreamU; ++s2) {
           const unsigned q = base + (unsigned)s2 * 32u + lane;
           const unsigned j = warp_owner(incl, q);
           const Off bj = __shfl_sync(kFull, b, j);
           const unsigned xj = __shfl_sync(kFull, excl, j);
-          const bool hit = q < tot && bit_test(ubits, ridx[bj + (Off)(q - xj)]);
-          t |= __reduce_or_sync(kFull, hit ? (1u << j) : 0u);
+          jj[s2] = j;
+          ok[s2] = q < tot;
+          x[s2] = ok[s2] ? ridx[bj + (Off)(q - xj)] : 0u;
+        }
+#pragma unroll
+        for (int s2 = 0; s2 < kStreamU; ++s2) {
+          const bool hit = ok[s2] && bit_test(ubits, x[s2]);
+          t |= __reduce_or_sync(kFull, hit ? (1u << jj[s2]) : 0u);
         }
       }
       if (lane == wl) myt = t;
