@@ -220,3 +220,22 @@ def make(config: str) -> CSR:
         g = percolated_grid(c["rows"], c["cols"], c["p"], c["seed"])
     g.name = config + ":" + g.name
     return g
+
+
+def edge_weights(nnz: int, seed: int = 3, lo: int = 1, hi: int = 10, integer: bool = True) -> np.ndarray:
+    """Seeded non-negative edge weights (SURVEY NEXT-4 / SPEC S:345 recipe: integers lo..hi,
+    or uniform reals in [lo, hi) when integer=False).  float32-exact values either way."""
+    rng = np.random.default_rng(seed)
+    if integer:
+        return rng.integers(lo, hi + 1, size=nnz).astype(np.float32)
+    return rng.uniform(lo, hi, size=nnz).astype(np.float32)
+
+
+def transpose_weighted(g: CSR, w: np.ndarray):
+    """CSC of a weighted CSR: (CSR of A^T, weights aligned with it).  Plumbing only."""
+    rows = np.repeat(np.arange(g.n, dtype=np.int64), np.diff(g.off))
+    order = np.lexsort((rows, g.idx.astype(np.int64)))
+    cidx = rows[order].astype(np.uint32)
+    coff = np.zeros(g.n + 1, np.int64)
+    np.cumsum(np.bincount(g.idx.astype(np.int64), minlength=g.n), out=coff[1:])
+    return CSR(g.n, coff, cidx, g.symmetric, g.name + "^T"), np.ascontiguousarray(w[order])
