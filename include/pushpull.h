@@ -220,6 +220,31 @@ pp_status pp_ctx_create_dist(int device, void* cuda_stream, const void* nccl_uni
 pp_status pp_partition(int64_t n, int32_t rank, int32_t nranks, int64_t* row_lo, int64_t* row_hi);
 pp_status pp_graph_partition(pp_graph g, int64_t* row_lo, int64_t* row_hi);
 
+/* ---- SSSP over the min-plus semiring (Sec. 5.6) ------------
+ * The paper's "simple 2-phase direction-optimized traversal" for SSSP: Bellman-Ford
+ * d <- min(d, A^T (min.+) f) with an active-vertex frontier f; unmasked column-based (push)
+ * mxv while nnz(f)/n <= alpha, then ONE switch to row-based (pull) mxv until f is empty.
+ * No mask, no early exit; the pull reads all of d (operand reuse).  Jacobi
+ * iteration, so the iteration count is deterministic (R28-R30).
+ * Arguments (ALL pointers are DEVICE memory the caller owns; nothing is retained):
+ *   csr_off[n+1] int64, csr_idx[nnz] uint32, csr_w[nnz] fp32: A by rows (out-edges, A(i,j)=w);
+ *   csc_off/csc_idx/csc_w: the same matrix by columns (rows of A^T, in-edges);
+ *   source in [0, n); alpha >= 0 the switch threshold on nnz(f)/n;
+ *   dist[n] fp32 output: 0 at the source, +inf where unreachable.
+ * Stream-ordered on the ctx stream; synchronises it once per iteration (frontier size).
+ * Errors: PP_ERR_ARG (NULL / n <= 0 / alpha < 0), PP_ERR_RANGE (source), PP_ERR_GRAPH
+ * (a negative or NaN weight), PP_ERR_CUDA / PP_ERR_OOM. */
+typedef struct {
+  int64_t iterations;        /* matvec steps run (the last one finds f empty)            */
+  int64_t push_iterations;   /* column-based steps                                       */
+  int64_t pull_iterations;   /* row-based steps                                          */
+  int64_t switch_iteration;  /* index of the first pull step, -1 if none                 */
+} pp_sssp_stats;
+pp_status pp_sssp(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr_off, const uint32_t* csr_idx,
+                  const float* csr_w, const int64_t* csc_off, const uint32_t* csc_idx,
+                  const float* csc_w, int64_t source, double alpha, float* dist,
+                  pp_sssp_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -65,6 +65,11 @@ class pp_bfs_options(ctypes.Structure):
                 ("want_parents", ctypes.c_int32), ("toggles", ctypes.c_uint32)]
 
 
+class pp_sssp_stats(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int64), ("push_iterations", ctypes.c_int64),
+                ("pull_iterations", ctypes.c_int64), ("switch_iteration", ctypes.c_int64)]
+
+
 class pp_bfs_stats(ctypes.Structure):
     _fields_ = [("levels", ctypes.c_int32), ("reached", ctypes.c_int64),
                 ("capacity", ctypes.c_int32), ("dir", ctypes.POINTER(ctypes.c_int8)),
@@ -98,6 +103,8 @@ _SIGS = {
     "pp_partition": ([_i64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
                      ctypes.c_int),
     "pp_graph_partition": ([_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)], ctypes.c_int),
+    "pp_sssp": ([_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64, ctypes.c_double, _vp,
+                 ctypes.POINTER(pp_sssp_stats)], ctypes.c_int),
 }
 for _name, (_args, _res) in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -378,3 +385,26 @@ def header_functions():
     with open(hdr) as f:
         text = f.read()
     return sorted(set(re.findall(r"^\s*(?:pp_status|const char\*)\s+(pp_\w+)\s*\(", text, re.M)))
+
+
+def pp_sssp(ctx, n, nnz, csr_off, csr_idx, csr_w, csc_off, csc_idx, csc_w, source, alpha, dist):
+    """C-ABI pp_sssp (include/pushpull.h; Sec. 5.6).  All arrays are device tensors."""
+    st = pp_sssp_stats()
+    _check(_lib.pp_sssp(ctx, int(n), int(nnz), _ptr(csr_off), _ptr(csr_idx), _ptr(csr_w), _ptr(csc_off),
+                        _ptr(csc_idx), _ptr(csc_w), int(source), float(alpha), _ptr(dist),
+                        ctypes.byref(st)))
+    return {"iterations": st.iterations, "push_iterations": st.push_iterations,
+            "pull_iterations": st.pull_iterations, "switch_iteration": st.switch_iteration}
+
+
+def sssp(ctx: Context, csr_off, csr_idx, csr_w, csc_off, csc_idx, csc_w, source: int,
+         alpha: float = 0.01, dist=None):
+    """Two-phase min-plus SSSP on device tensors (int64 offsets, int32/uint32 ids, fp32
+    weights).  Returns (dist fp32 device tensor, stats dict)."""
+    import torch
+    n = int(csr_off.numel()) - 1
+    if dist is None:
+        dist = torch.empty(n, dtype=torch.float32, device=csr_off.device)
+    st = pp_sssp(ctx.handle, n, int(csr_idx.numel()), csr_off, csr_idx, csr_w, csc_off, csc_idx,
+                 csc_w, source, alpha, dist)
+    return dist, st

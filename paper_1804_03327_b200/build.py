@@ -7,7 +7,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libpushpull.so")
-SOURCES = ["bfs.cu", "mxv.cu", "graph.cu", "relabel.cu", "dist.cu", "capi.cpp"]
+SOURCES = ["bfs.cu", "mxv.cu", "graph.cu", "relabel.cu", "dist.cu", "sssp.cu", "capi.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
          "-Xcompiler", "-fPIC,-O3", "-shared", "-cudart", "static", "-I", os.path.join(ROOT, "include"),

@@ -1,0 +1,199 @@
+// sssp.cu — SURVEY NEXT-4: the paper's generality claim (Sec. 5.6): SSSP as
+// Bellman-Ford over the min-plus semiring through the same push / pull matvec shapes, with
+// the "simple 2-phase direction-optimized traversal": unmasked column-based (push) mxv
+// while the active set is small, ONE switch to row-based (pull) mxv once nnz(f)/n > alpha.
+// No mask and no early exit (Boolean-only); operand reuse in the pull: the
+// row reads all of d instead of f.  Jacobi iteration (R28):
+//   t = d_k;  t(j) = min(t(j), d_k(i) + A(i,j)) over the step's edges;  f_{k+1} = {t < d_k};
+//   d_{k+1} = t.
+// Distances and non-negative weights are fp32 (R30); non-negative floats order like their
+// int32 bit patterns, so the push's min-reduction is a plain atomicMin on the bits.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "pp_internal.h"
+
+namespace {
+
+constexpr int kT = 256;                 // threads per CTA
+constexpr unsigned kInfBits = 0x7f800000u;
+
+__global__ void k_sssp_init(int64_t n, int64_t s, float* __restrict__ d, float* __restrict__ t,
+                            uint32_t* __restrict__ list, unsigned* __restrict__ cnt) {
+  const float inf = __int_as_float(kInfBits);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float v = i == s ? 0.f : inf;
+    d[i] = v;
+    t[i] = v;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    list[0] = (uint32_t)s;
+    cnt[0] = 0;  // next-frontier length
+    cnt[1] = 0;  // error flag (negative / NaN weight)
+  }
+}
+
+// negative weights are rejected (NaN fails w >= 0 too).
+__global__ void k_sssp_check(int64_t nnz, const float* __restrict__ w, unsigned* __restrict__ cnt) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x)
+    if (!(w[e] >= 0.f)) cnt[1] = 1;
+}
+
+// Column-based step (push, Alg. 3 shape P:370): one warp per active vertex u scatters
+// d(u) + A(u, v) into t(v).  The thread whose atomicMin moves t(v) off d(v) appends v.
+__global__ void k_sssp_push(const uint32_t* __restrict__ f, unsigned nf, const int64_t* __restrict__ off,
+                            const uint32_t* __restrict__ idx, const float* __restrict__ w,
+                            const float* __restrict__ d, float* __restrict__ t,
+                            uint32_t* __restrict__ next, unsigned* __restrict__ cnt) {
+  const unsigned lane = threadIdx.x & 31;
+  const unsigned nw = gridDim.x * (blockDim.x >> 5);
+  for (unsigned k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < nf; k += nw) {
+    const uint32_t u = f[k];
+    const float du = d[u];
+    const int64_t b = off[u], e = off[u + 1];
+    for (int64_t j = b + lane; j < e; j += 32) {
+      const uint32_t v = __ldg(idx + j);
+      const float nd = du + __ldg(w + j);
+      if (nd < t[v]) {
+        const int old = atomicMin(reinterpret_cast<int*>(t) + v, __float_as_int(nd));
+        if (__float_as_int(nd) < old && old == __float_as_int(d[v]))
+          next[atomicAdd(cnt, 1u)] = v;
+      }
+    }
+  }
+}
+
+// Row-based step (pull, Alg. 2 shape P:320 without mask / early exit): one warp per row j
+// of A^T reduces min_i d(i) + A(i, j) over the in-edges (operand reuse: all of d).
+__global__ void k_sssp_pull(int64_t n, const int64_t* __restrict__ coff, const uint32_t* __restrict__ cidx,
+                            const float* __restrict__ cw, const float* __restrict__ d,
+                            float* __restrict__ t, uint32_t* __restrict__ next, unsigned* __restrict__ cnt) {
+  const unsigned lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t j = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); j < n; j += nw) {
+    const int64_t b = coff[j], e = coff[j + 1];
+    float m = __int_as_float(kInfBits);
+    for (int64_t q = b + lane; q < e; q += 32) m = fminf(m, d[__ldg(cidx + q)] + __ldg(cw + q));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0 && m < d[j]) {
+      t[j] = m;
+      next[atomicAdd(cnt, 1u)] = (uint32_t)j;
+    }
+  }
+}
+
+// d_{k+1} = t on the changed set (t == d elsewhere).
+__global__ void k_sssp_commit(const uint32_t* __restrict__ list, const unsigned* __restrict__ cnt,
+                              const float* __restrict__ t, float* __restrict__ d) {
+  const unsigned nf = *cnt;
+  for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < nf; k += gridDim.x * blockDim.x) {
+    const uint32_t v = list[k];
+    d[v] = t[v];
+  }
+}
+
+unsigned grid_for(int64_t work, int per_block, int cap) {
+  int64_t g = (work + per_block - 1) / per_block;
+  return (unsigned)(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+}  // namespace
+
+using namespace pp;
+
+#define SS_CK(call, what)                                        \
+  do {                                                           \
+    cudaError_t _e = (call);                                     \
+    if (_e != cudaSuccess) { st = cuda_fail(_e, what); goto out; } \
+  } while (0)
+
+extern "C" pp_status pp_sssp(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr_off,
+                             const uint32_t* csr_idx, const float* csr_w, const int64_t* csc_off,
+                             const uint32_t* csc_idx, const float* csc_w, int64_t source,
+                             double alpha, float* dist, pp_sssp_stats* stats) {
+  if (!ctx || !csr_off || !csc_off || !dist || (nnz > 0 && (!csr_idx || !csr_w || !csc_idx || !csc_w))) {
+    set_error("pp_sssp: NULL argument");
+    return PP_ERR_ARG;
+  }
+  if (n <= 0 || nnz < 0 || n >= (int64_t)UINT32_MAX) {
+    set_error("pp_sssp: n=%lld nnz=%lld invalid", (long long)n, (long long)nnz);
+    return PP_ERR_ARG;
+  }
+  if (source < 0 || source >= n) {
+    set_error("pp_sssp: source %lld out of range [0, %lld)", (long long)source, (long long)n);
+    return PP_ERR_RANGE;
+  }
+  if (!(alpha >= 0.0)) {
+    set_error("pp_sssp: alpha must be >= 0");
+    return PP_ERR_ARG;
+  }
+  pp_status st = PP_OK;
+  cudaStream_t s = ctx->stream;
+  const int cap = ctx->num_sms * 8;
+  float* t = nullptr;
+  uint32_t *la = nullptr, *lb = nullptr;
+  unsigned* cnt = nullptr;
+  unsigned h[2] = {0, 0};
+  int64_t it = 0, push_it = 0, pull_it = 0, sw = -1;
+  int dir = 0;  // 0 push, 1 pull
+  unsigned nf = 1;
+  SS_CK(cudaSetDevice(ctx->device), "pp_sssp: cudaSetDevice");
+  SS_CK(cudaMallocAsync((void**)&t, sizeof(float) * n, s), "pp_sssp: alloc t");
+  SS_CK(cudaMallocAsync((void**)&la, sizeof(uint32_t) * n, s), "pp_sssp: alloc list");
+  SS_CK(cudaMallocAsync((void**)&lb, sizeof(uint32_t) * n, s), "pp_sssp: alloc list");
+  SS_CK(cudaMallocAsync((void**)&cnt, sizeof(unsigned) * 2, s), "pp_sssp: alloc counters");
+  k_sssp_init<<<grid_for(n, kT, cap), kT, 0, s>>>(n, source, dist, t, la, cnt);
+  ctx->launches++;
+  if (nnz > 0) {
+    k_sssp_check<<<grid_for(nnz, kT, cap), kT, 0, s>>>(nnz, csr_w, cnt);
+    k_sssp_check<<<grid_for(nnz, kT, cap), kT, 0, s>>>(nnz, csc_w, cnt);
+    ctx->launches += 2;
+  }
+  SS_CK(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s), "pp_sssp: read flags");
+  SS_CK(cudaStreamSynchronize(s), "pp_sssp: init");
+  if (h[1]) {
+    set_error("pp_sssp: negative or NaN edge weight (SPEC S:342)");
+    st = PP_ERR_GRAPH;
+    goto out;
+  }
+  while (nf > 0) {
+    if (dir == 0 && (double)nf / (double)n > alpha) {  // the one switch (R29)
+      dir = 1;
+      sw = it;
+    }
+    SS_CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned), s), "pp_sssp: reset counter");
+    if (dir == 0) {
+      k_sssp_push<<<grid_for(nf, kT / 32, cap), kT, 0, s>>>(la, nf, csr_off, csr_idx, csr_w, dist, t, lb, cnt);
+      push_it++;
+    } else {
+      k_sssp_pull<<<cap, kT, 0, s>>>(n, csc_off, csc_idx, csc_w, dist, t, lb, cnt);
+      pull_it++;
+    }
+    k_sssp_commit<<<cap, kT, 0, s>>>(lb, cnt, t, dist);
+    ctx->launches += 2;
+    SS_CK(cudaGetLastError(), "pp_sssp: launch");
+    SS_CK(cudaMemcpyAsync(h, cnt, sizeof(unsigned), cudaMemcpyDeviceToHost, s), "pp_sssp: read count");
+    SS_CK(cudaStreamSynchronize(s), "pp_sssp: step");
+    nf = h[0];
+    uint32_t* tmp = la;
+    la = lb;
+    lb = tmp;
+    it++;
+  }
+  if (stats) {
+    stats->iterations = it;
+    stats->push_iterations = push_it;
+    stats->pull_iterations = pull_it;
+    stats->switch_iteration = sw;
+  }
+out:
+  if (t) cudaFreeAsync(t, s);
+  if (la) cudaFreeAsync(la, s);
+  if (lb) cudaFreeAsync(lb, s);
+  if (cnt) cudaFreeAsync(cnt, s);
+  return st;
+}
