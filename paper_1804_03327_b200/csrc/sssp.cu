@@ -32,6 +32,9 @@ __global__ void k_sssp_init(int64_t n, int64_t s, float* __restrict__ d, float* 
     list[0] = (uint32_t)s;
     cnt[0] = 0;  // next-frontier length
     cnt[1] = 0;  // error flag (negative / NaN weight)
+    cnt[2] = 0;  // heavy active vertices of the step (push)
+    cnt[3] = 0;  // heavy rows of A^T (pull), counted once
+    cnt[4] = 0;  // their chunk descriptors
   }
 }
 
@@ -42,46 +45,138 @@ __global__ void k_sssp_check(int64_t nnz, const float* __restrict__ w, unsigned*
     if (!(w[e] >= 0.f)) cnt[1] = 1;
 }
 
-// Column-based step (push, Alg. 3 shape P:370): one warp per active vertex u scatters
-// d(u) + A(u, v) into t(v).  The thread whose atomicMin moves t(v) off d(v) appends v.
+constexpr int kG = 8;                   // lanes per light vertex / row (a warp holds 4 groups)
+constexpr int64_t kHeavyDeg = 256;      // longer rows / out-lists: one CTA each
+
+__device__ __forceinline__ unsigned group_mask() {
+  return ((1u << kG) - 1u) << ((threadIdx.x & 31) & ~(kG - 1));
+}
+
+// t(v) <- min(t(v), nd); the thread whose atomicMin moves t(v) off d(v) appends v.
+__device__ __forceinline__ void relax(uint32_t v, float nd, const float* __restrict__ d, float* t,
+                                      uint32_t* __restrict__ next, unsigned* __restrict__ cnt) {
+  if (nd < t[v]) {
+    const int old = atomicMin(reinterpret_cast<int*>(t) + v, __float_as_int(nd));
+    if (__float_as_int(nd) < old && old == __float_as_int(d[v])) next[atomicAdd(cnt, 1u)] = v;
+  }
+}
+
+constexpr int64_t kChunk = 2048;        // heavy rows / out-lists are cut into chunks of this
+                                        // many edges, one warp each (no serial hub tail)
+
+// Column-based step (push, Alg. 3 shape P:370): a kG-lane group per active vertex u scatters
+// d(u) + A(u, v) into t(v); a vertex with more than kHeavyDeg out-edges is cut into kChunk-edge
+// chunk descriptors {u, chunk} for k_sssp_push_heavy.
 __global__ void k_sssp_push(const uint32_t* __restrict__ f, unsigned nf, const int64_t* __restrict__ off,
                             const uint32_t* __restrict__ idx, const float* __restrict__ w,
                             const float* __restrict__ d, float* __restrict__ t,
-                            uint32_t* __restrict__ next, unsigned* __restrict__ cnt) {
+                            uint32_t* __restrict__ next, unsigned* __restrict__ cnt,
+                            uint2* __restrict__ chunks) {
+  const unsigned lane = threadIdx.x & (kG - 1);
+  const unsigned gpb = blockDim.x / kG;
+  for (unsigned k = blockIdx.x * gpb + threadIdx.x / kG; k < nf; k += gridDim.x * gpb) {
+    const uint32_t u = f[k];
+    const int64_t b = off[u], e = off[u + 1];
+    if (e - b > kHeavyDeg) {
+      const unsigned nch = (unsigned)((e - b + kChunk - 1) / kChunk);
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(cnt + 2, nch);
+      base = __shfl_sync(group_mask(), base, 0, kG);
+      for (unsigned c = lane; c < nch; c += kG) chunks[base + c] = make_uint2(u, c);
+      continue;
+    }
+    const float du = d[u];
+    for (int64_t j = b + lane; j < e; j += kG) relax(__ldg(idx + j), du + __ldg(w + j), d, t, next, cnt);
+  }
+}
+
+// Heavy out-lists of this step: one warp per kChunk-edge chunk.
+__global__ void k_sssp_push_heavy(const uint2* __restrict__ chunks, const int64_t* __restrict__ off,
+                                  const uint32_t* __restrict__ idx, const float* __restrict__ w,
+                                  const float* __restrict__ d, float* __restrict__ t,
+                                  uint32_t* __restrict__ next, unsigned* __restrict__ cnt) {
+  const unsigned nc = cnt[2];
   const unsigned lane = threadIdx.x & 31;
   const unsigned nw = gridDim.x * (blockDim.x >> 5);
-  for (unsigned k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < nf; k += nw) {
-    const uint32_t u = f[k];
-    const float du = d[u];
-    const int64_t b = off[u], e = off[u + 1];
-    for (int64_t j = b + lane; j < e; j += 32) {
-      const uint32_t v = __ldg(idx + j);
-      const float nd = du + __ldg(w + j);
-      if (nd < t[v]) {
-        const int old = atomicMin(reinterpret_cast<int*>(t) + v, __float_as_int(nd));
-        if (__float_as_int(nd) < old && old == __float_as_int(d[v]))
-          next[atomicAdd(cnt, 1u)] = v;
-      }
+  for (unsigned k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < nc; k += nw) {
+    const uint2 c = chunks[k];
+    const float du = d[c.x];
+    const int64_t b = off[c.x] + (int64_t)c.y * kChunk;
+    const int64_t e = min(off[c.x + 1], b + kChunk);
+    for (int64_t j = b + lane; j < e; j += 32) relax(__ldg(idx + j), du + __ldg(w + j), d, t, next, cnt);
+  }
+}
+
+// Row-based step (pull, Alg. 2 shape P:320 without mask / early exit): a kG-lane group per
+// row j of A^T reduces min_i d(i) + A(i, j) over the in-edges (operand reuse: all of d).
+// Rows longer than kHeavyDeg are left to k_sssp_pull_heavy / k_sssp_pull_finish.
+__global__ void k_sssp_pull(int64_t n, const int64_t* __restrict__ coff, const uint32_t* __restrict__ cidx,
+                            const float* __restrict__ cw, const float* __restrict__ d,
+                            float* __restrict__ t, uint32_t* __restrict__ next, unsigned* __restrict__ cnt) {
+  const unsigned lane = threadIdx.x & (kG - 1);
+  const unsigned gm = group_mask();
+  const int64_t gpb = blockDim.x / kG;
+  for (int64_t j = blockIdx.x * gpb + threadIdx.x / kG; j < n; j += (int64_t)gridDim.x * gpb) {
+    const int64_t b = coff[j], e = coff[j + 1];
+    if (e - b > kHeavyDeg) continue;
+    float m = __int_as_float(kInfBits);
+    for (int64_t q = b + lane; q < e; q += kG) m = fminf(m, d[__ldg(cidx + q)] + __ldg(cw + q));
+#pragma unroll
+    for (int o = kG / 2; o; o >>= 1) m = fminf(m, __shfl_xor_sync(gm, m, o));
+    if (lane == 0 && m < d[j]) {
+      t[j] = m;
+      next[atomicAdd(cnt, 1u)] = (uint32_t)j;
     }
   }
 }
 
-// Row-based step (pull, Alg. 2 shape P:320 without mask / early exit): one warp per row j
-// of A^T reduces min_i d(i) + A(i, j) over the in-edges (operand reuse: all of d).
-__global__ void k_sssp_pull(int64_t n, const int64_t* __restrict__ coff, const uint32_t* __restrict__ cidx,
-                            const float* __restrict__ cw, const float* __restrict__ d,
-                            float* __restrict__ t, uint32_t* __restrict__ next, unsigned* __restrict__ cnt) {
+// Heavy rows: one warp per kChunk-edge chunk (descriptors built once per call), partial min
+// folded into cand(j) with atomicMin on the fp32 bits.
+__global__ void k_sssp_pull_heavy(const uint2* __restrict__ chunks, unsigned nc,
+                                  const int64_t* __restrict__ coff, const uint32_t* __restrict__ cidx,
+                                  const float* __restrict__ cw, const float* __restrict__ d,
+                                  float* __restrict__ cand) {
   const unsigned lane = threadIdx.x & 31;
-  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t j = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); j < n; j += nw) {
-    const int64_t b = coff[j], e = coff[j + 1];
+  const unsigned nw = gridDim.x * (blockDim.x >> 5);
+  for (unsigned k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < nc; k += nw) {
+    const uint2 c = chunks[k];
+    const int64_t b = coff[c.x] + (int64_t)c.y * kChunk;
+    const int64_t e = min(coff[c.x + 1], b + kChunk);
     float m = __int_as_float(kInfBits);
     for (int64_t q = b + lane; q < e; q += 32) m = fminf(m, d[__ldg(cidx + q)] + __ldg(cw + q));
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0 && m < d[j]) {
+    if (lane == 0 && m < cand[c.x]) atomicMin(reinterpret_cast<int*>(cand) + c.x, __float_as_int(m));
+  }
+}
+
+// Heavy rows: t(j) = cand(j) where it improves d(j); cand reset to +inf for the next step.
+__global__ void k_sssp_pull_finish(const uint32_t* __restrict__ hrows, unsigned nh, const float* __restrict__ d,
+                                   float* __restrict__ t, float* __restrict__ cand,
+                                   uint32_t* __restrict__ next, unsigned* __restrict__ cnt) {
+  for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < nh; k += gridDim.x * blockDim.x) {
+    const uint32_t j = hrows[k];
+    const float m = cand[j];
+    cand[j] = __int_as_float(kInfBits);
+    if (m < d[j]) {
       t[j] = m;
-      next[atomicAdd(cnt, 1u)] = (uint32_t)j;
+      next[atomicAdd(cnt, 1u)] = j;
+    }
+  }
+}
+
+// Once per call: list the heavy rows of A^T and cut them into chunk descriptors.
+__global__ void k_sssp_heavy_rows(int64_t n, const int64_t* __restrict__ coff, uint32_t* __restrict__ hrows,
+                                  uint2* __restrict__ chunks, float* __restrict__ cand,
+                                  unsigned* __restrict__ cnt) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    cand[j] = __int_as_float(kInfBits);
+    const int64_t deg = coff[j + 1] - coff[j];
+    if (deg > kHeavyDeg) {
+      hrows[atomicAdd(cnt + 3, 1u)] = (uint32_t)j;
+      const unsigned nch = (unsigned)((deg + kChunk - 1) / kChunk);
+      const unsigned base = atomicAdd(cnt + 4, nch);
+      for (unsigned c = 0; c < nch; ++c) chunks[base + c] = make_uint2((uint32_t)j, c);
     }
   }
 }
@@ -136,16 +231,31 @@ extern "C" pp_status pp_sssp(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* 
   const int cap = ctx->num_sms * 8;
   float* t = nullptr;
   uint32_t *la = nullptr, *lb = nullptr;
+  uint32_t* hrows = nullptr;
+  uint2 *pch = nullptr, *hch = nullptr;  // push / pull chunk descriptors
+  float* cand = nullptr;
+  const int64_t nch_max = nnz / kHeavyDeg + 1;  // ceil(deg/kChunk) <= deg/kHeavyDeg for heavy rows
   unsigned* cnt = nullptr;
-  unsigned h[2] = {0, 0};
+  unsigned h[5] = {0, 0, 0, 0, 0};
   int64_t it = 0, push_it = 0, pull_it = 0, sw = -1;
   int dir = 0;  // 0 push, 1 pull
   unsigned nf = 1;
   SS_CK(cudaSetDevice(ctx->device), "pp_sssp: cudaSetDevice");
+  {  // keep the stream-ordered workspace mapped across calls: with the default release
+     // threshold (0) every per-iteration stream sync would unmap it and the next call remap it
+    cudaMemPool_t pool;
+    uint64_t keep = UINT64_MAX;
+    SS_CK(cudaDeviceGetDefaultMemPool(&pool, ctx->device), "pp_sssp: default mem pool");
+    SS_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep), "pp_sssp: pool threshold");
+  }
   SS_CK(cudaMallocAsync((void**)&t, sizeof(float) * n, s), "pp_sssp: alloc t");
   SS_CK(cudaMallocAsync((void**)&la, sizeof(uint32_t) * n, s), "pp_sssp: alloc list");
   SS_CK(cudaMallocAsync((void**)&lb, sizeof(uint32_t) * n, s), "pp_sssp: alloc list");
-  SS_CK(cudaMallocAsync((void**)&cnt, sizeof(unsigned) * 2, s), "pp_sssp: alloc counters");
+  SS_CK(cudaMallocAsync((void**)&hrows, sizeof(uint32_t) * n, s), "pp_sssp: alloc heavy rows");
+  SS_CK(cudaMallocAsync((void**)&cand, sizeof(float) * n, s), "pp_sssp: alloc candidates");
+  SS_CK(cudaMallocAsync((void**)&pch, sizeof(uint2) * nch_max, s), "pp_sssp: alloc chunks");
+  SS_CK(cudaMallocAsync((void**)&hch, sizeof(uint2) * nch_max, s), "pp_sssp: alloc chunks");
+  SS_CK(cudaMallocAsync((void**)&cnt, sizeof(unsigned) * 5, s), "pp_sssp: alloc counters");
   k_sssp_init<<<grid_for(n, kT, cap), kT, 0, s>>>(n, source, dist, t, la, cnt);
   ctx->launches++;
   if (nnz > 0) {
@@ -153,6 +263,8 @@ extern "C" pp_status pp_sssp(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* 
     k_sssp_check<<<grid_for(nnz, kT, cap), kT, 0, s>>>(nnz, csc_w, cnt);
     ctx->launches += 2;
   }
+  k_sssp_heavy_rows<<<grid_for(n, kT, cap), kT, 0, s>>>(n, csc_off, hrows, hch, cand, cnt);
+  ctx->launches++;
   SS_CK(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s), "pp_sssp: read flags");
   SS_CK(cudaStreamSynchronize(s), "pp_sssp: init");
   if (h[1]) {
@@ -165,16 +277,22 @@ extern "C" pp_status pp_sssp(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* 
       dir = 1;
       sw = it;
     }
-    SS_CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned), s), "pp_sssp: reset counter");
+    SS_CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * 3, s), "pp_sssp: reset counters");
     if (dir == 0) {
-      k_sssp_push<<<grid_for(nf, kT / 32, cap), kT, 0, s>>>(la, nf, csr_off, csr_idx, csr_w, dist, t, lb, cnt);
+      k_sssp_push<<<grid_for(nf, kT / kG, cap), kT, 0, s>>>(la, nf, csr_off, csr_idx, csr_w, dist, t, lb, cnt, pch);
+      k_sssp_push_heavy<<<cap, kT, 0, s>>>(pch, csr_off, csr_idx, csr_w, dist, t, lb, cnt);
       push_it++;
     } else {
       k_sssp_pull<<<cap, kT, 0, s>>>(n, csc_off, csc_idx, csc_w, dist, t, lb, cnt);
+      if (h[3]) {
+        k_sssp_pull_heavy<<<cap, kT, 0, s>>>(hch, h[4], csc_off, csc_idx, csc_w, dist, cand);
+        k_sssp_pull_finish<<<grid_for(h[3], kT, cap), kT, 0, s>>>(hrows, h[3], dist, t, cand, lb, cnt);
+        ctx->launches += 2;
+      }
       pull_it++;
     }
     k_sssp_commit<<<cap, kT, 0, s>>>(lb, cnt, t, dist);
-    ctx->launches += 2;
+    ctx->launches += 3;
     SS_CK(cudaGetLastError(), "pp_sssp: launch");
     SS_CK(cudaMemcpyAsync(h, cnt, sizeof(unsigned), cudaMemcpyDeviceToHost, s), "pp_sssp: read count");
     SS_CK(cudaStreamSynchronize(s), "pp_sssp: step");
@@ -194,6 +312,10 @@ out:
   if (t) cudaFreeAsync(t, s);
   if (la) cudaFreeAsync(la, s);
   if (lb) cudaFreeAsync(lb, s);
+  if (hrows) cudaFreeAsync(hrows, s);
+  if (cand) cudaFreeAsync(cand, s);
+  if (pch) cudaFreeAsync(pch, s);
+  if (hch) cudaFreeAsync(hch, s);
   if (cnt) cudaFreeAsync(cnt, s);
   return st;
 }
