@@ -45,7 +45,10 @@ __global__ void k_sssp_check(int64_t nnz, const float* __restrict__ w, unsigned*
     if (!(w[e] >= 0.f)) cnt[1] = 1;
 }
 
-constexpr int kG = 8;                   // lanes per light vertex / row (a warp holds 4 groups)
+#ifndef PP_SSSP_G
+#define PP_SSSP_G 4
+#endif
+constexpr int kG = PP_SSSP_G;           // lanes per light vertex / row (32/kG groups per warp)
 constexpr int64_t kHeavyDeg = 256;      // longer rows / out-lists: one CTA each
 
 __device__ __forceinline__ unsigned group_mask() {
@@ -143,7 +146,14 @@ __global__ void k_sssp_pull_heavy(const uint2* __restrict__ chunks, unsigned nc,
     const int64_t b = coff[c.x] + (int64_t)c.y * kChunk;
     const int64_t e = min(coff[c.x + 1], b + kChunk);
     float m = __int_as_float(kInfBits);
-    for (int64_t q = b + lane; q < e; q += 32) m = fminf(m, d[__ldg(cidx + q)] + __ldg(cw + q));
+    int64_t q = b + lane;
+    for (; q + 96 < e; q += 128) {  // 4 independent gathers in flight per lane
+      uint32_t i0 = __ldg(cidx + q), i1 = __ldg(cidx + q + 32), i2 = __ldg(cidx + q + 64),
+               i3 = __ldg(cidx + q + 96);
+      float w0 = __ldg(cw + q), w1 = __ldg(cw + q + 32), w2 = __ldg(cw + q + 64), w3 = __ldg(cw + q + 96);
+      m = fminf(fminf(m, fminf(d[i0] + w0, d[i1] + w1)), fminf(d[i2] + w2, d[i3] + w3));
+    }
+    for (; q < e; q += 32) m = fminf(m, d[__ldg(cidx + q)] + __ldg(cw + q));
 #pragma unroll
     for (int o = 16; o; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (lane == 0 && m < cand[c.x]) atomicMin(reinterpret_cast<int*>(cand) + c.x, __float_as_int(m));
