@@ -26,7 +26,7 @@ def build(force=False, verbose=False):
     if not force and not needs_build():
         return SO
     tmp = SO + f".tmp{os.getpid()}"
-    extra = [f"-D{k}={os.environ[k]}" for k in ("PP_BFS_BLOCK", "PP_SUM_WORDS", "PP_PULL_WORDS", "PP_PULL_KC", "PP_SOLO_EDGES", "PP_LOWLAT_EDGES", "PP_NARROW_MAX_EDGES", "PP_NARROW_MAX_DEG", "PP_VREC", "PP_INIT_VEC", "PP_STREAM_U", "PP_SSSP_G") if os.environ.get(k)]
+    extra = [f"-D{k}={os.environ[k]}" for k in ("PP_BFS_BLOCK", "PP_SUM_WORDS", "PP_PULL_WORDS", "PP_PULL_KC", "PP_SOLO_EDGES", "PP_LOWLAT_EDGES", "PP_NARROW_MAX_EDGES", "PP_NARROW_MAX_DEG", "PP_VREC", "PP_INIT_VEC", "PP_STREAM_U", "PP_SSSP_G", "PP_SSSP_HEAVY") if os.environ.get(k)]
     extra += ["-DPP_IDX_NOALLOC"] if os.environ.get("PP_IDX_NOALLOC") else []
     extra += ["-ldl"]
     cmd = [NVCC] + FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + \

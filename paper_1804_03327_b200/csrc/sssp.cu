@@ -49,7 +49,10 @@ __global__ void k_sssp_check(int64_t nnz, const float* __restrict__ w, unsigned*
 #define PP_SSSP_G 4
 #endif
 constexpr int kG = PP_SSSP_G;           // lanes per light vertex / row (32/kG groups per warp)
-constexpr int64_t kHeavyDeg = 256;      // longer rows / out-lists: one CTA each
+#ifndef PP_SSSP_HEAVY
+#define PP_SSSP_HEAVY 256
+#endif
+constexpr int64_t kHeavyDeg = PP_SSSP_HEAVY;  // longer rows / out-lists: kChunk-edge warp chunks
 
 __device__ __forceinline__ unsigned group_mask() {
   return ((1u << kG) - 1u) << ((threadIdx.x & 31) & ~(kG - 1));
