@@ -4,16 +4,18 @@
 One step = one whole BFS (pp_bfs: every level of push / pull / convert / direction
 switch, all in the library's CUDA kernels) from one seeded source over the resident
 synthetic graph of config C2 (RMAT s22 ef16, Graph500 parameters).
-TEPS follows the paper: nnz(A) / BFS time.
+TEPS follows the paper: nnz(A) / BFS time; the Graph500 convention
+(undirected edges of the traversed component / time, harmonic mean) is reported beside it.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
 
-N > 1 (torchrun): one process per GPU.  Default --mode replicas: each rank traverses its
-own sources on its own replica of the graph (independent problems, weak scaling, no
-data-path collective).  --mode partitioned: one BFS at a time over the 1D row partition
-(pp_ctx_create_dist; per-level ncclAllGather of the next-frontier bitmap), strong scaling.
-Timing is the max over ranks.  --impl reference times the CPU oracle
-(queue BFS, 1 core) on the same graph, sources, metric and unit.
+N > 1 (torchrun): one process per GPU.  Default --mode partitioned: ONE BFS at a time over
+the 1D row partition: every rank uploads only its block, and the multi-rank
+kernel exchanges each level's frontier slice and counters by storing into the peers'
+exchange buffers -- strong scaling.  --mode replicas: independent BFS
+traversals per rank (weak scaling, labelled as such).  Timing is the max over ranks.
+--impl reference times the CPU oracle (queue BFS, 1 core) on the same graph, sources,
+metric, unit and config.
 """
 from __future__ import annotations
 
@@ -24,7 +26,6 @@ import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 
 import numpy as np
@@ -37,6 +38,7 @@ import synth  # noqa: E402
 METRIC = "DOBFS GTEPS on RMAT Scale 22 at 1/2/4/8 B200; achieved HBM GB/s fraction"
 UNIT = "GTEPS"
 FLUSH_BYTES = 256 << 20  # > 126 MB L2
+NOMINAL_HBM_GBS = 8000.0  # B200 nominal (DGX figure; SURVEY §8(d) "8 TB/s nominal")
 
 
 def env_rank():
@@ -48,9 +50,34 @@ def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (burst copy)"
+        return float(p["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (burst copy, of measured)"
     except Exception:
-        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md, of fallback)"
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, len(os.sched_getaffinity(0))
+
+
+def workload_config(args, g, world, mode):
+    """The config object both arms print (identical strings -> same_config)."""
+    partitioned = mode == "partitioned" and world > 1
+    return {"workload": f"{args.config}: {g.name} (Graph500 RMAT a,b,c=.57,.19,.19, scrambled, "
+                        f"symmetrised, dedup), n={g.n}, nnz={g.nnz}, one DO-BFS per step from "
+                        f"seeded sources",
+            "heuristic": args.heuristic,
+            "l2": "flushed between steps (256 MiB write, not timed)",
+            "parallelism": (f"1D row partition x{world} (multi-rank kernel, peer-memory exchange)"
+                            if partitioned else f"replicas x{world}")}
 
 
 class ClockSampler:
@@ -106,49 +133,125 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def byte_model(torch, g_dev, depth, dirs, n, nnz, off_bytes, per_level=False):
-    """Algorithmic HBM bytes of one BFS under DESIGN.md §6's model (byte-exact; the
-    visited-bitmap probes are L2-resident and excluded).  Computed from the result
-    (depth vector) and the level directions with torch ops on the graph's CSR."""
-    off, idx, rows, deg, noniso = g_dev
-    O = off_bytes
+# ---- algorithmic bytes (roofline numerator) ---------------------------------
+
+def _sectors_unique(torch, byte_addr):
+    """32-byte sectors touched by a set of scattered 4-byte accesses (byte addresses)."""
+    if byte_addr.numel() == 0:
+        return 0
+    return 32 * int(torch.unique(byte_addr // 32).numel())
+
+
+def _sectors_runs(torch, start_elem, length):
+    """32-byte sectors spanned by runs of 4-byte elements [start, start+len) (len > 0)."""
+    m = length > 0
+    if not bool(m.any()):
+        return 0
+    s, l = start_elem[m], length[m]
+    return 32 * int((((s + l) * 4 + 31) // 32 - (s * 4) // 32).sum())
+
+
+def byte_models(torch, gd, depth, dirs, n, off_bytes, per_level=False):
+    """Algorithmic HBM bytes of one BFS from its result (depth vector, in the ids of the layout
+    the kernel scans) and its direction sequence -- never from kernel self-reports.  Three models:
+      s8d         SURVEY §8(d) byte-exact, as written (a candidate-list pull design):
+                  push 4|F| + O|F| + 4 m_f + 4|F'| + 4|F'|; pull [rebuild n/4 + 4|C| on
+                  push->pull] + 4|C| + O|C| + 4S + 4|F'| + 4|C'| + n/8; after a pull n/4, plus
+                  n/8 + 4|F'| before a push; O = bytes per offset pair; init 4n + n/8 (a2 row)
+      s8d_sector  the same with every scattered access rounded to the 32-byte sectors it touches
+                  (distinct sectors; sorted streams rounded up): the realistic HBM floor
+      design      this design's own traffic (no candidate list: each pull scans the visited
+                  bitmap for zero bits; pushes read 16-byte frontier entries)
+    S = sum over candidates of the ids read = first-hit index + 1, or the degree on a miss."""
+    off, idx, rows, deg, noniso = gd
+    O = 2 * off_bytes
     d = depth.to(torch.int64)
     L = len(dirs)
-    total = 4 * n + 2 * (n // 8)                       # init: depth, visited <- isolated
-    parts = [total]                                      # per_level: [init, level 1, ...]
+    nb8 = n // 8
+    init = 4 * n + nb8
+    tot = {"s8d": init, "s8d_sector": init, "design": 4 * n + 2 * nb8}
+    parts = {k: [v] for k, v in tot.items()}
     cnt = torch.bincount(d, minlength=L + 2)
-    outdeg_sum = torch.zeros(L + 2, dtype=torch.int64, device=d.device).index_add_(0, d, deg)
-    dj = d[idx]                                          # depth of each edge's head
-    for k in range(1, L + 1):                            # level k expands depth-k frontier
-        before = total
+    dj = d[idx]
+    ar = torch.arange(idx.numel(), device=d.device)
+    for k in range(1, L + 1):
+        before = dict(tot)
         F = int(cnt[k])
         Fn = int(cnt[k + 1]) if k + 1 <= L + 1 else 0
-        if dirs[k - 1] == 0:  # push
-            m_in = int(outdeg_sum[k])
-            total += F * (4 + 2 * O) + 4 * m_in + Fn * (4 + 4 + 2 * O)
-        else:                 # pull: candidates unvisited at level start, scan to first hit
+        newf = (d == k + 1)
+        depth_sec = _sectors_unique(torch, 4 * torch.nonzero(newf).flatten())
+        if dirs[k - 1] == 0:  # push: expand F_k
+            fv = torch.nonzero(d == k).flatten()
+            m_in = int(deg[fv].sum())
+            tot["s8d"] += 4 * F + O * F + 4 * m_in + 8 * Fn
+            offs = torch.cat([fv * off_bytes, (fv + 1) * off_bytes])
+            tot["s8d_sector"] += (32 * ((4 * F + 31) // 32) + _sectors_unique(torch, offs) +
+                                  _sectors_runs(torch, off[fv], deg[fv]) + depth_sec +
+                                  32 * ((4 * Fn + 31) // 32))
+            tot["design"] += F * (4 + O) + 4 * m_in + Fn * (4 + 4 + O)
+        else:  # pull: candidates = non-isolated, unvisited at level start; scan to the first hit
             cand = noniso & ((d == 0) | (d > k))
             hit = (dj >= 1) & (dj <= k)
-            pos = torch.arange(nnz, device=d.device) - off[rows]
+            pos = ar - off[rows]
             first = torch.full((n,), torch.iinfo(torch.int64).max, dtype=torch.int64, device=d.device)
             first.scatter_reduce_(0, rows[hit], pos[hit], reduce="amin")
             scanned = torch.where(first < torch.iinfo(torch.int64).max, first + 1, deg)
-            S = int(scanned[cand].sum())
-            C = int(cand.sum())
-            total += 2 * (n // 8) + C * 2 * O + 4 * S + 4 * Fn
-            if k < L and dirs[k] == 0:                 # pull -> push: convert
-                total += 2 * (n // 8) + Fn * (4 + 2 * O)
-        parts.append(total - before)
-    return parts if per_level else total
+            cv = torch.nonzero(cand).flatten()
+            C = int(cv.numel())
+            S = int(scanned[cv].sum())
+            Cs = C - Fn
+            rebuild = (k == 1) or dirs[k - 2] == 0
+            tot["s8d"] += (2 * nb8 + 4 * C) if rebuild else 0  # candidate rebuild n/4 + 4|C|
+            tot["s8d"] += 4 * C + O * C + 4 * S + 4 * Fn + 4 * Cs + nb8 + 2 * nb8
+            offs = torch.cat([cv * off_bytes, (cv + 1) * off_bytes])
+            seq = lambda b: 32 * ((b + 31) // 32)
+            tot["s8d_sector"] += ((seq(2 * nb8) + seq(4 * C) if rebuild else 0) + seq(4 * C) +
+                                  _sectors_unique(torch, offs) +
+                                  _sectors_runs(torch, off[cv], scanned[cv]) + depth_sec +
+                                  seq(4 * Fn) + seq(4 * Cs) + seq(nb8) + seq(2 * nb8))
+            tot["design"] += 2 * nb8 + C * O + 4 * S + 4 * Fn
+            if k < L and dirs[k] == 0:  # pull -> push: bitmap -> list
+                tot["s8d"] += nb8 + 4 * Fn
+                tot["s8d_sector"] += seq(nb8) + seq(4 * Fn)
+                tot["design"] += 2 * nb8 + Fn * (4 + O)
+        for key in tot:
+            parts[key].append(tot[key] - before[key])
+    return parts if per_level else tot
+
+
+def byte_model(torch, g_dev, depth, dirs, n, nnz, off_bytes, per_level=False):
+    """DESIGN.md §6 design model (kept for tools/level_roofline.py)."""
+    r = byte_models(torch, g_dev, depth, dirs, n, off_bytes, per_level)
+    return r["design"]
+
+
+def graph_layout(torch, g, dev, relabel):
+    """CSR in the ids the kernel scans (relabelled: degree order, rows re-sorted)."""
+    n = g.n
+    off_t = torch.from_numpy(g.off).to(dev)
+    idx_t = torch.from_numpy(g.idx.astype(np.int64)).to(dev)
+    deg_t = off_t[1:] - off_t[:-1]
+    rows_t = torch.repeat_interleave(torch.arange(n, device=dev), deg_t)
+    key_t = None
+    if relabel:
+        key_t = torch.from_numpy(synth.degree_order_key(g).astype(np.int64)).to(dev)
+        e = torch.sort(key_t[rows_t] * n + key_t[idx_t]).values
+        rows_t, idx_t = e // n, e % n
+        deg_t = torch.bincount(rows_t, minlength=n)
+        off_t = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+        off_t[1:] = torch.cumsum(deg_t, 0)
+        del e
+    return (off_t, idx_t, rows_t, deg_t, deg_t > 0), key_t
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU oracle (textbook queue BFS, 1 core), same metric."""
+    """--impl reference: the CPU oracle (textbook queue BFS, 1 core), same metric and config."""
     import oracle
     if rank != 0:
         return
     g = synth.make(args.config)
     srcs = synth.sources(g, max(args.steps + args.warmup, 1), seed=2)
+    model, ncores = cpu_info()
     for k in range(args.warmup):
         oracle.bfs(g, srcs[k % len(srcs)])
     times = []
@@ -159,12 +262,14 @@ def run_reference(args, rank, world):
     ms = 1e3 * sum(times) / len(times)
     val = g.nnz / (sum(times) / len(times)) / 1e9
     line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if (args.mode == "partitioned" and world > 1) else "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": f"{args.config}: {g.name}, n={g.n}, nnz={g.nnz}, one BFS per step"},
+            "config": workload_config(args, g, world, args.mode),
             "impl": "reference",
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{args.steps} full queue-BFS traversals of {g.name}"},
+                             "sample": f"{args.steps} full queue-BFS traversals of {g.name} "
+                                       f"(1 thread of {ncores} available: {model})"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -179,9 +284,12 @@ def main():
     ap.add_argument("--heuristic", default="edges", choices=["edges", "paper"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--model-sources", type=int, default=4)
-    ap.add_argument("--mode", default="replicas", choices=["replicas", "partitioned"])
+    ap.add_argument("--mode", default="partitioned", choices=["partitioned", "replicas"],
+                    help="N > 1 only: 1D row partition (default) or independent replicas")
     ap.add_argument("--no-relabel", action="store_true",
                     help="upload without PP_GRAPH_RELABEL (caller vertex order)")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the secondary timings (parents, no-relabel)")
     args = ap.parse_args()
     rank, world, local = env_rank()
     if args.impl == "reference":
@@ -208,50 +316,69 @@ def main():
     relabel = not args.no_relabel and not partitioned
     G = pp.Graph.from_csr(ctx, g, relabel=relabel)
     n, nnz = g.n, g.nnz
-    lo, hi = G.partition() if partitioned else (0, n)
+    lo, hi = G.partition()
     off_bytes = 4 if nnz < 2**32 - 1 else 8
     heur = pp.PP_HEUR_EDGES if args.heuristic == "edges" else pp.PP_HEUR_PAPER_R
     all_src = synth.sources(g, 64, seed=2)
+
     def src(k):  # partitioned: every rank runs the same (collective) BFS
         return int(all_src[((0 if partitioned else rank) * 17 + k) % len(all_src)])
 
     depth = torch.empty(max(hi - lo, 1), dtype=torch.int32, device=dev)
+    parent = torch.empty(max(hi - lo, 1), dtype=torch.int32, device=dev)
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-    for k in range(args.warmup):
-        pp.bfs(G, src(k), depth, heuristic=heur)
-    torch.cuda.synchronize()
+
+    def timed_loop(graph, want_parent=False, clocks=None):
+        for k in range(args.warmup):
+            pp.bfs(graph, src(k), depth, parent if want_parent else None, heuristic=heur)
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(args.steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        if clocks:
+            clocks.start()
+            time.sleep(0.3)
+        l0 = ctx.launches()
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            flush.zero_()
+            ev[k][0].record(stream)
+            pp.bfs(graph, src(args.warmup + k), depth, parent if want_parent else None,
+                   heuristic=heur)
+            ev[k][1].record(stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        launches = ctx.launches() - l0
+        if world > 1:
+            dist.barrier()
+        clk = clocks.stop() if clocks else None
+        step_ms = [a.elapsed_time(b) for a, b in ev]
+        tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        return float(tot.item()), step_ms, launches, wall, clk
 
     # ---- timed region: K BFS steps, L2 flushed between steps (flush not timed) ----
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    clocks = ClockSampler(local)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    time.sleep(0.3)
-    launches0 = ctx.launches()
-    t_wall0 = time.perf_counter()
-    for k in range(args.steps):
-        flush.zero_()
-        ev[k][0].record(stream)
-        pp.bfs(G, src(args.warmup + k), depth, heuristic=heur)
-        ev[k][1].record(stream)
-    torch.cuda.synchronize()
-    t_wall = time.perf_counter() - t_wall0
-    launches = ctx.launches() - launches0
-    if world > 1:
-        dist.barrier()
-    clk = clocks.stop()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    tot_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(tot_ms, op=dist.ReduceOp.MAX)
-    tot_ms = float(tot_ms.item())
+    tot_ms, step_ms, launches, t_wall, clk = timed_loop(G, clocks=ClockSampler(local))
     ms_per_step = tot_ms / args.steps
     units = 1 if partitioned else world  # BFS traversals per step across the job
     value = units * args.steps * nnz / (tot_ms * 1e-3) / 1e9
+
+    # ---- secondary timings (same protocol): with parents, without relabelling ----
+    extras = {}
+    if not args.no_extras:
+        pm, _, _, _, _ = timed_loop(G, want_parent=True)
+        extras["with_parents"] = {"ms_per_step": pm / args.steps,
+                                  "value": units * args.steps * nnz / (pm * 1e-3) / 1e9}
+        if relabel:
+            G2 = pp.Graph.from_csr(ctx, g, relabel=False)
+            nm, _, _, _, _ = timed_loop(G2)
+            extras["no_relabel"] = {"ms_per_step": nm / args.steps,
+                                    "value": units * args.steps * nnz / (nm * 1e-3) / 1e9}
+            G2.close()
 
     # ---- end to end through the public API: host output buffer, D2H inside the call ----
     host_depth = torch.empty(max(hi - lo, 1), dtype=torch.int32).pin_memory().numpy()
@@ -261,6 +388,8 @@ def main():
     for k in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
         pp.bfs(G, src(args.warmup + k), host_depth, heuristic=heur)   # syncs, copies back
         e2e_t.append(time.perf_counter() - t0)
@@ -269,39 +398,28 @@ def main():
         dist.all_reduce(e2e_tot, op=dist.ReduceOp.MAX)
     e2e_val = units * args.steps * nnz / float(e2e_tot.item()) / 1e9
 
-    line = None
     if rank == 0:
         peak, peak_src = measured_peaks()
-        nmod = 0 if partitioned else min(args.model_sources, args.steps)
-        mb, mt = 0, 0.0
-        if nmod:
-            # ---- roofline of the dominant (only) kernel: bfs_persistent ----
-            off_t = torch.from_numpy(g.off).to(dev)
-            idx_t = torch.from_numpy(g.idx.astype(np.int64)).to(dev)
-            deg_t = off_t[1:] - off_t[:-1]
-            rows_t = torch.repeat_interleave(torch.arange(n, device=dev), deg_t)
-            key_t = None
-            if relabel:  # the layout the kernel scans: internal ids, rows in that order
-                key_t = torch.from_numpy(synth.degree_order_key(g).astype(np.int64)).to(dev)
-                e = torch.sort(key_t[rows_t] * n + key_t[idx_t]).values
-                rows_t, idx_t = e // n, e % n
-                deg_t = torch.bincount(rows_t, minlength=n)
-                off_t = torch.zeros(n + 1, dtype=torch.int64, device=dev)
-                off_t[1:] = torch.cumsum(deg_t, 0)
-                del e
-            noniso = deg_t > 0
-            gd = (off_t, idx_t, rows_t, deg_t, noniso)
-            for k in range(nmod):
-                s = src(args.warmup + k)
-                st = pp.bfs(G, s, depth, heuristic=heur, stats_capacity=4096)
-                dm = depth
-                if key_t is not None:
-                    dm = torch.empty_like(depth)
-                    dm[key_t] = depth
-                mb += byte_model(torch, gd, dm, list(st["dir"]), n, nnz, off_bytes)
+        nmod = min(args.model_sources, args.steps)
+        models = {"s8d": 0, "s8d_sector": 0, "design": 0}
+        mt = 0.0
+        g500 = []
+        gd, key_t = graph_layout(torch, g, dev, relabel)
+        for k in range(0 if partitioned else args.steps):  # rank 0 holds only its slice then
+            s = src(args.warmup + k)
+            st = pp.bfs(G, s, depth, heuristic=heur, stats_capacity=4096)
+            dm = depth
+            if key_t is not None:
+                dm = torch.empty_like(depth)
+                dm[key_t] = depth
+            comp_edges = int(gd[3][dm > 0].sum()) // 2  # undirected edges of the component
+            g500.append(comp_edges / (step_ms[k] * 1e-3) / 1e9)
+            if k < nmod:
+                r = byte_models(torch, gd, dm, list(st["dir"]), n, off_bytes)
+                for key in models:
+                    models[key] += r[key]
                 mt += step_ms[k] * 1e-3
-            del off_t, idx_t, rows_t, deg_t, noniso, gd
-        achieved = mb / mt / 1e9 if mt > 0 else None
+        ach = {key: (v / mt / 1e9 if mt > 0 else None) for key, v in models.items()}
         traffic = None
         prof = os.path.join(ROOT, "profiles", f"ncu_{args.config}.json")
         if os.path.exists(prof) and not partitioned:
@@ -313,6 +431,7 @@ def main():
         cpu = None
         if not args.no_cpu_baseline and not partitioned:
             import oracle
+            model, ncores = cpu_info()
             os.sched_setaffinity(0, {sorted(os.sched_getaffinity(0))[0]})
             ts, k = [], 0
             t_start = time.perf_counter()
@@ -323,28 +442,34 @@ def main():
                 k += 1
             cpu = {"value": nnz / (sum(ts) / len(ts)) / 1e9, "unit": UNIT, "cores": 1,
                    "kind": "oracle",
-                   "sample": f"{len(ts)} full queue-BFS traversals of {g.name} (1 thread; "
-                             f"host has {os.cpu_count()} cores)"}
+                   "sample": f"{len(ts)} full queue-BFS traversals of {g.name} (1 thread of "
+                             f"{ncores} available: {model})"}
+        a8 = ach["s8d"]
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if partitioned else "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic",
-            "config": {"workload": f"{args.config}: {g.name} (Graph500 RMAT a,b,c=.57,.19,.19, "
-                                   f"scrambled, symmetrised, dedup), n={n}, nnz={nnz}, one DO-BFS "
-                                   f"per step from seeded sources",
-                       "heuristic": args.heuristic, "relabel": relabel,
-                       "l2": "flushed between steps (256 MiB write, "
-                       "not timed)",
-                       "parallelism": (f"1D row partition x{world} (NCCL allgather per level)"
-                                       if partitioned else f"replicas x{world}")},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak if achieved else None, "traffic": traffic,
-                         "kernel": ("k_dist_push/k_dist_pull + ncclAllGather per level" if partitioned
+            "config": dict(workload_config(args, g, world, args.mode), relabel=relabel),
+            "roofline": {"bound": "hbm", "achieved": a8, "peak": peak * (world if partitioned else 1),
+                         "unit": "GB/s",
+                         "frac": a8 / (peak * (world if partitioned else 1)) if a8 else None,
+                         "traffic": traffic,
+                         "kernel": ("bfs_ranks (multi-rank: one cooperative launch per rank, "
+                                    "peer-memory exchange)" if partitioned
                                     else "bfs_persistent (whole BFS in one cooperative launch)"),
                          "peak_source": peak_src,
-                         "model": f"byte-exact DESIGN.md §6 over {nmod} sources: "
-                                  f"{mb / max(1, nmod) / 1e6:.1f} MB/BFS"},
+                         "model": f"SURVEY §8(d) byte-exact over {nmod} timed sources: "
+                                  f"{models['s8d'] / max(1, nmod) / 1e6:.1f} MB/BFS",
+                         "frac_sector_floor": (ach["s8d_sector"] / peak) if ach["s8d_sector"] else None,
+                         "sector_floor_MB_per_bfs": models["s8d_sector"] / max(1, nmod) / 1e6,
+                         "frac_design_model": (ach["design"] / peak) if ach["design"] else None,
+                         "design_model_MB_per_bfs": models["design"] / max(1, nmod) / 1e6,
+                         "frac_of_nominal_8TBs": (a8 / NOMINAL_HBM_GBS) if a8 else None},
+            "teps_graph500": ({"value": len(g500) / sum(1.0 / x for x in g500), "unit": UNIT,
+                               "convention": "undirected edges in the traversed component / BFS "
+                                             "time, harmonic mean over the timed sources"}
+                              if g500 else None),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": 8,
                     "d2h_bytes_per_step": 4 * (hi - lo),
@@ -355,6 +480,7 @@ def main():
             "step_ms": {"min": min(step_ms), "median": statistics.median(step_ms),
                         "max": max(step_ms)},
         }
+        line.update(extras)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -84,8 +84,24 @@ pp_status pp_ctx_launch_count(pp_ctx ctx, uint64_t* out);
  * of the lowest id.  Needs nnz, n < 2^31; single-GPU contexts only (else
  * PP_ERR_UNSUPPORTED). */
 #define PP_GRAPH_RELABEL 8u
-pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr_off,
-                          const uint32_t* csr_idx, const int64_t* csc_off,
+/* PP_GRAPH_OFF64: store 64-bit offsets even when nnz < 2^32 (the layout large graphs get;
+ * lets tests exercise it on small graphs).  Results are identical. */
+#define PP_GRAPH_OFF64 16u
+/* Rows [row_lo, row_hi) are the rows this context owns:
+ *  - single-GPU context: row_lo = 0, row_hi = n (else PP_ERR_ARG); offsets have n+1
+ *    entries, nnz = off[n].
+ *  - multi-rank context (pp_ctx_create_dist / pp_team_create, 1D row partition):
+ *    [row_lo, row_hi) must be pp_partition(n, rank, nranks) (else PP_ERR_ARG); csr_off /
+ *    csc_off are the block's row-local offsets (row_hi - row_lo + 1 entries starting at 0),
+ *    ids are GLOBAL vertex ids, nnz = csr_off[row_hi - row_lo].  The library keeps only the
+ *    block: its CSC rows (pull), the push structure (for every vertex u, u's out-neighbours
+ *    inside the block, built on the device from the CSC rows) and the block's out-degrees;
+ *    csr_idx is not used in a multi-rank context (may be NULL unless SYMMETRIC, where the
+ *    CSR rows are the CSC rows).  With pp_ctx_create_dist the call is COLLECTIVE (the ranks
+ *    exchange CUDA IPC handles of their exchange buffers over NCCL); in a team it is not.
+ *    PP_GRAPH_RELABEL is rejected (PP_ERR_UNSUPPORTED). */
+pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t row_lo, int64_t row_hi, int64_t nnz,
+                          const int64_t* csr_off, const uint32_t* csr_idx, const int64_t* csc_off,
                           const uint32_t* csc_idx, uint32_t flags, pp_graph* out);
 pp_status pp_graph_free(pp_graph g);
 /* n, nnz, device bytes held by the handle (graph + BFS work buffers). */
@@ -201,24 +217,45 @@ pp_status pp_bfs(pp_graph g, int64_t source, const pp_bfs_options* opts, int32_t
  * out_ns != NULL copies the last BFS's records (levels x *nctas, level-major) to host. */
 pp_status pp_bfs_debug_times(pp_graph g, int32_t levels, int64_t* out_ns, int32_t* nctas);
 
-/* ---- multi-GPU: 1D row partition + per-level NCCL all-gather ----------
- * One process per GPU.  pp_nccl_unique_id: rank 0 creates the 128-byte NCCL id and shares it
- * (e.g. a torch.distributed broadcast); PP_ERR_NCCL if libnccl.so.2 cannot be loaded.
- * pp_ctx_create_dist: context with an NCCL communicator of nranks ranks (collective).
+/* ---- multi-rank BFS: 1D row partition, exchange fused into the level kernel (SURVEY.md 8e,
+ *      NEXT-1; P:516 names distributed GPUs as future work) --------------------------------
+ * Rank p of P owns the vertex block [row_lo, row_hi) = pp_partition(n, p, P) and stores only
+ * that block (see pp_graph_upload).  pp_bfs runs ONE cooperative kernel per rank for the whole
+ * traversal: push levels expand the global frontier into owned targets, pull levels scan the
+ * owned unvisited rows against the replicated visited bitmap; after every level the kernel
+ * itself stores the owned words of the level's frontier bitmap and the rank's counters into
+ * every peer's exchange buffer (peer memory over NVLink / NVSwitch), then one release flag per
+ * peer; every rank then holds the global counters and takes the same push/pull decision
+ * (R10/R11) with no host round trip and no host-issued collective.
+ * One process per GPU: pp_nccl_unique_id (rank 0 creates the 128-byte NCCL id and shares it,
+ * e.g. by a torch.distributed broadcast; PP_ERR_NCCL if libnccl.so.2 cannot be loaded) and
+ * pp_ctx_create_dist (collective; the communicator is the bootstrap of the peer mappings).
  * pp_partition: rank's block [row_lo, row_hi): contiguous, 1024-vertex aligned, blocks of
- * ceil(ceil(n/32)/32/nranks)*1024 vertices (pure function, no GPU).
- * In a dist ctx pp_graph_upload takes the FULL graph on every rank (it stays resident) and
- * adds the rank's push ranges; pp_graph_partition returns the block.  pp_bfs is then
- * collective: every rank passes the same source/options; depth/parent hold the rank's block
- * slice (row_hi - row_lo entries, same conventions); stats are global and identical on all
- * ranks.  Each level: push (global frontier, owned targets) or pull (owned rows), then one
- * in-place ncclAllGather of the next-frontier bitmap slices, then a finish kernel.  Ablation
- * toggles are single-GPU only (PP_ERR_UNSUPPORTED). */
+ * ceil(ceil(n/32)/32/nranks)*1024 vertices (pure function, no GPU); pp_graph_partition
+ * returns a graph's block.  pp_bfs on such a graph is collective: every rank passes the same
+ * source/options; depth/parent hold the block's slice (row_hi - row_lo entries, same
+ * conventions as single-GPU: min-id parents); stats are global and identical on all ranks.
+ * nranks <= 8; ablation toggles and pp_mxv are single-GPU only (PP_ERR_UNSUPPORTED). */
 pp_status pp_nccl_unique_id(void* out128);
 pp_status pp_ctx_create_dist(int device, void* cuda_stream, const void* nccl_unique_id, int rank,
                              int nranks, pp_ctx* out);
 pp_status pp_partition(int64_t n, int32_t rank, int32_t nranks, int64_t* row_lo, int64_t* row_hi);
 pp_status pp_graph_partition(pp_graph g, int64_t* row_lo, int64_t* row_hi);
+
+/* Single-device team: nranks (<= 8) rank contexts on ONE device and stream, ctxs[r] = rank r.
+ * Each rank uploads its block with pp_graph_upload (not collective); pp_bfs_team then runs
+ * the P ranks as P CTA groups of ONE cooperative launch: the same kernel, the same peer stores,
+ * counter records and cross-rank release/acquire flags as the multi-GPU path, with every
+ * peer's exchange buffer on the same device.  It is how the multi-rank path is verified on one
+ * GPU (tests/test_gpu_dist.py), and a way to run the partitioned layout on one GPU.
+ * graphs[r] = rank r's graph (uploaded through ctxs[r]); depth[r] / parent[r] (parent may be
+ * NULL, or entries NULL only together) = device slices of rank r's block; stats (host,
+ * nullable) = the global per-level record (identical on every rank), synchronises.
+ * Errors as pp_bfs; PP_ERR_ARG if the graphs are not ranks 0..nranks-1 of one team. */
+pp_status pp_team_create(int device, void* cuda_stream, int32_t nranks, pp_ctx* ctxs);
+pp_status pp_bfs_team(const pp_graph* graphs, int32_t nranks, int64_t source,
+                      const pp_bfs_options* opts, int32_t* const* depth, int32_t* const* parent,
+                      pp_bfs_stats* stats);
 
 /* ---- SSSP over the min-plus semiring (Sec. 5.6) ------------
  * The paper's "simple 2-phase direction-optimized traversal" for SSSP: Bellman-Ford

@@ -30,7 +30,8 @@ PP_OK, PP_ERR_ARG, PP_ERR_RANGE, PP_ERR_DIM, PP_ERR_GRAPH, PP_ERR_UNSUPPORTED, P
 STATUS_NAMES = {0: "PP_OK", 1: "PP_ERR_ARG", 2: "PP_ERR_RANGE", 3: "PP_ERR_DIM", 4: "PP_ERR_GRAPH",
                 5: "PP_ERR_UNSUPPORTED", 6: "PP_ERR_CUDA", 7: "PP_ERR_NCCL", 8: "PP_ERR_OOM",
                 9: "PP_ERR_TIMEOUT"}
-PP_GRAPH_SYMMETRIC, PP_GRAPH_DEVICE, PP_GRAPH_VALIDATE, PP_GRAPH_RELABEL = 1, 2, 4, 8
+PP_GRAPH_SYMMETRIC, PP_GRAPH_DEVICE, PP_GRAPH_VALIDATE, PP_GRAPH_RELABEL, PP_GRAPH_OFF64 = \
+    1, 2, 4, 8, 16
 PP_VEC_LIST, PP_VEC_BITMAP = 0, 1
 PP_SR_LOR_LAND = 0
 PP_DIR_AUTO, PP_DIR_PUSH, PP_DIR_PULL = 0, 1, 2
@@ -85,7 +86,7 @@ _SIGS = {
     "pp_ctx_create": ([ctypes.c_int, _vp, ctypes.POINTER(_vp)], ctypes.c_int),
     "pp_ctx_destroy": ([_vp], ctypes.c_int),
     "pp_ctx_launch_count": ([_vp, ctypes.POINTER(ctypes.c_uint64)], ctypes.c_int),
-    "pp_graph_upload": ([_vp, _i64, _i64, _vp, _vp, _vp, _vp, _u32, ctypes.POINTER(_vp)],
+    "pp_graph_upload": ([_vp, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _vp, _u32, ctypes.POINTER(_vp)],
                         ctypes.c_int),
     "pp_graph_free": ([_vp], ctypes.c_int),
     "pp_graph_info": ([_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
@@ -103,6 +104,10 @@ _SIGS = {
     "pp_partition": ([_i64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
                      ctypes.c_int),
     "pp_graph_partition": ([_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)], ctypes.c_int),
+    "pp_team_create": ([ctypes.c_int, _vp, ctypes.c_int32, ctypes.POINTER(_vp)], ctypes.c_int),
+    "pp_bfs_team": ([ctypes.POINTER(_vp), ctypes.c_int32, _i64, ctypes.POINTER(pp_bfs_options),
+                     ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(pp_bfs_stats)],
+                    ctypes.c_int),
     "pp_sssp": ([_vp, _i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64, ctypes.c_double, _vp,
                  ctypes.POINTER(pp_sssp_stats)], ctypes.c_int),
 }
@@ -146,10 +151,10 @@ def pp_ctx_launch_count(ctx) -> int:
     return out.value
 
 
-def pp_graph_upload(ctx, n, nnz, csr_off, csr_idx, csc_off, csc_idx, flags):
+def pp_graph_upload(ctx, n, row_lo, row_hi, nnz, csr_off, csr_idx, csc_off, csc_idx, flags):
     out = _vp()
-    _check(_lib.pp_graph_upload(ctx, n, nnz, csr_off, csr_idx, csc_off, csc_idx, flags,
-                                ctypes.byref(out)))
+    _check(_lib.pp_graph_upload(ctx, n, row_lo, row_hi, nnz, csr_off, csr_idx, csc_off, csc_idx,
+                                flags, ctypes.byref(out)))
     return out.value
 
 
@@ -222,6 +227,21 @@ def pp_graph_partition(g):
     return lo.value, hi.value
 
 
+def pp_team_create(device: int, cuda_stream: int, nranks: int):
+    arr = (_vp * nranks)()
+    _check(_lib.pp_team_create(device, cuda_stream, nranks, arr))
+    return [arr[r] for r in range(nranks)]
+
+
+def pp_bfs_team(graphs, source, opts, depth_ptrs, parent_ptrs, stats):
+    P = len(graphs)
+    ga = (_vp * P)(*graphs)
+    da = (_vp * P)(*depth_ptrs)
+    pa = None if parent_ptrs is None else (_vp * P)(*parent_ptrs)
+    _check(_lib.pp_bfs_team(ga, P, int(source), None if opts is None else ctypes.byref(opts), da, pa,
+                            None if stats is None else ctypes.byref(stats)))
+
+
 # ---- conveniences (torch tensors as device memory) ----------------------------------------
 
 def _ptr(x):
@@ -275,19 +295,102 @@ class DistContext(Context):
         self.handle = pp_ctx_create_dist(device, stream.cuda_stream, nccl_id, rank, nranks)
 
 
+def block_rows(off, idx, lo, hi):
+    """Rows [lo, hi) of a CSR as (row-local int64 offsets, ids) — the block a rank of the 1D
+    row partition uploads (host arrays; no method arithmetic)."""
+    off = np.asarray(off, dtype=np.int64)
+    b, e = int(off[lo]), int(off[hi])
+    return np.ascontiguousarray(off[lo:hi + 1] - b), np.ascontiguousarray(np.asarray(idx)[b:e],
+                                                                        dtype=np.uint32)
+
+
+class _RankCtx:
+    """One rank context of a Team (handle + rank/nranks for Graph's block upload)."""
+
+    def __init__(self, handle, rank, nranks, device, stream):
+        self.handle, self.rank, self.nranks = handle, rank, nranks
+        self.device, self.stream = device, stream
+
+    def launches(self) -> int:
+        return pp_ctx_launch_count(self.handle)
+
+
+class Team:
+    """Single-device team of `nranks` rank contexts (pp_team_create): the multi-rank engine's
+    ranks run as CTA groups of one cooperative launch on one GPU (pp_bfs_team)."""
+
+    def __init__(self, nranks: int, device: int = 0, stream=None):
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.device, self.stream, self.nranks = device, stream, nranks
+        hs = pp_team_create(device, stream.cuda_stream, nranks)
+        self.ctxs = [_RankCtx(h, r, nranks, device, stream) for r, h in enumerate(hs)]
+
+    def upload(self, csr, csc=None, validate=False, off64=False):
+        """Every rank uploads its block of the graph; returns the per-rank Graph list."""
+        return [Graph.from_csr(c, csr, csc, validate=validate, off64=off64) for c in self.ctxs]
+
+    def launches(self) -> int:
+        return sum(c.launches() for c in self.ctxs)
+
+    def close(self):
+        for c in self.ctxs:
+            if c.handle:
+                pp_ctx_destroy(c.handle)
+                c.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def bfs_team(graphs, source: int, depths, parents=None, heuristic=PP_HEUR_EDGES, mode=PP_MODE_DO,
+             alpha=0.0, beta=0.0, stats_capacity=0):
+    """pp_bfs_team over a Team's per-rank graphs; depths/parents: per-rank device slices."""
+    o = pp_bfs_options(heuristic, mode, alpha, beta, 1 if parents is not None else 0, 0)
+    st, arrays = _stats(stats_capacity)
+    pp_bfs_team([g.handle for g in graphs], source, o, [_ptr(d) for d in depths],
+                None if parents is None else [_ptr(p) for p in parents], st)
+    return _stats_dict(st, arrays, stats_capacity)
+
+
 class Graph:
-    """Device-resident graph (library-owned copy of CSR + CSC)."""
+    """Device-resident graph (library-owned copy of CSR + CSC).  On a multi-rank context
+    (DistContext / Team member) off/idx/coff/cidx are the FULL host CSR / CSC and only the
+    rank's block [row_lo, row_hi) = pp_partition(n, rank, nranks) is uploaded."""
 
     def __init__(self, ctx: Context, n, off, idx, coff=None, cidx=None, symmetric=None,
-                 validate=False, device_ptrs=False, relabel=False):
+                 validate=False, device_ptrs=False, relabel=False, off64=False):
         self.ctx = ctx
         self.n = int(n)
-        nnz = int(off[-1]) if not device_ptrs else int(idx.numel())
         if symmetric is None:
             symmetric = coff is None
         flags = (PP_GRAPH_SYMMETRIC if symmetric else 0) | (PP_GRAPH_VALIDATE if validate else 0) | \
             (PP_GRAPH_RELABEL if relabel else 0) | \
-            (PP_GRAPH_DEVICE if device_ptrs else 0)
+            (PP_GRAPH_DEVICE if device_ptrs else 0) | (PP_GRAPH_OFF64 if off64 else 0)
+        self.relabel = bool(relabel)
+        nranks = getattr(ctx, "nranks", 0)
+        if nranks:
+            assert not device_ptrs, "multi-rank upload takes host arrays"
+            lo, hi = pp_partition(self.n, ctx.rank, nranks)
+            boff, bidx = block_rows(off, idx, lo, hi)
+            if symmetric:
+                cboff, cbidx = None, None
+            else:
+                cboff, cbidx = block_rows(coff, cidx, lo, hi)
+            self.nnz = int(boff[-1])
+            self._keep = (boff, bidx, cboff, cbidx)
+            self.handle = pp_graph_upload(ctx.handle, self.n, lo, hi, self.nnz, _ptr(boff),
+                                          _ptr(bidx) if len(bidx) else None,
+                                          None if cboff is None else _ptr(cboff),
+                                          None if cbidx is None or not len(cbidx) else _ptr(cbidx),
+                                          flags)
+            self._keep = None
+            return
+        nnz = int(off[-1]) if not device_ptrs else int(idx.numel())
         if not device_ptrs:
             off = np.ascontiguousarray(off, dtype=np.int64)
             idx = np.ascontiguousarray(idx, dtype=np.uint32)
@@ -295,20 +398,19 @@ class Graph:
                 coff = np.ascontiguousarray(coff, dtype=np.int64)
                 cidx = np.ascontiguousarray(cidx, dtype=np.uint32)
         self.nnz = nnz
-        self.relabel = bool(relabel)
         self._keep = (off, idx, coff, cidx)
-        self.handle = pp_graph_upload(ctx.handle, self.n, nnz, _ptr(off), _ptr(idx) if nnz else None,
-                                      _ptr(coff), _ptr(cidx) if (cidx is not None and nnz) else None,
-                                      flags)
+        self.handle = pp_graph_upload(ctx.handle, self.n, 0, self.n, nnz, _ptr(off),
+                                      _ptr(idx) if nnz else None, _ptr(coff),
+                                      _ptr(cidx) if (cidx is not None and nnz) else None, flags)
         self._keep = None
 
     @classmethod
-    def from_csr(cls, ctx, csr, csc=None, validate=False, relabel=False):
+    def from_csr(cls, ctx, csr, csc=None, validate=False, relabel=False, off64=False):
         if csc is None and not getattr(csr, "symmetric", True):
             raise ValueError("directed graph needs its CSC")
         return cls(ctx, csr.n, csr.off, csr.idx, None if csc is None else csc.off,
                    None if csc is None else csc.idx, symmetric=csc is None, validate=validate,
-                   relabel=relabel)
+                   relabel=relabel, off64=off64)
 
     def info(self):
         return pp_graph_info(self.handle)
@@ -333,22 +435,30 @@ def bfs(graph: Graph, source: int, depth, parent=None, heuristic=PP_HEUR_EDGES, 
     """Run pp_bfs.  depth/parent: int32 torch tensors (device) or numpy arrays (host).
     Returns a dict of per-level stats when stats_capacity > 0, else None."""
     o = pp_bfs_options(heuristic, mode, alpha, beta, 1 if parent is not None else 0, toggles)
-    st = None
-    arrays = None
-    if stats_capacity > 0:
-        arrays = dict(dir=np.zeros(stats_capacity, np.int8), c=np.zeros(stats_capacity, np.int64),
-                      m_f=np.zeros(stats_capacity, np.int64), m_u=np.zeros(stats_capacity, np.int64),
-                      ns=np.zeros(stats_capacity, np.int64))
-        st = pp_bfs_stats(0, 0, stats_capacity,
-                          arrays["dir"].ctypes.data_as(ctypes.POINTER(ctypes.c_int8)),
-                          arrays["c"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
-                          arrays["m_f"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
-                          arrays["m_u"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
-                          arrays["ns"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), 0)
+    st, arrays = _stats(stats_capacity)
     pp_bfs(graph.handle, source, o, _ptr(depth), _ptr(parent), st)
+    return _stats_dict(st, arrays, stats_capacity)
+
+
+def _stats(cap):
+    if cap <= 0:
+        return None, None
+    arrays = dict(dir=np.zeros(cap, np.int8), c=np.zeros(cap, np.int64),
+                  m_f=np.zeros(cap, np.int64), m_u=np.zeros(cap, np.int64),
+                  ns=np.zeros(cap, np.int64))
+    st = pp_bfs_stats(0, 0, cap,
+                      arrays["dir"].ctypes.data_as(ctypes.POINTER(ctypes.c_int8)),
+                      arrays["c"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                      arrays["m_f"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                      arrays["m_u"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                      arrays["ns"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), 0)
+    return st, arrays
+
+
+def _stats_dict(st, arrays, cap):
     if st is None:
         return None
-    L = min(st.levels, stats_capacity)
+    L = min(st.levels, cap)
     return dict(levels=st.levels, reached=st.reached, dir=arrays["dir"][:L], c=arrays["c"][:L],
                 m_f=arrays["m_f"][:L], m_u=arrays["m_u"][:L], ns=arrays["ns"][:L],
                 init_ns=st.init_ns)
@@ -403,6 +513,18 @@ def sssp(ctx: Context, csr_off, csr_idx, csr_w, csc_off, csc_idx, csc_w, source:
     weights).  Returns (dist fp32 device tensor, stats dict)."""
     import torch
     n = int(csr_off.numel()) - 1
+    want = ((csr_off, (torch.int64,)), (csc_off, (torch.int64,)),
+            (csr_idx, (torch.int32, torch.uint32)), (csc_idx, (torch.int32, torch.uint32)),
+            (csr_w, (torch.float32,)), (csc_w, (torch.float32,)))
+    dev0 = csr_off.device
+    for t, dts in want:
+        if not isinstance(t, torch.Tensor) or t.dtype not in dts or not t.is_contiguous() \
+                or t.device != dev0 or t.device.type != "cuda":
+            raise ValueError("sssp: int64 offsets, 32-bit ids and float32 weights, contiguous, "
+                             "all on one CUDA device")
+    if csc_off.numel() != n + 1 or csr_idx.numel() != csc_idx.numel() or \
+            csr_w.numel() != csr_idx.numel() or csc_w.numel() != csc_idx.numel():
+        raise ValueError("sssp: CSR / CSC array lengths disagree")
     if dist is None:
         dist = torch.empty(n, dtype=torch.float32, device=csr_off.device)
     st = pp_sssp(ctx.handle, n, int(csr_idx.numel()), csr_off, csr_idx, csr_w, csc_off, csc_idx,

@@ -23,15 +23,29 @@ def needs_build():
 
 
 def build(force=False, verbose=False):
+    """Compile every source to an object in parallel, then link the shared library."""
     if not force and not needs_build():
         return SO
+    import concurrent.futures as cf
     tmp = SO + f".tmp{os.getpid()}"
     extra = [f"-D{k}={os.environ[k]}" for k in ("PP_BFS_BLOCK", "PP_SUM_WORDS", "PP_PULL_WORDS", "PP_PULL_KC", "PP_SOLO_EDGES", "PP_LOWLAT_EDGES", "PP_NARROW_MAX_EDGES", "PP_NARROW_MAX_DEG", "PP_VREC", "PP_INIT_VEC", "PP_STREAM_U", "PP_SSSP_G", "PP_SSSP_HEAVY") if os.environ.get(k)]
     extra += ["-DPP_IDX_NOALLOC"] if os.environ.get("PP_IDX_NOALLOC") else []
-    extra += ["-ldl"]
-    cmd = [NVCC] + FLAGS + extra + (["-Xptxas", "-v"] if verbose else []) + \
-        [os.path.join(CSRC, f) for f in SOURCES] + ["-o", tmp]
-    subprocess.check_call(cmd)
+    odir = os.path.join(HERE, "build")
+    os.makedirs(odir, exist_ok=True)
+    cflags = [f for f in FLAGS if f != "-shared"]
+
+    def comp(src):
+        obj = os.path.join(odir, src + f".{os.getpid()}.o")
+        cmd = [NVCC] + cflags + extra + (["-Xptxas", "-v"] if verbose else []) + \
+            ["-c", os.path.join(CSRC, src), "-o", obj]
+        subprocess.check_call(cmd)
+        return obj
+
+    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(comp, SOURCES))
+    subprocess.check_call([NVCC] + FLAGS + objs + ["-ldl", "-o", tmp])
+    for o in objs:
+        os.unlink(o)
     os.replace(tmp, SO)
     return SO
 

@@ -1,4 +1,8 @@
+#include <algorithm>
 #include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
 // bfs.cu — persistent, device-resident direction-optimised BFS (Algorithm 1).
 //
 // One cooperative launch runs the whole traversal: every level is one phase
@@ -70,6 +74,28 @@ struct BfsArgs {
   int max_levels;
   long long* dbg;  // optional: per level, per CTA work duration (ns) of the level's phase
   int dbg_levels;
+  // CTAs of this rank in the launch: [cta_base, cta_base + ncta) (a single-device team runs
+  // its ranks as CTA groups of one cooperative launch; otherwise 0 and gridDim.x)
+  int cta_base, ncta;
+  // ---- multi-rank (1D row partition; D-template instantiations only) ----
+  // rank owns vertices [lo, hi) = bitmap words [wlo, wlo + wcnt); off/idx = push structure
+  // (global rows, owned targets), coff/cidx/head = CSC rows of the block (local row v - lo),
+  // depth/parent = the block's slices.  Each level's discoveries are OR-ed into xfr[d & 1]
+  // and the owned words are stored into every peer's copy (pfr), the per-rank counters into
+  // every peer's record slot (pcnt), then one release flag per peer (pflag).
+  int64_t lo, hi;
+  uint32_t wlo, wcnt;
+  int me, nranks;  // this rank's index, ranks in the group
+  uint32_t* xfr0;
+  uint32_t* xfr1;
+  unsigned long long* xcnt;   // own [2][kMaxRanks][4]
+  unsigned long long* xflag;  // own [kMaxRanks]
+  uint32_t* pfr[kMaxRanks][2];
+  unsigned long long* pcnt[kMaxRanks];
+  unsigned long long* pflag[kMaxRanks];
+  unsigned long long xseq;  // flag epoch base of this BFS (monotone across calls)
+  const uint32_t* __restrict__ odeg;  // directed: global out-degree of the owned rows
+  long long in_total;                 // sum of in-degrees over all ranks
 };
 
 constexpr unsigned long long kWatchdogNs = 4000000000ull;  // 4 s per barrier wait
@@ -94,12 +120,13 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
   return v;
 }
 
-__device__ __forceinline__ bool grid_barrier(GridBarrier* b, BfsStatus* st, unsigned& epoch) {
+__device__ __forceinline__ bool grid_barrier(GridBarrier* b, BfsStatus* st, unsigned& epoch,
+                                             unsigned ncta) {
   __shared__ int s_ok;
   __syncthreads();
   if (threadIdx.x == 0) {
     ++epoch;
-    const unsigned long long target = (unsigned long long)epoch * gridDim.x;
+    const unsigned long long target = (unsigned long long)epoch * ncta;
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(&b->count);
     unsigned long long v = atom_add_release_u64(cnt, 1ull) + 1ull;
     if (v < target) {
@@ -129,13 +156,13 @@ __device__ __forceinline__ void cluster_barrier() {
                "barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 __device__ __forceinline__ bool level_barrier(bool narrow, GridBarrier* b, BfsStatus* st,
-                                              unsigned& epoch) {
+                                              unsigned& epoch, unsigned ncta) {
   if (narrow) {
     __syncthreads();
     cluster_barrier();
     return true;
   }
-  return grid_barrier(b, st, epoch);
+  return grid_barrier(b, st, epoch, ncta);
 }
 
 // Per-lane accumulators of a level's counters, flushed once per phase.
@@ -178,13 +205,17 @@ __device__ __forceinline__ void flush_acc(Acc& acc, LevelCtr* out,
 // same mix of heavy and light items) and its warps grab them dynamically through a
 // shared-memory counter (reset to 0 before each phase by read_level), which balances the
 // irregular per-item cost inside the CTA without any global atomics.
-__device__ __forceinline__ unsigned cta_grab(unsigned* sctr) {
+template <typename Off>
+__device__ __forceinline__ unsigned cta_of(const BfsArgs<Off>& a) { return blockIdx.x - a.cta_base; }
+template <typename Off>
+__device__ __forceinline__ unsigned cta_grab(const BfsArgs<Off>& a, unsigned* sctr) {
   unsigned j = 0;
   if (lane_id() == 0) j = atomicAdd(sctr, 1u);
   j = __shfl_sync(kFull, j, 0);
-  return blockIdx.x + j * gridDim.x;
+  return cta_of(a) + j * (unsigned)a.ncta;
 }
-__device__ __forceinline__ unsigned nwarps() { return gridDim.x * kBfsWarps; }
+template <typename Off>
+__device__ __forceinline__ unsigned nwarps(const BfsArgs<Off>& a) { return (unsigned)a.ncta * kBfsWarps; }
 
 
 
@@ -303,11 +334,17 @@ __device__ __forceinline__ void append_frontier4(const bool (&disc)[kU], const u
 // (w unvisited) precedes the OR-merge (atomicOr on the visited bitmap).  Parents:
 // atomicMin over every edge whose head was unvisited when the level started
 // (SURVEY.md G14): bit clear in a post-barrier read, or depth 0 / newdepth.
-template <typename Off, bool PARENTS>
+//
+// Multi-rank (D): every target w is owned (the push structure holds only owned targets);
+// a discovery writes the block's depth slot w - lo and ORs w into the level's frontier
+// bitmap `frout` (exchanged after the level) instead of appending to the local lists, and
+// counts the GLOBAL out-degree of w for m_f (the decision needs global sums).
+template <typename Off, bool PARENTS, bool D>
 __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&valid)[kU],
                                             const uint32_t (&u)[kU], const uint32_t (&w)[kU],
                                             uint32_t* vis, int newdepth, uint4* Lout,
-                                            uint2* Hout, LevelCtr* out, Acc& acc, bool lowlat) {
+                                            uint2* Hout, LevelCtr* out, Acc& acc, bool lowlat,
+                                            uint32_t* frout) {
   uint32_t cur[kU];
   bool disc[kU];
   Off sb[kU], se[kU];
@@ -351,14 +388,31 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
     for (int t = 0; t < kU; ++t) {
       if (!valid[t]) continue;
       bool fresh = disc[t] || !((cur[t] >> (w[t] & 31u)) & 1u);
+      const uint32_t slot = D ? w[t] - (uint32_t)a.lo : w[t];
       if (!fresh) {
-        const int dw = ld_relaxed_s32(&a.depth[a.perm ? a.perm[w[t]] : w[t]]);
+        const int dw = ld_relaxed_s32(&a.depth[D ? slot : (a.perm ? a.perm[w[t]] : w[t])]);
         fresh = (dw == 0 || dw == newdepth);
       }
-      if (fresh) atomicMin(&a.parent[w[t]], u[t]);
+      if (fresh) atomicMin(&a.parent[slot], u[t]);
     }
   }
   if (!__any_sync(kFull, disc[0] || disc[1] || disc[2] || disc[3])) return;
+  if (D) {
+#pragma unroll
+    for (int t = 0; t < kU; ++t) {
+      if (!disc[t]) continue;
+      const uint32_t r = w[t] - (uint32_t)a.lo;  // local row of the owned target
+      const Off degin = a.coff[r + 1] - a.coff[r];
+      const Off dg = a.symmetric ? degin : (Off)a.odeg[r];
+      a.depth[r] = newdepth;
+      atomicOr(&frout[w[t] >> 5], 1u << (w[t] & 31u));
+      acc.c += 1;
+      acc.mf += (unsigned long long)dg;
+      acc.mfin += (unsigned long long)degin;
+      acc.big += dg >= (Off)kBig ? 1u : 0u;
+    }
+    return;
+  }
   Off deg[kU], beg[kU];
   uint32_t dpos[kU];  // where the discovery's depth goes (caller id)
 #pragma unroll
@@ -391,10 +445,11 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
 
 // Edges of up to 32 light frontier vertices (lane l holds v, row begin b, degree deg),
 // balanced over lanes by a warp scan of the degrees, kU edges in flight per lane.
-template <typename Off, bool PARENTS>
+template <typename Off, bool PARENTS, bool D>
 __device__ __forceinline__ void push_round(const BfsArgs<Off>& a, uint32_t v, Off b, unsigned deg,
                                            uint4* Lout, uint2* Hout, LevelCtr* out,
-                                           uint32_t* vis, int newdepth, Acc& acc, bool lowlat) {
+                                           uint32_t* vis, int newdepth, Acc& acc, bool lowlat,
+                                           uint32_t* frout) {
   const unsigned lane = lane_id();
   const unsigned incl = warp_incl_scan(deg);
   const unsigned excl = incl - deg;
@@ -412,7 +467,8 @@ __device__ __forceinline__ void push_round(const BfsArgs<Off>& a, uint32_t v, Of
       valid[t] = e < tot;
       w[t] = valid[t] ? a.idx[bj + (Off)(e - xj)] : 0u;
     }
-    push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat);
+    push_visit4<Off, PARENTS, D>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat,
+                                 frout);
   }
 }
 
@@ -428,20 +484,20 @@ constexpr unsigned kPW = PP_PULL_WORDS;  // bitmap words per warp item (32*kPW r
 // 128 consecutive edges = one warp iteration with 4 coalesced loads per lane.  Light
 // round = R frontier vertices (R = 32, or fewer when the frontier is too small to occupy
 // every warp), their edges balanced over lanes by a warp scan of degrees.
-template <typename Off, bool PARENTS>
+template <typename Off, bool PARENTS, bool D>
 __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
                            const uint2* Hin, unsigned nH, unsigned nB, const uint32_t* fr,
                            uint4* Lout,
                            uint2* Hout, LevelCtr* out, uint32_t* vis, int newdepth, Acc& acc,
-                           unsigned* sctr, bool lowlat) {
+                           unsigned* sctr, bool lowlat, uint32_t* frout) {
   const unsigned lane = lane_id();
-  const unsigned NW = nwarps();
+  const unsigned NW = nwarps(a);
   unsigned R = 32;
   while (R > 1 && (nL + R / 2 - 1) / (R / 2) <= NW) R >>= 1;
   const unsigned nRounds = fr ? a.nwords / kPW : (nL + R - 1) / R;
   const unsigned nHC = nH + 32u * nB;  // chunk items: descriptors, then 32 per hub block
   const unsigned total = nHC + nRounds;
-  for (unsigned item = cta_grab(sctr); item < total; item = cta_grab(sctr)) {
+  for (unsigned item = cta_grab(a, sctr); item < total; item = cta_grab(a, sctr)) {
     if (item < nHC) {
       bool valid[kU];
       uint32_t u[kU], w[kU];
@@ -463,7 +519,8 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
         u[t] = h.x;
         w[t] = valid[t] ? a.idx[p] : 0u;
       }
-      push_visit4<Off, PARENTS>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat);
+      push_visit4<Off, PARENTS, D>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat,
+                                   frout);
     } else if (!fr) {
       const unsigned i = (item - nHC) * R + lane;
       uint32_t v = 0;
@@ -475,7 +532,7 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
         deg = le.y;
         b = light_begin<Off>(le);
       }
-      push_round<Off, PARENTS>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc, lowlat);
+      push_round<Off, PARENTS, D>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc, lowlat, frout);
     } else {
       const unsigned wbase = (item - nHC) * kPW;
       const uint32_t fw = lane < kPW ? fr[wbase + lane] : 0u;
@@ -496,7 +553,8 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
           b = a.off[v];
           deg = (unsigned)(a.off[v + 1] - b);
         }
-        push_round<Off, PARENTS>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc, lowlat);
+        push_round<Off, PARENTS, D>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc, lowlat,
+                                    frout);
       }
     }
   }
@@ -543,7 +601,7 @@ __device__ __forceinline__ V8 ld_nc_v8(const uint32_t* p) {
   return v;
 }
 
-template <typename Off, bool PARENTS>
+template <typename Off, bool PARENTS, bool D>
 struct PullCtx {
   const BfsArgs<Off>& a;
   const uint32_t* __restrict__ vin;
@@ -556,12 +614,13 @@ struct PullCtx {
   const uint32_t* ssum;  // shared-memory copy of the visited summary (snapshot)
   uint2* hubs;           // no early exit: long-row chunk descriptors (2 uint2 each) ...
   unsigned* hub_count;   // ... and their count
+  uint32_t* fr;          // the level's frontier bitmap (multi-rank: the exchanged xfr[d & 1])
 
   // Visited test of a probed neighbour.  The summary in shared memory rejects most
   // unvisited neighbours without a global access (false positives only: a set summary
   // bit is confirmed against the exact snapshot bitmap).
   __device__ __forceinline__ bool hit(uint32_t x) const {
-    if (no_reuse) return a.depth[a.perm ? a.perm[x] : x] == d;
+    if (!D && no_reuse) return a.depth[a.perm ? a.perm[x] : x] == d;
     if (kSumWordsMax) {
       const uint32_t gi = x >> a.sum_shift;
       if (!((ssum[gi >> 5] >> (gi & 31u)) & 1u)) return false;
@@ -610,15 +669,16 @@ struct PullCtx {
       atomicOr(&sfound[(i >> 5) - wbase], bit);
     } else {
       atomicOr(&vout[i >> 5], bit);
-      atomicOr(&a.fr[i >> 5], bit);
+      atomicOr(&fr[i >> 5], bit);
     }
-    a.depth[dpos] = d + 1;  // caller id of i
-    if (PARENTS) a.parent[i] = par;
+    a.depth[dpos] = d + 1;  // caller id of i (multi-rank: the block's slot i - lo)
+    if (PARENTS) a.parent[D ? i - (uint32_t)a.lo : i] = par;
     if (kSumWordsMax && !in_item) {  // in-item finds reach the summary at item close
       const uint32_t gi = i >> a.sum_shift;
       atomicOr(&a.sumv[gi >> 5], 1u << (gi & 31u));
     }
-    const Off deg = a.symmetric ? degin : (Off)(a.off[i + 1] - a.off[i]);
+    const Off deg = a.symmetric ? degin
+                    : (D ? (Off)a.odeg[i - (uint32_t)a.lo] : (Off)(a.off[i + 1] - a.off[i]));
     acc.c += 1;
     acc.mf += (unsigned long long)deg;
     acc.mfin += (unsigned long long)degin;
@@ -748,7 +808,8 @@ struct PullCtx {
     }
     if (valid && found && !committed) {
       const bool in_item = (i >> 5) >= wbase && (i >> 5) < wbase + pw;
-      commit(i, par, (Off)degin, wbase, in_item, a.perm ? a.perm[i] : i);
+      commit(i, par, (Off)degin, wbase, in_item,
+             D ? i - (uint32_t)a.lo : (a.perm ? a.perm[i] : i));
     }
   }
 };
@@ -764,17 +825,23 @@ struct PullCtx {
 // group / warp tiers).  Found bits are OR-ed in shared memory; the owning lane writes
 // v' = v | found and the frontier bitmap; rows resolved after their item closed use
 // atomicOr.
-template <typename Off, bool PARENTS>
+//
+// Multi-rank (D): the items cover the owned words [wlo, wlo + wcnt) only; the rows' CSC
+// data is local (row i - lo), the probed in-neighbour ids are global and test the
+// replicated visited snapshot.
+template <typename Off, bool PARENTS, bool D>
 __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
                            uint32_t* __restrict__ vout, LevelCtr* out, int d, Acc& acc,
                            uint32_t* sfound, ResidualQ<Off>& rq, const uint32_t* ssum,
-                           unsigned* sctr) {
+                           unsigned* sctr, uint32_t* fr) {
   const unsigned lane = lane_id();
-  const unsigned nitems = a.nwords / kPW;
+  const unsigned nitems = (D ? a.wcnt : a.nwords) / kPW;
+  const unsigned wb0 = D ? a.wlo : 0u;
+  const uint32_t lo = D ? (uint32_t)a.lo : 0u;
   const bool no_mask = (a.toggles & PP_OPT_NO_MASKING) != 0;
-  PullCtx<Off, PARENTS> C{a, vin, vout, d, !(a.toggles & PP_OPT_NO_EARLYEXIT),
-                          (a.toggles & PP_OPT_NO_REUSE) != 0, acc, sfound, rq, ssum,
-                          a.H0, &out->work2};
+  PullCtx<Off, PARENTS, D> C{a, vin, vout, d, !(a.toggles & PP_OPT_NO_EARLYEXIT),
+                             (a.toggles & PP_OPT_NO_REUSE) != 0, acc, sfound, rq, ssum,
+                             a.H0, &out->work2, fr};
   int qn = 0;
   unsigned wbase = 0;
   // CTA b owns items b, b+G, ... (G = grid, interleaved so every CTA sees the same mix of
@@ -782,10 +849,11 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
   // The warp grabs one step ahead and loads the next item's visited words meanwhile.
   // (Handing a CTA's last items out one word at a time, or smaller items, measured slower:
   // DESIGN.md §11.)
-  const unsigned G = gridDim.x;
-  const unsigned K = nitems > blockIdx.x ? (nitems - blockIdx.x + G - 1) / G : 0u;
+  const unsigned G = (unsigned)a.ncta;
+  const unsigned cta = cta_of(a);
+  const unsigned K = nitems > cta ? (nitems - cta + G - 1) / G : 0u;
   auto map = [&](unsigned k, unsigned& w0, unsigned& pw) {
-    w0 = (blockIdx.x + k * G) * kPW;
+    w0 = wb0 + (cta + k * G) * kPW;
     pw = kPW;
   };
   auto grab = [&]() {
@@ -840,12 +908,13 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
       uint32_t dpos[kC];  // caller id of the row (relabelled graph: loaded with the head)
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
-        dpos[t] = i[t];
+        const uint32_t li = i[t] - lo;  // row of the CSC block (lo = 0 on one GPU)
+        dpos[t] = li;
         if (valid[t]) {
-          if (a.perm) dpos[t] = a.perm[i[t]];
-          rb[t] = a.coff[i[t]];
-          e[t] = a.coff[i[t] + 1];
-          hd[t] = ld_nc_v8(a.head + (size_t)i[t] * 8u);
+          if (!D && a.perm) dpos[t] = a.perm[i[t]];
+          rb[t] = a.coff[li];
+          e[t] = a.coff[li + 1];
+          hd[t] = ld_nc_v8(a.head + (size_t)li * 8u);
         }
       }
       // stage: probe the first neighbour, then the other head ids of rows that missed
@@ -899,7 +968,7 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
     const uint32_t fw = own ? sfound[lane] : 0u;
     if (own) {
       vout[wbase + lane] = vw | fw;
-      a.fr[wbase + lane] = fw;
+      fr[wbase + lane] = fw;
     }
     if (kSumWordsMax && a.sum_shift >= 5) {
       // the item's rows map into one summary word: one aggregated atomic per item
@@ -926,8 +995,8 @@ __device__ void pull_hub_chunks(const BfsArgs<Off>& a, const uint32_t* __restric
                                 uint32_t* __restrict__ vout, LevelCtr* out, unsigned nch, int d,
                                 Acc& acc, ResidualQ<Off>& rq) {
   const unsigned lane = lane_id();
-  PullCtx<Off, PARENTS> C{a, vin, vout, d, false, (a.toggles & PP_OPT_NO_REUSE) != 0, acc,
-                          nullptr, rq, nullptr, a.H0, nullptr};
+  PullCtx<Off, PARENTS, false> C{a, vin, vout, d, false, (a.toggles & PP_OPT_NO_REUSE) != 0,
+                                 acc, nullptr, rq, nullptr, a.H0, nullptr, a.fr};
   while (true) {
     unsigned j = 0;
     if (lane == 0) j = atomicAdd(&out->work, 1u);
@@ -975,9 +1044,9 @@ __device__ void convert_phase(const BfsArgs<Off>& a, const uint32_t* vnew, const
                               uint4* Lout, uint2* Hout, LevelCtr* out, unsigned* sctr) {
   const unsigned lane = lane_id();
   const unsigned nchunks = a.nwords / 32u;
-  for (unsigned item = cta_grab(sctr); item < nchunks; item = cta_grab(sctr)) {
+  for (unsigned item = cta_grab(a, sctr); item < nchunks; item = cta_grab(a, sctr)) {
     const unsigned w = item * 32u + lane;
-    uint32_t diff = vnew[w] & ~vold[w];
+    uint32_t diff = vold ? (vnew[w] & ~vold[w]) : vnew[w];  // multi-rank: vnew = frontier
     while (__ballot_sync(kFull, diff != 0u)) {
       const bool valid = diff != 0u;
       uint32_t v = 0;
@@ -1031,32 +1100,146 @@ __device__ __forceinline__ void read_level(const LevelCtr* out, BfsShared<Off>& 
   __syncthreads();
 }
 
-template <typename Off, bool PARENTS>
-__global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
+__device__ __forceinline__ void st_release_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Multi-rank: one cross-rank rendezvous.  Thread 0 of CTA 0 stores `tag` into its slot of
+// every peer's flag array (release, system scope: the rank's earlier peer stores, fenced by
+// every CTA and collected by the rank-local barrier before this call, become visible first);
+// thread 0 of every CTA then waits (acquire, system scope) until every peer's flag in its own
+// array reached `tag`.  Watchdog as in grid_barrier.
+template <typename Off>
+__device__ __forceinline__ bool rank_rendezvous(const BfsArgs<Off>& a, unsigned long long tag) {
+  __shared__ int s_ok;
+  if (threadIdx.x == 0) {
+    int ok = 1;
+    if (cta_of(a) == 0)
+      for (int q = 0; q < a.nranks; ++q)
+        if (q != a.me) st_release_sys_u64(a.pflag[q] + a.me, tag);
+    const unsigned long long t0 = global_timer_ns();
+    for (int q = 0; q < a.nranks && ok; ++q) {
+      if (q == a.me) continue;
+      while (ld_acquire_sys_u64(a.xflag + q) < tag) {
+        __nanosleep(32);
+        if (global_timer_ns() - t0 > kWatchdogNs) {
+          atomicExch(&a.status->error, (int)PP_ERR_TIMEOUT);
+          atomicOr(reinterpret_cast<unsigned long long*>(&a.bar->count), kAbortBit);
+          ok = 0;
+          break;
+        }
+      }
+    }
+    __threadfence();
+    s_ok = ok;
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+// Multi-rank exchange after level d (SURVEY.md §8e, NEXT-1 "exchange fused into the level
+// kernel over NVLink").  Entered by every CTA of the rank right after the level barrier;
+// sh.lvl holds this rank's counter sums.  (1) the owned words of the level's frontier bitmap
+// go straight into every peer's copy (16-byte peer stores); (2) the rank's counter record
+// (c, m_f, m_fin, big) goes into its slot of every rank's table; (3) system-scope fence,
+// rank-local barrier, one release flag per peer and the wait for the peers' flags;
+// (4) every CTA sums the P records, so every rank continues with identical global counters
+// and takes the identical direction decision (R10/R11) without any host round trip.
+template <typename Off>
+__device__ bool exchange(const BfsArgs<Off>& a, BfsShared<Off>& sh, const uint32_t* frout, int d,
+                         unsigned& epoch, long long extra_mfin, unsigned long long gtid,
+                         unsigned long long gsize) {
+  const int P = a.nranks, me = a.me;
+  const unsigned par = (unsigned)d & 1u;
+  if (P > 1) {
+    const unsigned nv = a.wcnt / 4u;
+    const uint4* src = reinterpret_cast<const uint4*>(frout + a.wlo);
+    const unsigned long long tot = (unsigned long long)nv * (unsigned)(P - 1);
+    for (unsigned long long k = gtid; k < tot; k += gsize) {
+      const int qi = (int)(k / nv);
+      const unsigned j = (unsigned)(k - (unsigned long long)qi * nv);
+      const int q = qi >= me ? qi + 1 : qi;
+      reinterpret_cast<uint4*>(a.pfr[q][par] + a.wlo)[j] = src[j];
+    }
+  }
+  if (cta_of(a) == 0 && threadIdx.x < (unsigned)P) {
+    unsigned long long* rec = a.pcnt[threadIdx.x] + ((size_t)par * kMaxRanks + (size_t)me) * 4u;
+    rec[0] = (unsigned long long)sh.lvl[0];
+    rec[1] = (unsigned long long)sh.lvl[1];
+    rec[2] = (unsigned long long)(sh.lvl[2] + extra_mfin);
+    rec[3] = (unsigned long long)sh.lvl[5];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) __threadfence_system();
+  if (!grid_barrier(a.bar, a.status, epoch, (unsigned)a.ncta)) return false;
+  if (P > 1 && !rank_rendezvous(a, a.xseq + (unsigned long long)d)) return false;
+  if (threadIdx.x == 0) {
+    long long c = 0, mf = 0, mfin = 0, big = 0;
+    for (int q = 0; q < P; ++q) {
+      const unsigned long long* rec = a.xcnt + ((size_t)par * kMaxRanks + (size_t)q) * 4u;
+      c += (long long)ld_relaxed_u64(rec + 0);
+      mf += (long long)ld_relaxed_u64(rec + 1);
+      mfin += (long long)ld_relaxed_u64(rec + 2);
+      big += (long long)ld_relaxed_u64(rec + 3);
+    }
+    sh.lvl[0] = c;
+    sh.lvl[1] = mf;
+    sh.lvl[2] = mfin;
+    sh.lvl[5] = big;
+  }
+  __syncthreads();
+  return true;
+}
+
+// The BFS loop (Algorithm 1) run by the CTAs of one rank.  D = multi-rank (1D
+// row partition): the same push / pull / convert phases over the rank's block, plus the
+// exchange after every level and a merge of the peers' discoveries into the visited bitmap.
+template <typename Off, bool PARENTS, bool D>
+__device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
   __shared__ BfsShared<Off> sh;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
   ResidualQ<Off>* rqs = reinterpret_cast<ResidualQ<Off>*>(dyn_smem);
   uint32_t* ssum = reinterpret_cast<uint32_t*>(dyn_smem + sizeof(ResidualQ<Off>) * kBfsWarps);
   const unsigned warp = threadIdx.x >> 5;
-  const unsigned long long gtid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const unsigned long long gsize = (unsigned long long)gridDim.x * blockDim.x;
-  const uint32_t s = a.rank ? a.rank[a.source] : a.source;  // internal id of the source
+  const unsigned cta = cta_of(a);
+  const unsigned long long gtid = (unsigned long long)cta * blockDim.x + threadIdx.x;
+  const unsigned long long gsize = (unsigned long long)a.ncta * blockDim.x;
+  // internal id of the source (relabelled graph) / its global id (multi-rank)
+  const uint32_t s = (!D && a.rank) ? a.rank[a.source] : a.source;
   if (a.resume && a.bar->rs.done) return;  // the narrow launch finished the BFS
-  if (!a.resume && blockIdx.x == 0 && threadIdx.x == 0)
+  if (!a.resume && cta == 0 && threadIdx.x == 0)
     a.status->t_start = (long long)global_timer_ns();
   unsigned epoch = 0;  // grid barriers passed (thread 0)
-
+  // multi-rank: the owned block and the source's slot in it
+  const bool own_s = D && (int64_t)s >= a.lo && (int64_t)s < a.hi;
+  const unsigned long long nloc = D ? (unsigned long long)(a.hi - a.lo) : (unsigned long long)a.n;
+  const unsigned long long srcl = D ? (own_s ? (unsigned long long)(s - (uint32_t)a.lo) : ~0ull)
+                                    : (unsigned long long)a.source;
 
   int dir = (a.mode == 2) ? 1 : 0;
   int cur = 0;  // visited bitmap in use
   int sel = 0;  // frontier list / chunk buffers holding the current frontier
   long long c_old = 1;
-  const Off indeg_s = a.coff[s + 1] - a.coff[s];
-  long long m_u = a.nnz - (long long)indeg_s;
+  long long m_u, indeg_s_own = 0;
+  if (D) {
+    // m_u starts at the global in-degree mass; the source's owner adds indeg(s) to its
+    // level-1 m_fin record, so every rank subtracts it after level 1
+    m_u = a.in_total;
+    if (own_s) indeg_s_own = (long long)(a.coff[s - (uint32_t)a.lo + 1] - a.coff[s - (uint32_t)a.lo]);
+  } else {
+    const Off indeg_s = a.coff[s + 1] - a.coff[s];
+    m_u = a.nnz - (long long)indeg_s;
+  }
   long long reached = 1;
   Acc acc{0, 0, 0, 0};
-  bool from_bits = false;  // next push reads the pull's frontier bitmap
-  long long mf_last = (long long)(a.off[s + 1] - a.off[s]);  // edges the next push expands
+  bool from_bits = false;  // next push reads the previous level's frontier bitmap
+  // edges the next push expands (a latency heuristic only; multi-rank: this rank's part)
+  long long mf_last = (long long)(a.off[s + 1] - a.off[s]);
   int d = 1;
   unsigned nL = 0, nH = 0, nB = 0;
   if (a.resume) {  // continue where the narrow cluster stopped (stream-ordered after it)
@@ -1079,34 +1262,41 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   // ---- Alg. 1 lines 2-4: d <- 1, f <- e_s, v <- 0 (depth 0 = unvisited) ----
   if (kInitVec && !PARENTS && (reinterpret_cast<uintptr_t>(a.depth) & 15u) == 0) {
     // 16-byte stores: a quarter of the store instructions of the scalar loop
-    const unsigned long long n4 = (unsigned long long)a.n / 4u;
+    const unsigned long long n4 = nloc / 4u;
     int4* d4 = reinterpret_cast<int4*>(a.depth);
     for (unsigned long long q = gtid; q < n4; q += gsize) {
       const unsigned long long v0 = q * 4u;
-      d4[q] = make_int4(v0 == a.source, v0 + 1 == a.source, v0 + 2 == a.source, v0 + 3 == a.source);
+      d4[q] = make_int4(v0 == srcl, v0 + 1 == srcl, v0 + 2 == srcl, v0 + 3 == srcl);
     }
-    for (unsigned long long v = n4 * 4u + gtid; v < (unsigned long long)a.n; v += gsize)
-      a.depth[v] = (v == a.source) ? 1 : 0;
+    for (unsigned long long v = n4 * 4u + gtid; v < nloc; v += gsize)
+      a.depth[v] = (v == srcl) ? 1 : 0;
   } else {
-    for (unsigned long long v = gtid; v < (unsigned long long)a.n; v += gsize) {
-      a.depth[v] = (v == a.source) ? 1 : 0;                          // caller ids
-      if (PARENTS) a.parent[v] = (v == s) ? s : 0xFFFFFFFFu;         // internal ids
+    for (unsigned long long v = gtid; v < nloc; v += gsize) {
+      a.depth[v] = (v == srcl) ? 1 : 0;                              // caller ids / block slots
+      if (PARENTS) a.parent[v] = (v == (D ? srcl : (unsigned long long)s)) ? s : 0xFFFFFFFFu;
     }
   }
   // visited starts as {s} plus the isolated / padding vertices, which no pull may
-  // compute and no push can reach (they have no edges).
-  for (unsigned long long w = gtid; w < a.nwords; w += gsize)
-    a.vis0[w] = a.isolated[w] | ((w == (s >> 5)) ? (1u << (s & 31u)) : 0u);
+  // compute and no push can reach (they have no edges).  Multi-rank: the isolated words of
+  // other blocks are 0 here (never tested), and the level-0 frontier {s} is xfr0.
+  const uint32_t sbit_w = s >> 5, sbit = 1u << (s & 31u);
+  for (unsigned long long w = gtid; w < a.nwords; w += gsize) {
+    a.vis0[w] = a.isolated[w] | ((w == sbit_w) ? sbit : 0u);
+    if (D) {
+      a.xfr0[w] = (w == sbit_w) ? sbit : 0u;
+      if (w >= a.wlo && w < (unsigned long long)a.wlo + a.wcnt) a.xfr1[w] = 0u;
+    }
+  }
   {
     const uint32_t gs = s >> a.sum_shift;
     for (unsigned long long w = gtid; w < a.sum_words; w += gsize)
       a.sumv[w] = (w == (gs >> 5)) ? (1u << (gs & 31u)) : 0u;
   }
-  if (blockIdx.x == 0) {
+  if (cta == 0) {
     for (int t = threadIdx.x; t < kRing * (int)(sizeof(LevelCtr) / 4); t += blockDim.x)
       reinterpret_cast<unsigned*>(a.ctr)[t] = 0u;
     __syncthreads();
-    const Off deg = a.off[s + 1] - a.off[s];
+    const Off deg = a.off[s + 1] - a.off[s];  // multi-rank: s's edges into this block
     if (deg >= (Off)kHeavy) {
       const unsigned nch = (unsigned)((deg + (Off)kChunk - 1) / (Off)kChunk);
       if (nch <= kSelfChunks) {
@@ -1123,9 +1313,9 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       a.ctr[0].nL = 1;
     }
   }
-  if (!level_barrier(a.narrow, a.bar, a.status, epoch)) return;
+  if (!level_barrier(a.narrow, a.bar, a.status, epoch, (unsigned)a.ncta)) return;
   read_level(&a.ctr[0], sh);
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.status->t_init = (long long)global_timer_ns();
+  if (cta == 0 && threadIdx.x == 0) a.status->t_init = (long long)global_timer_ns();
   nL = (unsigned)sh.lvl[3];
   nH = (unsigned)sh.lvl[4];
   nB = (unsigned)sh.lvl[6];
@@ -1133,7 +1323,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   for (;; ++d) {
     if (a.narrow && (dir == 1 || (unsigned long long)mf_last > kNarrowMaxEdges)) {
       // this level is too wide for one cluster: hand the loop to the whole grid
-      if (blockIdx.x == 0 && threadIdx.x == 0) {
+      if (cta == 0 && threadIdx.x == 0) {
         BfsResume& r = a.bar->rs;
         r.d = d;
         r.dir = dir;
@@ -1153,43 +1343,48 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
     }
     const long long t_lvl = (a.dbg && threadIdx.x == 0) ? (long long)global_timer_ns() : 0;
     LevelCtr* out = &a.ctr[d & (kRing - 1)];
-    if (blockIdx.x == 0 && threadIdx.x < sizeof(LevelCtr) / 4)
+    if (cta == 0 && threadIdx.x < sizeof(LevelCtr) / 4)
       reinterpret_cast<unsigned*>(&a.ctr[(d + 1) & (kRing - 1)])[threadIdx.x] = 0u;
     uint32_t* vis = cur ? a.vis1 : a.vis0;
     uint32_t* vis_other = cur ? a.vis0 : a.vis1;
+    // frontier bitmap this level writes (pull; multi-rank also push) and the previous one
+    uint32_t* frout = D ? ((d & 1) ? a.xfr1 : a.xfr0) : a.fr;
+    uint32_t* frin = D ? ((d & 1) ? a.xfr0 : a.xfr1) : a.fr;
     if (dir == 0) {
-      push_phase<Off, PARENTS>(a, sel ? a.L1 : a.L0, from_bits ? 0u : nL, sel ? a.H1 : a.H0,
-                               from_bits ? 0u : nH, from_bits ? 0u : nB, from_bits ? a.fr : nullptr,
-                               sel ? a.L0 : a.L1, sel ? a.H0 : a.H1, out, vis, d + 1, acc,
-                               &sh.work, (unsigned long long)mf_last <= kLowLatEdges);
+      push_phase<Off, PARENTS, D>(a, sel ? a.L1 : a.L0, from_bits ? 0u : nL, sel ? a.H1 : a.H0,
+                                  from_bits ? 0u : nH, from_bits ? 0u : nB, from_bits ? frin : nullptr,
+                                  sel ? a.L0 : a.L1, sel ? a.H0 : a.H1, out, vis, d + 1, acc,
+                                  &sh.work, (unsigned long long)mf_last <= kLowLatEdges, frout);
       from_bits = false;
     } else {
       if (kSumWordsMax) {
         for (unsigned t = threadIdx.x; t < a.sum_words; t += blockDim.x) ssum[t] = a.sumv[t];
         __syncthreads();
       }
-      pull_phase<Off, PARENTS>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp],
-                               ssum, &sh.work);
-      if (a.toggles & PP_OPT_NO_EARLYEXIT) {  // ablation arms: long rows grid-wide
-        if (!level_barrier(a.narrow, a.bar, a.status, epoch)) return;
+      pull_phase<Off, PARENTS, D>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp],
+                                  ssum, &sh.work, frout);
+      if (!D && (a.toggles & PP_OPT_NO_EARLYEXIT)) {  // ablation arms: long rows grid-wide
+        if (!level_barrier(a.narrow, a.bar, a.status, epoch, (unsigned)a.ncta)) return;
         const unsigned nch = ld_relaxed_u32(&out->work2);
         if (nch) pull_hub_chunks<Off, PARENTS>(a, vis, vis_other, out, nch, d, acc, rqs[warp]);
       }
     }
     if (a.dbg && threadIdx.x == 0 && d - 1 < a.dbg_levels)
-      a.dbg[(size_t)(d - 1) * gridDim.x + blockIdx.x] = (long long)global_timer_ns() - t_lvl;
+      a.dbg[(size_t)(d - 1) * a.ncta + cta] = (long long)global_timer_ns() - t_lvl;
     flush_acc(acc, out, sh.red);
-    if (!level_barrier(a.narrow, a.bar, a.status, epoch)) return;
+    if (!level_barrier(a.narrow, a.bar, a.status, epoch, (unsigned)a.ncta)) return;
     read_level(out, sh);
+    if (D && !exchange<Off>(a, sh, frout, d, epoch, (d == 1) ? indeg_s_own : 0, gtid, gsize)) return;
     const long long c_new = sh.lvl[0], mf = sh.lvl[1], mfin = sh.lvl[2];
     nL = (unsigned)sh.lvl[3];
     nH = (unsigned)sh.lvl[4];
     nB = (unsigned)sh.lvl[6];
+    const int dir_done = dir;
     if (dir == 1) cur ^= 1;
-    else sel ^= 1;
-    m_u -= a.symmetric ? mf : mfin;
+    else if (!D) sel ^= 1;  // multi-rank pushes append nothing (the frontier is exchanged)
+    m_u -= (D || !a.symmetric) ? mfin : mf;
     reached += c_new;
-    if (blockIdx.x == 0 && threadIdx.x == 0 && d - 1 < a.stats_cap) {
+    if (cta == 0 && threadIdx.x == 0 && d - 1 < a.stats_cap) {
       LevelStat st;
       st.dir = dir;
       st.pad = 0;
@@ -1204,7 +1399,34 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
     if (!done && a.mode == 0)
       next = decide(a.rule, dir, c_old, c_new, mf, m_u, a.n, a.alpha, a.beta);
     if (done) break;
-    if (dir == 1 && next == 0 && sh.lvl[5] == 0) {
+    if (D) {
+      // merge the peers' discoveries into the visited bitmap the next level reads (the owned
+      // words are already final), clear the owned words of the next push's output bitmap,
+      // and build this rank's push frontier from the exchanged bitmap: straight from the
+      // bitmap when no frontier vertex is big, else Dense2sparse into light list / chunks
+      uint32_t* vbase = dir_done ? vis : vis;        // pull: the snapshot; push: updated in place
+      uint32_t* vnext = cur ? a.vis1 : a.vis0;       // bitmap the next level reads
+      uint32_t* frnext = (d & 1) ? a.xfr0 : a.xfr1;  // output of level d + 1
+      const unsigned long long wlo = a.wlo, whi = (unsigned long long)a.wlo + a.wcnt;
+      for (unsigned long long w = gtid; w < a.nwords; w += gsize) {
+        if (w >= wlo && w < whi) {
+          if (next == 0) frnext[w] = 0u;
+        } else {
+          vnext[w] = vbase[w] | frout[w];
+        }
+      }
+      if (next == 0 && sh.lvl[5] != 0) {
+        convert_phase<Off>(a, frout, nullptr, sel ? a.L1 : a.L0, sel ? a.H1 : a.H0, out, &sh.work);
+        if (!level_barrier(a.narrow, a.bar, a.status, epoch, (unsigned)a.ncta)) return;
+        read_level(out, sh);
+        nL = (unsigned)sh.lvl[3];
+        nH = (unsigned)sh.lvl[4];
+        nB = (unsigned)sh.lvl[6];
+      } else {
+        from_bits = next == 0;
+        if (!level_barrier(a.narrow, a.bar, a.status, epoch, (unsigned)a.ncta)) return;
+      }
+    } else if (dir == 1 && next == 0 && sh.lvl[5] == 0) {
       from_bits = true;  // every new frontier vertex is light: push straight from `fr`
     } else if (dir == 1 && next == 0) {
       // pull -> push with a high-degree vertex in the frontier: Dense2sparse into the
@@ -1212,7 +1434,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
       uint32_t* vnew = cur ? a.vis1 : a.vis0;
       uint32_t* vold = cur ? a.vis0 : a.vis1;
       convert_phase<Off>(a, vnew, vold, sel ? a.L1 : a.L0, sel ? a.H1 : a.H0, out, &sh.work);
-      if (!level_barrier(a.narrow, a.bar, a.status, epoch)) return;
+      if (!level_barrier(a.narrow, a.bar, a.status, epoch, (unsigned)a.ncta)) return;
       read_level(out, sh);
       nL = (unsigned)sh.lvl[3];
       nH = (unsigned)sh.lvl[4];
@@ -1222,12 +1444,18 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
     c_old = c_new;
     mf_last = mf;
   }
-  if (a.narrow && blockIdx.x == 0 && threadIdx.x == 0) a.bar->rs.done = 1;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (a.narrow && cta == 0 && threadIdx.x == 0) a.bar->rs.done = 1;
+  if (cta == 0 && threadIdx.x == 0) {
     a.status->levels = d;
     a.status->reached = reached;
   }
-  if (PARENTS && a.perm) {  // relabelled graph: internal parents -> caller ids (after the
+  if (D && a.nranks > 1) {
+    // no rank leaves while a peer may still read its own buffers for this BFS: a fast rank's
+    // next BFS writes into the peers' exchange buffers
+    if (!grid_barrier(a.bar, a.status, epoch, (unsigned)a.ncta)) return;
+    if (cta == 0) rank_rendezvous(a, a.xseq + 0xFFFFFFFFull);
+  }
+  if (!D && PARENTS && a.perm) {  // relabelled graph: internal parents -> caller ids (after
     for (unsigned long long i = gtid; i < (unsigned long long)a.n; i += gsize) {  // last barrier)
       const uint32_t p = a.parent[i];
       a.pout[a.perm[i]] = p == 0xFFFFFFFFu ? p : a.perm[p];
@@ -1235,25 +1463,57 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
   }
 }
 
+// One GPU: the whole grid runs one BFS; the arguments are a kernel parameter.
+template <typename Off, bool PARENTS>
+__global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
+  bfs_body<Off, PARENTS, false>(a);
+}
+
+// Multi-rank: `all` holds one argument block per rank of this launch, rank r running on the
+// CTAs [all[r].cta_base, all[r].cta_base + all[r].ncta).  One process per GPU launches with
+// nranks = 1 (the whole grid); a single-device team launches its P ranks as P CTA groups of
+// one cooperative launch, so every rank is co-resident and the cross-rank flags cannot
+// deadlock.
+template <typename Off, bool PARENTS>
+__global__ void __launch_bounds__(kBfsBlock, 1) bfs_ranks(const BfsArgs<Off>* __restrict__ all,
+                                                          int nranks) {
+  __shared__ BfsArgs<Off> sa;
+  if (threadIdx.x == 0) {
+    int r = 0;
+    while (r + 1 < nranks && (int)blockIdx.x >= all[r + 1].cta_base) ++r;
+    sa = all[r];
+  }
+  __syncthreads();
+  bfs_body<Off, PARENTS, true>(sa);
+}
+
 template <typename Off>
 constexpr size_t dyn_smem_bytes() {
   return sizeof(ResidualQ<Off>) * kBfsWarps + sizeof(uint32_t) * kSumWordsMax;
 }
 
+// Cooperative grid size per (device, kernel) (and the dynamic shared-memory attribute, which
+// is per device too): computed once, guarded by a mutex.
+static int coop_grid(const void* fn, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find({dev, fn});
+  if (it != cache.end()) return it->second;
+  int sms = 0, per = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fn, kBfsBlock, smem);
+  const int g = sms * (per > 0 ? per : 1);
+  cache[{dev, fn}] = g;
+  return g;
+}
+
 template <typename Off, bool PARENTS>
 static int grid_for() {
-  static int cached = -1;
-  if (cached < 0) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(bfs_persistent<Off, PARENTS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)dyn_smem_bytes<Off>());
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, bfs_persistent<Off, PARENTS>, kBfsBlock,
-                                                  dyn_smem_bytes<Off>());
-    cached = sms * (per > 0 ? per : 1);
-  }
-  return cached;
+  return coop_grid((const void*)bfs_persistent<Off, PARENTS>, dyn_smem_bytes<Off>());
 }
 
 int bfs_grid_size(pp_graph g, bool parents) {
@@ -1262,8 +1522,10 @@ int bfs_grid_size(pp_graph g, bool parents) {
 }
 
 template <typename Off, bool PARENTS>
-static cudaError_t launch_t(pp_graph g, const BfsArgs<Off>& args) {
+static cudaError_t launch_t(pp_graph g, BfsArgs<Off> args) {
   const int grid = grid_for<Off, PARENTS>();
+  args.cta_base = 0;
+  args.ncta = grid;
   void* params[] = {(void*)&args};
   g->ctx->launches += 1;
   return cudaLaunchCooperativeKernel((const void*)bfs_persistent<Off, PARENTS>, dim3(grid),
@@ -1275,7 +1537,9 @@ static cudaError_t launch_t(pp_graph g, const BfsArgs<Off>& args) {
 // they stay small, then hands the loop state to the cooperative whole-grid launch queued
 // right behind it on the stream (which returns at once if the cluster finished the BFS).
 template <typename Off, bool PARENTS>
-static cudaError_t launch_narrow(pp_graph g, const BfsArgs<Off>& args) {
+static cudaError_t launch_narrow(pp_graph g, BfsArgs<Off> args) {
+  args.cta_base = 0;
+  args.ncta = kNarrowCtas;
   (void)grid_for<Off, PARENTS>();  // sets the dynamic shared memory attribute
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kNarrowCtas);
@@ -1309,6 +1573,7 @@ static cudaError_t launch_off(pp_graph g, uint32_t source, int mode, int rule, d
                               double beta, uint32_t toggles, int32_t* depth, uint32_t* parent,
                               int max_levels) {
   BfsArgs<Off> a;
+  memset(&a, 0, sizeof(a));
   a.n = g->n;
   a.nnz = g->nnz;
   a.nwords = g->nwords;
@@ -1371,5 +1636,103 @@ cudaError_t launch_bfs(pp_graph g, uint32_t source, int mode, int rule, double a
   return launch_off<uint32_t>(g, source, mode, rule, alpha, beta, toggles, depth, parent,
                               max_levels);
 }
+
+}  // namespace pp
+
+namespace pp {
+
+template <typename Off, bool PARENTS>
+static cudaError_t launch_ranks_t(pp_graph* gs, int P, uint32_t source, int mode, int rule,
+                                  double alpha, double beta, int32_t* const* depth,
+                                  uint32_t* const* parent) {
+  pp_graph g0 = gs[0];
+  const void* fn = (const void*)bfs_ranks<Off, PARENTS>;
+  const int grid = coop_grid(fn, dyn_smem_bytes<Off>());
+  if (grid < P) return cudaErrorInvalidConfiguration;
+  BfsArgs<Off> h[kMaxRanks];
+  memset(h, 0, sizeof(h));
+  for (int r = 0; r < P; ++r) {
+    pp_graph g = gs[r];
+    BfsArgs<Off>& a = h[r];
+    a.n = g->n;
+    a.nnz = g->nnz;
+    a.nwords = g->nwords;
+    a.off = (const Off*)g->off;
+    a.idx = g->idx;
+    a.coff = (const Off*)g->coff;
+    a.cidx = g->cidx;
+    a.symmetric = g->symmetric ? 1 : 0;
+    a.isolated = g->isolated;
+    a.vis0 = g->vis[0];
+    a.vis1 = g->vis[1];
+    a.fr = g->xfr[0];
+    a.head = g->head;
+    a.sumv = nullptr;
+    a.sum_shift = 3;
+    a.sum_words = 0;
+    a.L0 = reinterpret_cast<uint4*>(g->L[0]);
+    a.L1 = reinterpret_cast<uint4*>(g->L[1]);
+    a.H0 = g->H[0];
+    a.H1 = g->H[1];
+    a.hcap = (unsigned)g->hcap;
+    a.depth = depth[r];
+    a.parent = parent ? parent[r] : nullptr;
+    a.pout = a.parent;
+    a.ctr = g->ctr;
+    a.stats = g->stats;
+    a.stats_cap = g->stats_cap;
+    a.bar = g->bar;
+    a.status = g->status;
+    a.source = source;
+    a.mode = mode;
+    a.rule = rule;
+    a.alpha = alpha;
+    a.beta = beta;
+    a.toggles = 0;
+    a.max_levels = (int)std::min<int64_t>(g->n + 1, 0x7FFFFFFF);
+    a.cta_base = (int)((int64_t)r * grid / P);
+    a.ncta = (int)((int64_t)(r + 1) * grid / P) - a.cta_base;
+    a.lo = g->row_lo;
+    a.hi = g->row_hi;
+    a.wlo = (uint32_t)(g->me * g->chunk_words);
+    a.wcnt = (uint32_t)g->chunk_words;
+    a.me = g->me;
+    a.nranks = g->nranks;
+    a.xfr0 = g->xfr[0];
+    a.xfr1 = g->xfr[1];
+    a.xcnt = g->xcnt;
+    a.xflag = g->xflag;
+    for (int q = 0; q < kMaxRanks; ++q) {
+      a.pfr[q][0] = g->pfr[q][0];
+      a.pfr[q][1] = g->pfr[q][1];
+      a.pcnt[q] = g->pcnt[q];
+      a.pflag[q] = g->pflag[q];
+    }
+    g->xseq += 1;  // identical on every rank: pp_bfs is collective
+    a.xseq = g->xseq << 32;
+    a.odeg = g->odeg;
+    a.in_total = g->in_total;
+  }
+  cudaStream_t st = g0->ctx->stream;
+  // pageable source: the runtime stages it before returning, so `h` may go out of scope
+  cudaError_t e = cudaMemcpyAsync(g0->dargs, h, sizeof(BfsArgs<Off>) * P, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  const BfsArgs<Off>* dall = (const BfsArgs<Off>*)g0->dargs;
+  void* params[] = {(void*)&dall, (void*)&P};
+  g0->ctx->launches += 1;
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBfsBlock), params, dyn_smem_bytes<Off>(), st);
+}
+
+cudaError_t launch_bfs_ranks(pp_graph* graphs, int nranks, uint32_t source, int mode, int rule,
+                             double alpha, double beta, int32_t* const* depth,
+                             uint32_t* const* parent) {
+  if (graphs[0]->off64)
+    return parent ? launch_ranks_t<uint64_t, true>(graphs, nranks, source, mode, rule, alpha, beta, depth, parent)
+                  : launch_ranks_t<uint64_t, false>(graphs, nranks, source, mode, rule, alpha, beta, depth, parent);
+  return parent ? launch_ranks_t<uint32_t, true>(graphs, nranks, source, mode, rule, alpha, beta, depth, parent)
+                : launch_ranks_t<uint32_t, false>(graphs, nranks, source, mode, rule, alpha, beta, depth, parent);
+}
+
+size_t bfs_args_bytes() { return sizeof(BfsArgs<uint64_t>) * kMaxRanks; }
 
 }  // namespace pp

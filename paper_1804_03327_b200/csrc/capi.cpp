@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "pp_internal.h"
 
@@ -69,18 +70,23 @@ bool is_device_ptr(const void* p) {
 
 void free_graph(pp_graph g) {
   if (!g) return;
-  void* ptrs[] = {g->off, g->idx, g->symmetric ? nullptr : g->coff,
-                  g->symmetric ? nullptr : (void*)g->cidx, g->isolated, g->head, g->vis[0], g->vis[1], g->fr, g->sumv,
+  // multi-rank: unmap the peers' exchange buffers first (CUDA IPC, multi-process only)
+  for (int q = 0; q < kMaxRanks; ++q)
+    if (g->ipc_base[q]) cudaIpcCloseMemHandle(g->ipc_base[q]);
+  const bool alias = g->dist ? false : g->symmetric;  // multi-rank: coff/off are distinct
+  void* ptrs[] = {g->off, g->idx, alias ? nullptr : g->coff,
+                  (alias || g->cidx == g->idx) ? nullptr : (void*)g->cidx, g->isolated, g->head,
+                  g->vis[0], g->vis[1], g->fr, g->sumv,
                   g->L[0], g->L[1], g->H[0], g->H[1], g->ctr, g->stats, g->bar,
                   g->sbits[0], g->sbits[1], g->sbits[2], g->sbits[3], g->sblock, g->hubq, g->scount,
                   g->dtmp[0], g->dtmp[1], g->dbg, g->perm, g->rank, g->pint, g->vrec,
                   g->rbits[0], g->rbits[1], g->rbits[2], g->rbits[3],
-                  g->dvis, g->dfr, g->dnxt, g->diso, g->pbeg, g->pend, g->dcnt};
+                  g->odeg, g->xbuf, g->dargs};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (g->status_host) cudaFreeHost(g->status_host);
   if (g->scount_host) cudaFreeHost(g->scount_host);
-  if (g->dcnt_host) cudaFreeHost(g->dcnt_host);
+  if (g->hargs) cudaFreeHost(g->hargs);
   delete g;
 }
 
@@ -88,6 +94,257 @@ struct Guard {  // frees a half-built graph on early return
   pp_graph g;
   ~Guard() { free_graph(g); }
 };
+
+// ---- multi-rank residency (dist.cu) -----------------------------------------
+// Layout of the exchange buffer every peer writes into (identical on every rank).
+struct XLayout {
+  size_t fr0, fr1, cnt, flag, bytes;
+};
+XLayout xlayout(int64_t nwords) {
+  XLayout L;
+  const size_t fb = sizeof(uint32_t) * (size_t)nwords;  // multiple of 128 bytes
+  L.fr0 = 0;
+  L.fr1 = fb;
+  L.cnt = 2 * fb;
+  L.flag = L.cnt + sizeof(unsigned long long) * 2 * kMaxRanks * 4;
+  L.bytes = L.flag + sizeof(unsigned long long) * kMaxRanks;
+  return L;
+}
+
+void set_peer(pp_graph g, int q, char* base, const XLayout& L) {
+  g->pfr[q][0] = (uint32_t*)(base + L.fr0);
+  g->pfr[q][1] = (uint32_t*)(base + L.fr1);
+  g->pcnt[q] = (unsigned long long*)(base + L.cnt);
+  g->pflag[q] = (unsigned long long*)(base + L.flag);
+}
+
+// Bootstrap record of one rank (all-gathered over the NCCL communicator).
+struct BootRec {
+  cudaIpcMemHandle_t h;  // 64 bytes: the rank's exchange buffer
+  int64_t n, lo, hi, nnz;
+  int32_t rank, nranks, off64, symmetric;
+  char pad[16];
+};
+static_assert(sizeof(BootRec) == 128, "BootRec layout");
+
+// Multi-process: map every peer's exchange buffer (CUDA IPC over NVLink) and check that the
+// ranks agree on the graph and tile it.
+pp_status bootstrap_ipc(pp_graph g) {
+  pp_ctx ctx = g->ctx;
+  const int P = ctx->nranks;
+  BootRec me;
+  memset(&me, 0, sizeof(me));
+  if (P > 1) PP_CK(cudaIpcGetMemHandle(&me.h, g->xbuf), "cudaIpcGetMemHandle");
+  me.n = g->n;
+  me.lo = g->row_lo;
+  me.hi = g->row_hi;
+  me.nnz = g->nnz;
+  me.rank = ctx->rank;
+  me.nranks = P;
+  me.off64 = g->off64 ? 1 : 0;
+  me.symmetric = g->symmetric ? 1 : 0;
+  BootRec all[kMaxRanks];
+  const char* why = "";
+  if (P > 1 || ctx->comm) {
+    if (!ctx->comm) PP_FAIL(PP_ERR_NCCL, "pp_graph_upload: multi-rank context without a communicator");
+    const int rc = nccl_allgather_host(ctx->comm, &me, all, sizeof(BootRec), P, ctx->stream, &why);
+    if (rc != 0) PP_FAIL(rc == -2 ? PP_ERR_NCCL : PP_ERR_CUDA, "pp_graph_upload: bootstrap: %s", why);
+  } else {
+    all[0] = me;
+  }
+  const XLayout L = xlayout(g->nwords);
+  int64_t in_total = 0;
+  for (int q = 0; q < P; ++q) {
+    const BootRec& r = all[q];
+    int64_t lo, hi, cw;
+    partition(g->n, q, P, &lo, &hi, &cw);
+    if (r.n != g->n || r.rank != q || r.nranks != P || r.lo != lo || r.hi != hi ||
+        r.off64 != me.off64 || r.symmetric != me.symmetric)
+      PP_FAIL(PP_ERR_ARG, "pp_graph_upload: rank %d disagrees on the graph or its block (n=%lld, "
+              "rows [%lld, %lld), offsets %s, %s)", q, (long long)r.n, (long long)r.lo,
+              (long long)r.hi, r.off64 ? "64-bit" : "32-bit", r.symmetric ? "symmetric" : "directed");
+    in_total += r.nnz;
+    if (q == ctx->rank) continue;
+    void* base = nullptr;
+    PP_CK(cudaIpcOpenMemHandle(&base, r.h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    g->ipc_base[q] = base;
+    set_peer(g, q, (char*)base, L);
+  }
+  g->in_total = in_total;
+  return PP_OK;
+}
+
+// pp_graph_upload on a multi-rank context: the rank's CSR / CSC rows [row_lo, row_hi) with
+// global column ids (offsets row-local: row_hi - row_lo + 1 entries starting at 0).
+pp_status upload_block(pp_ctx ctx, int64_t n, int64_t row_lo, int64_t row_hi, int64_t nnz,
+                       const int64_t* csr_off, const uint32_t* csr_idx, const int64_t* csc_off,
+                       const uint32_t* csc_idx, uint32_t flags, pp_graph* out) {
+  const bool symmetric = (flags & PP_GRAPH_SYMMETRIC) != 0;
+  if (flags & PP_GRAPH_RELABEL)
+    PP_FAIL(PP_ERR_UNSUPPORTED, "pp_graph_upload: PP_GRAPH_RELABEL is single-GPU only");
+  if (ctx->nranks > kMaxRanks)
+    PP_FAIL(PP_ERR_UNSUPPORTED, "pp_graph_upload: %d ranks (at most %d)", ctx->nranks, kMaxRanks);
+  if (n < 1 || n >= (int64_t)0xFFFFFFFFll)
+    PP_FAIL(PP_ERR_UNSUPPORTED, "pp_graph_upload: n=%lld outside [1, 2^32-1)", (long long)n);
+  int64_t lo, hi, cw;
+  partition(n, ctx->rank, ctx->nranks, &lo, &hi, &cw);
+  if (row_lo != lo || row_hi != hi)
+    PP_FAIL(PP_ERR_ARG, "pp_graph_upload: rank %d of %d owns rows [%lld, %lld) (pp_partition), got "
+            "[%lld, %lld)", ctx->rank, ctx->nranks, (long long)lo, (long long)hi,
+            (long long)row_lo, (long long)row_hi);
+  if (symmetric) {
+    csc_off = csr_off;
+    csc_idx = csr_idx;
+  }
+  if (!csc_off) PP_FAIL(PP_ERR_ARG, "pp_graph_upload: CSC rows required unless PP_GRAPH_SYMMETRIC");
+  const int64_t len = hi - lo;
+  PP_CK(cudaSetDevice(ctx->device), "cudaSetDevice");
+  cudaStream_t st = ctx->stream;
+  pp_graph g = new pp_graph_s;
+  Guard guard{g};
+  g->ctx = ctx;
+  g->dist = true;
+  g->n = n;
+  g->symmetric = symmetric;
+  g->me = ctx->rank;
+  g->nranks = ctx->nranks;
+  g->row_lo = lo;
+  g->row_hi = hi;
+  g->chunk_words = cw;
+  g->nwords = (uint32_t)(cw * ctx->nranks);
+  int64_t& bytes = g->device_bytes;
+  pp_status s;
+  const bool dev = (flags & PP_GRAPH_DEVICE) != 0;
+  int64_t junk = 0;
+  // block offsets staged as int64 on the device
+  if ((s = dalloc(&g->dtmp[0], (size_t)(len + 1) * 2, &junk, "offset staging")) != PP_OK) return s;
+  int64_t* d_off = g->dtmp[0];
+  int64_t* d_coff = g->dtmp[0] + (len + 1);
+  PP_CK(cudaMemcpyAsync(d_off, csr_off, sizeof(int64_t) * (len + 1),
+                        dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st), "copy offsets");
+  PP_CK(cudaMemcpyAsync(d_coff, csc_off, sizeof(int64_t) * (len + 1),
+                        dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st), "copy offsets");
+  int64_t ends[4];
+  PP_CK(cudaMemcpyAsync(&ends[0], d_off, 8, cudaMemcpyDeviceToHost, st), "read off[0]");
+  PP_CK(cudaMemcpyAsync(&ends[1], d_off + len, 8, cudaMemcpyDeviceToHost, st), "read off[len]");
+  PP_CK(cudaMemcpyAsync(&ends[2], d_coff, 8, cudaMemcpyDeviceToHost, st), "read coff[0]");
+  PP_CK(cudaMemcpyAsync(&ends[3], d_coff + len, 8, cudaMemcpyDeviceToHost, st), "read coff[len]");
+  PP_CK(cudaStreamSynchronize(st), "sync");
+  if (ends[0] != 0 || ends[1] != nnz)
+    PP_FAIL(PP_ERR_GRAPH, "pp_graph_upload: CSR block off[0]=%lld off[len]=%lld, expected 0 and nnz=%lld",
+            (long long)ends[0], (long long)ends[1], (long long)nnz);
+  const int64_t m = ends[3];  // in-edges of the block (CSC entries)
+  if (ends[2] != 0 || m < 0) PP_FAIL(PP_ERR_GRAPH, "pp_graph_upload: CSC block offsets malformed");
+  if (m > 0 && !csc_idx) PP_FAIL(PP_ERR_ARG, "pp_graph_upload: CSC ids missing");
+  g->nnz = m;
+  g->off64 = m >= (int64_t)0xFFFFFFFFll || (flags & PP_GRAPH_OFF64);
+  if ((s = dalloc(&g->cidx, (size_t)m + 8, &bytes, "csc idx")) != PP_OK) return s;
+  PP_CK(cudaMemsetAsync(g->cidx + m, 0, 8 * sizeof(uint32_t), st), "pad csc idx");
+  if (m) PP_CK(cudaMemcpyAsync(g->cidx, csc_idx, sizeof(uint32_t) * m, cudaMemcpyDefault, st), "copy csc idx");
+  if ((s = dalloc(&g->scount, 8, &bytes, "counters")) != PP_OK) return s;
+  PP_CK(cudaMallocHost((void**)&g->scount_host, 8 * sizeof(unsigned long long)), "pinned counters");
+  PP_CK(cudaMallocHost((void**)&g->status_host, sizeof(BfsStatus)), "pinned status");
+  if (flags & PP_GRAPH_VALIDATE) {
+    PP_CK(cudaMemsetAsync(g->scount, 0xFF, sizeof(unsigned long long), st), "memset");
+    PP_CK(launch_graph_validate(g, d_coff, g->cidx, g->scount, &ctx->launches, len), "validate");
+    PP_CK(cudaMemcpyAsync(g->scount_host, g->scount, 8, cudaMemcpyDeviceToHost, st), "copy");
+    PP_CK(cudaStreamSynchronize(st), "sync");
+    if (g->scount_host[0] != ~0ull)
+      PP_FAIL(PP_ERR_GRAPH, "pp_graph_upload: CSC row %llu of the block is malformed (offsets "
+              "decrease, an id >= n, or the row is not strictly increasing)",
+              (unsigned long long)(g->scount_host[0] + (unsigned long long)lo));
+  }
+  const size_t offb = g->off64 ? 8 : 4;
+  // CSC rows of the block (pull), narrowed offsets padded like the single-GPU layout
+  {
+    void* p = nullptr;
+    const size_t cnt = (size_t)cw * 32 + 16;
+    PP_CK(cudaMalloc(&p, offb * cnt), "block offsets");
+    PP_CK(cudaMemsetAsync(p, 0, offb * cnt, st), "memset");
+    g->coff = p;
+    bytes += (int64_t)(offb * cnt);
+    PP_CK(launch_off_narrow(g, d_coff, g->coff, len + 1), "narrow offsets");
+    // rows past the block end keep offset m (empty rows; they are padding, pre-visited)
+    if (cnt > (size_t)(len + 1)) {
+      // fill the tail with m so coff[r+1]-coff[r] = 0 there
+      std::vector<char> tail(offb * (cnt - (size_t)(len + 1)));
+      for (size_t k = 0; k < cnt - (size_t)(len + 1); ++k) {
+        if (offb == 8) reinterpret_cast<uint64_t*>(tail.data())[k] = (uint64_t)m;
+        else reinterpret_cast<uint32_t*>(tail.data())[k] = (uint32_t)m;
+      }
+      PP_CK(cudaMemcpyAsync((char*)p + offb * (len + 1), tail.data(), tail.size(),
+                            cudaMemcpyHostToDevice, st), "offsets tail");
+      PP_CK(cudaStreamSynchronize(st), "sync");
+    }
+  }
+  if ((s = dalloc(&g->head, (size_t)std::max<int64_t>(len, 1) * 8, &bytes, "row heads")) != PP_OK) return s;
+  PP_CK(launch_head(g, d_coff, g->cidx, len), "row heads");
+  if ((s = dalloc(&g->isolated, g->nwords, &bytes, "isolated")) != PP_OK) return s;
+  PP_CK(cudaMemsetAsync(g->isolated, 0, sizeof(uint32_t) * g->nwords, st), "memset");
+  if (!symmetric && (s = dalloc(&g->odeg, (size_t)std::max<int64_t>(len, 1), &bytes, "out-degrees")) != PP_OK)
+    return s;
+  PP_CK(launch_block_prepare(g, d_off, d_coff, len), "block prepare");
+  // push structure: transpose of the CSC block (global rows u, owned targets)
+  {
+    int64_t* poff64 = nullptr;
+    if ((s = dalloc(&poff64, (size_t)n + 1, &junk, "push offsets staging")) != PP_OK) return s;
+    g->dtmp[1] = poff64;
+    if ((s = dalloc(&g->idx, (size_t)m + 8, &bytes, "push ids")) != PP_OK) return s;
+    PP_CK(cudaMemsetAsync(g->idx + m, 0, 8 * sizeof(uint32_t), st), "pad push ids");
+    PP_CK(launch_push_structure(g, d_coff, len, m, poff64, g->idx), "push structure");
+    void* p = nullptr;
+    const size_t cnt = (size_t)g->nwords * 32 + 16;
+    PP_CK(cudaMalloc(&p, offb * cnt), "push offsets");
+    PP_CK(cudaMemsetAsync(p, 0, offb * cnt, st), "memset");
+    g->off = p;
+    bytes += (int64_t)(offb * cnt);
+    PP_CK(launch_off_narrow(g, poff64, g->off, n + 1), "narrow push offsets");
+    PP_CK(cudaMemsetAsync(g->scount, 0, 4 * sizeof(unsigned long long), st), "memset");
+    PP_CK(launch_hcap(g, poff64, n, g->scount, g->scount + 2), "chunk capacity");
+    PP_CK(cudaMemcpyAsync(g->scount_host, g->scount, 32, cudaMemcpyDeviceToHost, st), "copy");
+    PP_CK(cudaStreamSynchronize(st), "sync");
+    g->hcap = (int64_t)g->scount_host[0];
+    g->max_out_deg = (int64_t)g->scount_host[2];
+    cudaFree(poff64);
+    g->dtmp[1] = nullptr;
+  }
+  cudaFree(g->dtmp[0]);
+  g->dtmp[0] = nullptr;
+  // working set: replicated bitmaps, local frontier lists, exchange buffer
+  for (int k = 0; k < 2; ++k) {
+    if ((s = dalloc(&g->vis[k], g->nwords, &bytes, "visited")) != PP_OK) return s;
+    if ((s = dalloc(&g->L[k], (size_t)n * 4, &bytes, "frontier list")) != PP_OK) return s;
+    if ((s = dalloc(&g->H[k], (size_t)std::max<int64_t>(g->hcap, 1), &bytes, "heavy chunks")) != PP_OK)
+      return s;
+  }
+  if ((s = dalloc(&g->ctr, kRing, &bytes, "level counters")) != PP_OK) return s;
+  g->stats_cap = (int)std::min<int64_t>(n + 1, 1 << 16);
+  if ((s = dalloc(&g->stats, (size_t)g->stats_cap, &bytes, "level stats")) != PP_OK) return s;
+  if ((s = dalloc(&g->bar, 2, &bytes, "barrier")) != PP_OK) return s;
+  g->status = reinterpret_cast<BfsStatus*>(g->bar + 1);
+  PP_CK(cudaMemsetAsync(g->bar, 0, sizeof(GridBarrier) * 2, st), "memset");
+  const XLayout L = xlayout(g->nwords);
+  PP_CK(cudaMalloc(&g->xbuf, L.bytes), "exchange buffer");
+  bytes += (int64_t)L.bytes;
+  PP_CK(cudaMemsetAsync(g->xbuf, 0, L.bytes, st), "memset exchange buffer");
+  g->xfr[0] = (uint32_t*)((char*)g->xbuf + L.fr0);
+  g->xfr[1] = (uint32_t*)((char*)g->xbuf + L.fr1);
+  g->xcnt = (unsigned long long*)((char*)g->xbuf + L.cnt);
+  g->xflag = (unsigned long long*)((char*)g->xbuf + L.flag);
+  set_peer(g, g->me, (char*)g->xbuf, L);
+  PP_CK(cudaMalloc(&g->dargs, bfs_args_bytes()), "kernel arguments");
+  PP_CK(cudaStreamSynchronize(st), "sync");
+  g->in_total = m;
+  if (!ctx->team) {  // one process per GPU: map the peers now (collective)
+    if ((s = bootstrap_ipc(g)) != PP_OK) return s;
+  } else {
+    ctx->team->graphs[ctx->rank] = g;
+  }
+  guard.g = nullptr;
+  ctx->refs += 1;
+  *out = g;
+  return PP_OK;
+}
 
 }  // namespace
 
@@ -126,7 +383,12 @@ pp_status pp_ctx_create(int device, void* cuda_stream, pp_ctx* out) {
 
 static void ctx_release(pp_ctx ctx) {
   if (--ctx->refs == 0) {
+    if (ctx->team && --ctx->team->refs == 0) delete ctx->team;
     if (ctx->comm) nccl_comm_destroy(ctx->comm);
+    if (ctx->sssp_ws) {
+      cudaSetDevice(ctx->device);
+      cudaFree(ctx->sssp_ws);
+    }
     delete ctx;
   }
 }
@@ -178,12 +440,17 @@ pp_status pp_ctx_launch_count(pp_ctx ctx, uint64_t* out) {
   return PP_OK;
 }
 
-pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr_off,
-                          const uint32_t* csr_idx, const int64_t* csc_off,
+pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t row_lo, int64_t row_hi, int64_t nnz,
+                          const int64_t* csr_off, const uint32_t* csr_idx, const int64_t* csc_off,
                           const uint32_t* csc_idx, uint32_t flags, pp_graph* out) {
   if (!ctx || !out || !csr_off || (nnz > 0 && !csr_idx))
     PP_FAIL(PP_ERR_ARG, "pp_graph_upload: NULL argument");
   *out = nullptr;
+  if (ctx->nranks > 0)
+    return upload_block(ctx, n, row_lo, row_hi, nnz, csr_off, csr_idx, csc_off, csc_idx, flags, out);
+  if (row_lo != 0 || row_hi != n)
+    PP_FAIL(PP_ERR_ARG, "pp_graph_upload: rows [%lld, %lld) on a single-GPU context (must be [0, n))",
+            (long long)row_lo, (long long)row_hi);
   const bool symmetric = (flags & PP_GRAPH_SYMMETRIC) != 0;
   if (!symmetric && (!csc_off || (nnz > 0 && !csc_idx)))
     PP_FAIL(PP_ERR_ARG, "pp_graph_upload: CSC required unless PP_GRAPH_SYMMETRIC");
@@ -203,7 +470,7 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr
   g->n = n;
   g->nnz = nnz;
   g->symmetric = symmetric;
-  g->off64 = nnz >= (int64_t)0xFFFFFFFFll;
+  g->off64 = nnz >= (int64_t)0xFFFFFFFFll || (flags & PP_GRAPH_OFF64);
   const int64_t words = (n + 31) / 32;
   g->nwords = (uint32_t)(((words + 31) / 32) * 32);
   int64_t& bytes = g->device_bytes;
@@ -280,8 +547,6 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr
   // optional degree-ordered relabelling (relabel.cu): rows renumbered and re-sorted; the
   // prepare kernels below then see only internal ids
   if (flags & PP_GRAPH_RELABEL) {
-    if (ctx->nranks > 0)
-      PP_FAIL(PP_ERR_UNSUPPORTED, "pp_graph_upload: PP_GRAPH_RELABEL is single-GPU only");
     if (nnz >= (int64_t)0x7FFFFFFF || n >= (int64_t)0x7FFFFFFF)
       PP_FAIL(PP_ERR_UNSUPPORTED, "pp_graph_upload: PP_GRAPH_RELABEL needs nnz, n < 2^31");
     if ((s = dalloc(&g->perm, (size_t)n, &bytes, "relabel perm")) != PP_OK) return s;
@@ -362,25 +627,6 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr
     g->dtmp[0] = nullptr;
   }
   g->bfs_grid = bfs_grid_size(g, false);
-  if (ctx->nranks > 0) {  // distributed context: owned block, replicated bitmaps, push ranges
-    partition(n, ctx->rank, ctx->nranks, &g->row_lo, &g->row_hi, &g->chunk_words);
-    g->dist_words = g->chunk_words * ctx->nranks;
-    const size_t W = (size_t)g->dist_words;
-    if ((s = dalloc(&g->dvis, W, &bytes, "dist visited")) != PP_OK) return s;
-    if ((s = dalloc(&g->dfr, W, &bytes, "dist frontier")) != PP_OK) return s;
-    if ((s = dalloc(&g->dnxt, W, &bytes, "dist next")) != PP_OK) return s;
-    if ((s = dalloc(&g->diso, W, &bytes, "dist isolated")) != PP_OK) return s;
-    PP_CK(cudaMemsetAsync(g->diso, 0xFF, sizeof(uint32_t) * W, st), "memset");
-    PP_CK(cudaMemcpyAsync(g->diso, g->isolated, sizeof(uint32_t) * std::min<size_t>(W, g->nwords),
-                          cudaMemcpyDeviceToDevice, st), "copy isolated");
-    PP_CK(cudaMalloc(&g->pbeg, offb * (size_t)n), "push ranges");
-    PP_CK(cudaMalloc(&g->pend, offb * (size_t)n), "push ranges");
-    bytes += (int64_t)(2 * offb * (size_t)n);
-    if ((s = dalloc(&g->dcnt, 4, &bytes, "dist counters")) != PP_OK) return s;
-    PP_CK(cudaMallocHost((void**)&g->dcnt_host, 4 * sizeof(unsigned long long)), "pinned");
-    PP_CK(launch_push_ranges(g), "push ranges kernel");
-    PP_CK(cudaStreamSynchronize(st), "sync");
-  }
   guard.g = nullptr;
   ctx->refs += 1;
   *out = g;
@@ -390,6 +636,7 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* csr
 pp_status pp_graph_free(pp_graph g) {
   if (!g) PP_FAIL(PP_ERR_ARG, "pp_graph_free: NULL graph");
   pp_ctx ctx = g->ctx;
+  if (ctx->team && ctx->team->graphs[ctx->rank] == g) ctx->team->graphs[ctx->rank] = nullptr;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   free_graph(g);
@@ -399,8 +646,34 @@ pp_status pp_graph_free(pp_graph g) {
 
 pp_status pp_graph_partition(pp_graph g, int64_t* row_lo, int64_t* row_hi) {
   if (!g || !row_lo || !row_hi) PP_FAIL(PP_ERR_ARG, "pp_graph_partition: NULL argument");
-  *row_lo = g->ctx->nranks ? g->row_lo : 0;
-  *row_hi = g->ctx->nranks ? g->row_hi : g->n;
+  *row_lo = g->dist ? g->row_lo : 0;
+  *row_hi = g->dist ? g->row_hi : g->n;
+  return PP_OK;
+}
+
+pp_status pp_team_create(int device, void* cuda_stream, int32_t nranks, pp_ctx* ctxs) {
+  if (!ctxs || nranks < 1 || nranks > kMaxRanks)
+    PP_FAIL(PP_ERR_ARG, "pp_team_create: nranks %d outside [1, %d]", nranks, kMaxRanks);
+  pp_team_s* t = new pp_team_s;
+  t->device = device;
+  t->nranks = nranks;
+  for (int r = 0; r < nranks; ++r) {
+    pp_status s = pp_ctx_create(device, cuda_stream, &ctxs[r]);
+    if (s != PP_OK) {
+      for (int q = 0; q < r; ++q) {
+        ctxs[q]->team = nullptr;
+        delete ctxs[q];
+        ctxs[q] = nullptr;
+      }
+      delete t;
+      return s;
+    }
+    ctxs[r]->rank = r;
+    ctxs[r]->nranks = nranks;
+    ctxs[r]->team = t;
+    t->ctx[r] = ctxs[r];
+    t->refs += 1;
+  }
   return PP_OK;
 }
 
@@ -446,13 +719,14 @@ static pp_status check_vec(const pp_vector* v, int64_t n, const char* name) {
     PP_FAIL(PP_ERR_DIM, "pp_mxv: %s has unknown format %d", name, v->format);
   if (!v->data && !(v->format == PP_VEC_LIST && v->nnz == 0 && v->capacity == 0))
     PP_FAIL(PP_ERR_ARG, "pp_mxv: %s data is NULL", name);
-  if (v->format == PP_VEC_LIST && (v->nnz < 0 || v->nnz > std::max<int64_t>(v->capacity, v->nnz)))
+  if (v->format == PP_VEC_LIST && (v->nnz < 0 || v->nnz > v->capacity))
     PP_FAIL(PP_ERR_DIM, "pp_mxv: %s list nnz=%lld invalid", name, (long long)v->nnz);
   return PP_OK;
 }
 
 pp_status pp_mxv(pp_graph g, pp_vector* w, const pp_descriptor* desc, const pp_vector* u) {
   if (!g || !desc) PP_FAIL(PP_ERR_ARG, "pp_mxv: NULL graph or descriptor");
+  if (g->dist) PP_FAIL(PP_ERR_UNSUPPORTED, "pp_mxv: multi-rank graphs run pp_bfs only");
   pp_status s;
   if ((s = check_vec(u, g->n, "u")) != PP_OK) return s;
   if ((s = check_vec(w, g->n, "w")) != PP_OK) return s;
@@ -561,7 +835,7 @@ pp_status pp_mxv(pp_graph g, pp_vector* w, const pp_descriptor* desc, const pp_v
     PP_CK(cudaMemcpyAsync(g->scount_host, g->scount, 24, cudaMemcpyDeviceToHost, st), "copy");
     PP_CK(cudaStreamSynchronize(st), "sync");
     if (g->scount_host[2] != ~0ull)
-      PP_FAIL(PP_ERR_RANGE, "pp_mxv: input list entry %llu holds an id >= n",
+      PP_FAIL(PP_ERR_RANGE, "pp_mxv: input list entry %llu holds an id >= n or breaks the strictly increasing order",
               (unsigned long long)g->scount_host[2]);
     w->nnz = (int64_t)g->scount_host[0];
     if (w->format == PP_VEC_LIST && w->nnz > w->capacity)
@@ -569,6 +843,35 @@ pp_status pp_mxv(pp_graph g, pp_vector* w, const pp_descriptor* desc, const pp_v
               (long long)w->capacity);
   } else {
     w->nnz = -1;
+  }
+  return PP_OK;
+}
+
+// After a BFS launch: optional sync, device status check and the per-level stats.
+static pp_status finish_bfs(pp_graph g, pp_bfs_stats* stats, bool sync) {
+  cudaStream_t st = g->ctx->stream;
+  if (!sync) return PP_OK;
+  PP_CK(cudaMemcpyAsync(g->status_host, g->status, sizeof(BfsStatus), cudaMemcpyDeviceToHost, st),
+        "copy status");
+  PP_CK(cudaStreamSynchronize(st), "bfs sync");
+  if (g->status_host->error)
+    PP_FAIL((pp_status)g->status_host->error, "pp_bfs: device watchdog fired (barrier wait > 4 s)");
+  if (stats) {
+    stats->levels = g->status_host->levels;
+    stats->init_ns = g->status_host->t_init - g->status_host->t_start;
+    stats->reached = g->status_host->reached;
+    const int m = std::min(std::min(stats->capacity, g->status_host->levels), g->stats_cap);
+    if (m > 0) {
+      std::vector<LevelStat> hs((size_t)m);
+      PP_CK(cudaMemcpy(hs.data(), g->stats, sizeof(LevelStat) * m, cudaMemcpyDeviceToHost), "copy stats");
+      for (int k = 0; k < m; ++k) {
+        if (stats->ns) stats->ns[k] = hs[k].t_ns - (k ? hs[k - 1].t_ns : g->status_host->t_init);
+        if (stats->dir) stats->dir[k] = (int8_t)hs[k].dir;
+        if (stats->c) stats->c[k] = hs[k].c;
+        if (stats->m_f) stats->m_f[k] = hs[k].m_f;
+        if (stats->m_u) stats->m_u[k] = hs[k].m_u;
+      }
+    }
   }
   return PP_OK;
 }
@@ -608,40 +911,22 @@ pp_status pp_bfs(pp_graph g, int64_t source, const pp_bfs_options* opts, int32_t
       return s;
     d_parent = (uint32_t*)g->dtmp[1];
   }
-  if (g->ctx->nranks > 0 && o.toggles)
+  if (g->dist && o.toggles)
     PP_FAIL(PP_ERR_UNSUPPORTED, "pp_bfs: ablation toggles are single-GPU only");
-  if (g->ctx->nranks > 0) {  // collective 1D-partitioned BFS; depth/parent are block slices
-    const int cap = stats ? std::max(stats->capacity, 0) : 0;
-    DistLevel* lv = cap ? new DistLevel[cap] : nullptr;
-    int nlev = 0;
-    long long reached = 0;
-    const char* why = "";
-    const int rc = launch_bfs_dist(g, (uint32_t)source, o.mode, o.heuristic, alpha, beta, d_depth,
-                                   d_parent, lv, cap, &nlev, &reached, &why);
-    if (rc != 0) {
-      delete[] lv;
-      PP_FAIL(rc == -2 ? PP_ERR_NCCL : PP_ERR_CUDA, "pp_bfs (distributed): %s", why);
-    }
+  if (g->dist && g->ctx->team)
+    PP_FAIL(PP_ERR_ARG, "pp_bfs: a team member's graph runs through pp_bfs_team");
+  if (g->dist) {  // collective 1D-partitioned BFS; depth/parent are the block's slices
+    PP_CK(cudaMemsetAsync(g->bar, 0, sizeof(GridBarrier) + sizeof(BfsStatus), st), "memset control");
+    uint32_t* pp_ = (uint32_t*)d_parent;
+    PP_CK(launch_bfs_ranks(&g, 1, (uint32_t)source, o.mode, o.heuristic, alpha, beta, &d_depth,
+                           pp_ ? &pp_ : nullptr),
+          "bfs kernel launch");
     const int64_t len = g->row_hi - g->row_lo;
     if (host_depth && len)
       PP_CK(cudaMemcpyAsync(depth, d_depth, sizeof(int32_t) * len, cudaMemcpyDeviceToHost, st), "copy");
     if (host_parent && len)
       PP_CK(cudaMemcpyAsync(parent, d_parent, sizeof(int32_t) * len, cudaMemcpyDeviceToHost, st), "copy");
-    PP_CK(cudaStreamSynchronize(st), "sync");
-    if (stats) {
-      stats->levels = nlev;
-      stats->reached = reached;
-      stats->init_ns = 0;
-      for (int k = 0; k < std::min(cap, nlev); ++k) {
-        if (stats->dir) stats->dir[k] = (int8_t)lv[k].dir;
-        if (stats->c) stats->c[k] = lv[k].c;
-        if (stats->m_f) stats->m_f[k] = lv[k].m_f;
-        if (stats->m_u) stats->m_u[k] = lv[k].m_u;
-        if (stats->ns) stats->ns[k] = 0;
-      }
-    }
-    delete[] lv;
-    return PP_OK;
+    return finish_bfs(g, stats, stats || host_depth || host_parent);
   }
   PP_CK(cudaMemsetAsync(g->bar, 0, sizeof(GridBarrier) + sizeof(BfsStatus), st), "memset control");
   const int max_levels = (int)std::min<int64_t>(g->n + 1, 0x7FFFFFFF);
@@ -652,40 +937,73 @@ pp_status pp_bfs(pp_graph g, int64_t source, const pp_bfs_options* opts, int32_t
     PP_CK(cudaMemcpyAsync(depth, d_depth, sizeof(int32_t) * g->n, cudaMemcpyDeviceToHost, st), "copy depth");
   if (host_parent)
     PP_CK(cudaMemcpyAsync(parent, d_parent, sizeof(int32_t) * g->n, cudaMemcpyDeviceToHost, st), "copy parent");
-  if (stats || host_depth || host_parent) {
-    PP_CK(cudaMemcpyAsync(g->status_host, g->status, sizeof(BfsStatus), cudaMemcpyDeviceToHost, st),
-          "copy status");
-    PP_CK(cudaStreamSynchronize(st), "bfs sync");
-    if (g->status_host->error)
-      PP_FAIL((pp_status)g->status_host->error, "pp_bfs: device watchdog fired (grid barrier wait > 4 s)");
+  return finish_bfs(g, stats, stats || host_depth || host_parent);
+}
+
+pp_status pp_bfs_team(const pp_graph* graphs, int32_t nranks, int64_t source,
+                      const pp_bfs_options* opts, int32_t* const* depth, int32_t* const* parent,
+                      pp_bfs_stats* stats) {
+  if (!graphs || !depth || nranks < 1 || nranks > kMaxRanks)
+    PP_FAIL(PP_ERR_ARG, "pp_bfs_team: NULL argument or nranks %d outside [1, %d]", nranks, kMaxRanks);
+  pp_team_s* team = nullptr;
+  for (int r = 0; r < nranks; ++r) {
+    pp_graph g = graphs[r];
+    if (!g || !g->dist || !g->ctx->team || g->ctx->rank != r || !depth[r])
+      PP_FAIL(PP_ERR_ARG, "pp_bfs_team: graphs[%d] is not rank %d of a team (or depth[%d] is NULL)", r, r, r);
+    if (r == 0) team = g->ctx->team;
+    if (g->ctx->team != team || team->nranks != nranks || g->n != graphs[0]->n ||
+        g->off64 != graphs[0]->off64 || g->symmetric != graphs[0]->symmetric)
+      PP_FAIL(PP_ERR_ARG, "pp_bfs_team: graphs[%d] belongs to another team or graph", r);
+    if (!is_device_ptr(depth[r]) || (parent && parent[r] && !is_device_ptr(parent[r])))
+      PP_FAIL(PP_ERR_ARG, "pp_bfs_team: depth / parent slices must be device memory");
   }
-  if (stats) {
-    stats->levels = g->status_host->levels;
-    stats->init_ns = g->status_host->t_init - g->status_host->t_start;
-    stats->reached = g->status_host->reached;
-    const int m = std::min(std::min(stats->capacity, g->status_host->levels), g->stats_cap);
-    if (m > 0) {
-      LevelStat* hs = new LevelStat[m];
-      cudaError_t e = cudaMemcpy(hs, g->stats, sizeof(LevelStat) * m, cudaMemcpyDeviceToHost);
-      if (e != cudaSuccess) {
-        delete[] hs;
-        return cuda_fail(e, "copy stats");
-      }
-      for (int k = 0; k < m; ++k) {
-        if (stats->ns) stats->ns[k] = hs[k].t_ns - (k ? hs[k - 1].t_ns : g->status_host->t_init);
-        if (stats->dir) stats->dir[k] = (int8_t)hs[k].dir;
-        if (stats->c) stats->c[k] = hs[k].c;
-        if (stats->m_f) stats->m_f[k] = hs[k].m_f;
-        if (stats->m_u) stats->m_u[k] = hs[k].m_u;
-      }
-      delete[] hs;
-    }
+  pp_graph g0 = graphs[0];
+  if (source < 0 || source >= g0->n)
+    PP_FAIL(PP_ERR_RANGE, "pp_bfs_team: source %lld out of range [0, %lld)", (long long)source, (long long)g0->n);
+  pp_bfs_options o;
+  if (opts) o = *opts;
+  else pp_bfs_options_default(&o);
+  if (o.heuristic != PP_HEUR_EDGES && o.heuristic != PP_HEUR_PAPER_R)
+    PP_FAIL(PP_ERR_ARG, "pp_bfs_team: heuristic %d", o.heuristic);
+  if (o.mode < PP_MODE_DO || o.mode > PP_MODE_PULL_ONLY) PP_FAIL(PP_ERR_ARG, "pp_bfs_team: mode %d", o.mode);
+  if (o.toggles) PP_FAIL(PP_ERR_UNSUPPORTED, "pp_bfs_team: ablation toggles are single-GPU only");
+  double alpha = o.alpha, beta = o.beta;
+  if (alpha <= 0) alpha = (o.heuristic == PP_HEUR_EDGES) ? 15.0 : 0.01;
+  if (beta <= 0) beta = (o.heuristic == PP_HEUR_EDGES) ? 18.0 : 0.01;
+  const bool want_parents = o.want_parents && parent;
+  // the peers' exchange buffers are on this device: map them directly
+  const XLayout L = xlayout(g0->nwords);
+  int64_t in_total = 0;
+  for (int r = 0; r < nranks; ++r) in_total += graphs[r]->nnz;
+  for (int r = 0; r < nranks; ++r) {
+    for (int q = 0; q < nranks; ++q) set_peer(graphs[r], q, (char*)graphs[q]->xbuf, L);
+    graphs[r]->in_total = in_total;
   }
+  PP_CK(cudaSetDevice(g0->ctx->device), "cudaSetDevice");
+  cudaStream_t st = g0->ctx->stream;
+  for (int r = 0; r < nranks; ++r)
+    PP_CK(cudaMemsetAsync(graphs[r]->bar, 0, sizeof(GridBarrier) + sizeof(BfsStatus), st), "memset control");
+  std::vector<pp_graph> gs(graphs, graphs + nranks);
+  PP_CK(launch_bfs_ranks(gs.data(), nranks, (uint32_t)source, o.mode, o.heuristic, alpha, beta, depth,
+                         want_parents ? (uint32_t* const*)parent : nullptr),
+        "bfs kernel launch");
+  for (int r = 1; r < nranks; ++r) {  // every rank's status (each has its own watchdog)
+    pp_status s = finish_bfs(graphs[r], nullptr, true);
+    if (s != PP_OK) return s;
+  }
+  pp_status s = finish_bfs(g0, stats, true);
+  if (s != PP_OK) return s;
+  for (int r = 1; r < nranks; ++r)
+    if (graphs[r]->status_host->levels != g0->status_host->levels ||
+        graphs[r]->status_host->reached != g0->status_host->reached)
+      PP_FAIL(PP_ERR_CUDA, "pp_bfs_team: ranks disagree (levels %d vs %d)", graphs[r]->status_host->levels,
+              g0->status_host->levels);
   return PP_OK;
 }
 
 pp_status pp_bfs_debug_times(pp_graph g, int32_t levels, int64_t* out_ns, int32_t* nctas) {
   if (!g) PP_FAIL(PP_ERR_ARG, "pp_bfs_debug_times: NULL graph");
+  if (g->dist) PP_FAIL(PP_ERR_UNSUPPORTED, "pp_bfs_debug_times: single-GPU graphs only");
   PP_CK(cudaSetDevice(g->ctx->device), "cudaSetDevice");
   if (nctas) *nctas = g->bfs_grid;
   if (levels > 0 && !g->dbg) {

@@ -1,18 +1,29 @@
-// dist.cu — multi-GPU direction-optimised BFS over a 1D row partition (
-// the paper names distributed GPUs as future work).
+// dist.cu — multi-rank graph residency for the 1D row partition (the paper
+// names distributed GPUs as future work).  DESIGN.md §7.
 //
-// One process per GPU.  Rank p owns the vertex block [lo_p, hi_p) (boundaries aligned to
-// 1024 vertices = 32 bitmap words).  Every rank keeps the whole graph resident (s26 is
-// ~9 GB, far inside 180 GB) and, for push, the sub-range of every row's sorted ids that
-// falls inside its block, so a push expands the *global* frontier but discovers only owned
-// vertices (no all-to-all).  Pull scans owned unvisited rows against the replicated
-// visited bitmap.  Each level ends with one in-place ncclAllGather of the owned slices of
-// the next-frontier bitmap over NVLink/NVSwitch; a finish kernel then ORs it into the
-// replicated visited bitmap and counts c, m_f, m_fin, so every rank takes the identical
-// push/pull decision (R10/R11) with no further communication.
+// Rank p of P owns the vertex block [lo_p, hi_p) (bitmap words [p*cw, (p+1)*cw), cw a
+// multiple of 32 words, so blocks are 1024-vertex aligned) and keeps ONLY:
+//   - the CSC rows of its block (in-neighbours, global ids) + their 8-id row heads: pull;
+//   - the PUSH structure: for every global vertex u, the out-neighbours of u inside the
+//     block — the transpose of the CSC block, built here on the device (count, scan,
+//     scatter, per-row sort) — so a push expands the global frontier but discovers only
+//     owned vertices (no all-to-all);
+//   - the global out-degree of its rows (directed graphs; m_f of the direction rule);
+//   - replicated bitmaps (visited x2, frontier x2: n/8 bytes each) and an exchange buffer
+//     that the peers write into: frontier bitmaps, per-level counter records, flags.
+// Graph bytes per rank ~ (2 * 4 * nnz + 4 n) / P + 4 n: the graph is partitioned, only the
+// O(n) push offsets and bitmaps are replicated.
+//
+// The peers' exchange buffers are mapped into every rank's address space: through CUDA IPC
+// handles exchanged over the NCCL communicator (one process per GPU), or directly for a
+// single-device team (pp_team_create, same device).  The BFS kernel (bfs.cu, D = true)
+// writes the peers' copies itself — no host-issued collective on the data path.
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 
@@ -34,7 +45,8 @@ struct NcclApi {
 static NcclApi g_nccl;
 
 // libnccl.so.2 is resolved at run time (torch.distributed has usually loaded it already),
-// so libpushpull.so loads and serves single-GPU calls on systems without NCCL.
+// so libpushpull.so loads and serves single-GPU calls on systems without NCCL.  NCCL is the
+// bootstrap of the multi-rank path only (exchange of the IPC handles at upload).
 bool nccl_load(const char** why) {
   if (g_nccl.loaded) return true;
   const char* names[] = {"libnccl.so.2", "libnccl.so"};
@@ -85,6 +97,40 @@ int nccl_comm_init(void** comm, int nranks, const void* id128, int rank, const c
   return 0;
 }
 
+// All-gather of a small host record (bootstrap only), staged through device memory:
+// recv receives nranks * bytes.
+int nccl_allgather_host(void* comm, const void* send, void* recv, size_t bytes, int nranks,
+                        cudaStream_t st, const char** why) {
+  char* d = nullptr;
+  if (cudaMalloc((void**)&d, bytes * (size_t)(nranks + 1)) != cudaSuccess) {
+    cudaGetLastError();
+    *why = "cudaMalloc (bootstrap buffer)";
+    return -1;
+  }
+  int rc = 0;
+  if (cudaMemcpyAsync(d, send, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) {
+    *why = "cudaMemcpyAsync (bootstrap)";
+    rc = -1;
+  }
+  if (!rc) {
+    const ncclResult_t r = g_nccl.allGather(d, d + bytes, bytes, ncclUint8, (ncclComm_t)comm, st);
+    if (r != ncclSuccess) {
+      *why = g_nccl.getErrorString(r);
+      rc = -2;
+    }
+  }
+  if (!rc && (cudaMemcpyAsync(recv, d + bytes, bytes * (size_t)nranks, cudaMemcpyDeviceToHost, st) !=
+                  cudaSuccess ||
+              cudaStreamSynchronize(st) != cudaSuccess)) {
+    *why = "cudaMemcpy (bootstrap)";
+    rc = -1;
+  }
+  cudaStreamSynchronize(st);
+  cudaFree(d);
+  cudaGetLastError();
+  return rc;
+}
+
 void nccl_comm_destroy(void* comm) {
   if (comm && g_nccl.loaded) g_nccl.commDestroy((ncclComm_t)comm);
 }
@@ -104,289 +150,120 @@ void partition(int64_t n, int rank, int nranks, int64_t* lo, int64_t* hi, int64_
 
 // ---------------------------------------------------------------------------- kernels ----
 
-// Push ranges: positions [pb[u], pe[u]) of row u's sorted ids that lie in [lo, hi).
-template <typename Off>
-__global__ void k_push_ranges(const Off* __restrict__ off, const uint32_t* __restrict__ idx,
-                              int64_t n, uint32_t lo, uint32_t hi, Off* __restrict__ pb,
-                              Off* __restrict__ pe) {
-  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
-       u += (int64_t)gridDim.x * blockDim.x) {
-    Off b = off[u], e = off[u + 1];
-    Off l = b, r = e;  // first id >= lo
-    while (l < r) {
-      const Off m = l + (r - l) / 2;
-      if (idx[m] < lo) l = m + 1;
-      else r = m;
-    }
-    const Off s = l;
-    r = e;  // first id >= hi
-    while (l < r) {
-      const Off m = l + (r - l) / 2;
-      if (idx[m] < hi) l = m + 1;
-      else r = m;
-    }
-    pb[u] = s;
-    pe[u] = l;
-  }
+// in-edge count per global source u over the block's CSC ids (push-structure row lengths)
+__global__ void k_count_src(const uint32_t* __restrict__ cidx, int64_t m,
+                            unsigned long long* __restrict__ cnt) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[cidx[e]], 1ull);
 }
 
-// Init: visited = {s}, frontier = {s}, next = {}; owned depth/parent slices.
-__global__ void k_dist_init(uint32_t* vis, uint32_t* fr, uint32_t* nxt, int64_t W, uint32_t s,
-                            int32_t* depth, uint32_t* parent, int64_t lo, int64_t hi) {
-  const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t gs = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t w = t0; w < W; w += gs) {
-    const uint32_t b = (w == (int64_t)(s >> 5)) ? (1u << (s & 31u)) : 0u;
-    vis[w] = b;
-    fr[w] = b;
-    nxt[w] = 0u;
-  }
-  for (int64_t v = lo + t0; v < hi; v += gs) {
-    depth[v - lo] = (v == (int64_t)s) ? 1 : 0;
-    if (parent) parent[v - lo] = (v == (int64_t)s) ? s : 0xFFFFFFFFu;
-  }
-}
-
-// Push level: every frontier vertex u (global bitmap `fr`), edges into the owned block only.
-// Warp per frontier word; each frontier vertex's owned range is walked by its lane, or by
-// the whole warp when longer than 32.
-template <typename Off, bool PARENTS>
-__global__ void __launch_bounds__(kBlock) k_dist_push(
-    const uint32_t* __restrict__ fr, uint32_t* vis, uint32_t* nxt, int64_t W,
-    const Off* __restrict__ pb, const Off* __restrict__ pe, const uint32_t* __restrict__ idx,
-    int64_t lo, int32_t* depth, uint32_t* parent, int newdepth) {
-  const unsigned lane = lane_id();
-  const int64_t nw = (int64_t)gridDim.x * kWarps;
-  for (int64_t w = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); w < W; w += nw) {
-    const uint32_t word = fr[w];
-    if (!word) continue;
-    auto visit = [&](uint32_t u, uint32_t x) {
-      const uint32_t wi = x >> 5, bit = 1u << (x & 31u);
-      const uint32_t cur = vis[wi];
-      bool disc = false;
-      if (!(cur & bit)) disc = !(atomicOr(&vis[wi], bit) & bit);
-      if (disc) {
-        depth[x - lo] = newdepth;
-        atomicOr(&nxt[wi], bit);
-      }
-      if (PARENTS) {
-        bool fresh = disc || !(cur & bit);
-        if (!fresh) {
-          const int dx = ld_relaxed_s32(&depth[x - lo]);
-          fresh = dx == 0 || dx == newdepth;
-        }
-        if (fresh) atomicMin(&parent[x - lo], u);
-      }
-    };
-    // lanes take the word's vertices; short owned ranges lane-serial, long ones by the warp
-    const bool mine = (word >> lane) & 1u;
-    const uint32_t u = (uint32_t)w * 32u + lane;
-    Off b = 0, e = 0;
-    if (mine) {
-      b = pb[u];
-      e = pe[u];
-    }
-    const bool longr = mine && (e - b) > (Off)32;
-    if (mine && !longr)
-      for (Off p = b; p < e; ++p) visit(u, idx[p]);
-    unsigned lm = __ballot_sync(kFull, longr);
-    while (lm) {
-      const unsigned l = __ffs(lm) - 1;
-      lm &= lm - 1;
-      const Off lb = __shfl_sync(kFull, b, l), le = __shfl_sync(kFull, e, l);
-      const uint32_t lu = (uint32_t)w * 32u + l;
-      for (Off p = lb + lane; p < le; p += 32) visit(lu, idx[p]);
+// scatter: CSC entry (u -> lo + r) of local row r lands in push row u (warp per row)
+__global__ void k_fill_push(const int64_t* __restrict__ coff, const uint32_t* __restrict__ cidx,
+                            int64_t rows, uint32_t lo, unsigned long long* __restrict__ cursor,
+                            uint32_t* __restrict__ pidx) {
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x / 32);
+  for (int64_t r = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); r < rows; r += nw) {
+    const int64_t b = coff[r], e = coff[r + 1];
+    for (int64_t p = b + lane_id(); p < e; p += 32) {
+      const unsigned long long pos = atomicAdd(&cursor[cidx[p]], 1ull);
+      pidx[pos] = lo + (uint32_t)r;
     }
   }
 }
 
-// Pull level: owned unvisited non-isolated rows scan their in-neighbours (global ids) against
-// the replicated visited snapshot; first hit in sorted order = parent (early exit).
-template <typename Off, bool PARENTS>
-__global__ void __launch_bounds__(kBlock) k_dist_pull(
-    const uint32_t* __restrict__ vis, const uint32_t* __restrict__ iso, uint32_t* nxt,
-    int64_t w_lo, int64_t w_hi, const Off* __restrict__ coff, const uint32_t* __restrict__ cidx,
-    int64_t lo, int64_t n, int32_t* depth, uint32_t* parent, int newdepth) {
-  const unsigned lane = lane_id();
-  const int64_t nw = (int64_t)gridDim.x * kWarps;
-  for (int64_t w = w_lo + (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5); w < w_hi; w += nw) {
-    uint32_t cand = ~vis[w] & ~iso[w];
-    uint32_t found = 0;
-    while (cand) {  // one candidate per lane per round
-      const unsigned cnt = __popc(cand);
-      const bool act = lane < cnt;
-      const unsigned bit = act ? __fns(cand, 0, (int)lane + 1) : 0u;
-      const int64_t i = (int64_t)w * 32 + bit;
-      bool f = false;
-      uint32_t par = 0;
-      if (act && i < n) {
-        const Off b = coff[i], e = coff[i + 1];
-        for (Off p = b; p < e; ++p) {
-          const uint32_t x = cidx[p];
-          if (bit_test(vis, x)) {
-            f = true;
-            par = x;
-            break;
-          }
-        }
-      }
-      if (f) {
-        depth[i - lo] = newdepth;
-        if (PARENTS) parent[i - lo] = par;
-      }
-      found |= __reduce_or_sync(kFull, f ? (1u << bit) : 0u);
-      // drop the (up to 32) candidates handled this round
-      uint32_t handled = 0, c2 = cand;
-      for (unsigned k = 0; k < 32 && c2; ++k) {
-        handled |= c2 & (0u - c2);
-        c2 &= c2 - 1;
-      }
-      cand &= ~handled;
+// isolated / padding bits of the owned words: local row >= rows (past the block or n), or no
+// in- and no out-edges
+__global__ void k_iso_block(const int64_t* __restrict__ off, const int64_t* __restrict__ coff,
+                            int64_t rows, uint32_t wlo, uint32_t cw, uint32_t* __restrict__ iso) {
+  for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < cw; w += gridDim.x * blockDim.x) {
+    uint32_t bits = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int64_t r = (int64_t)w * 32 + b;
+      bool isolated = true;
+      if (r < rows) isolated = (off[r + 1] == off[r]) && (coff[r + 1] == coff[r]);
+      bits |= (isolated ? 1u : 0u) << b;
     }
-    if (lane == 0 && found) nxt[w] = found;
+    iso[wlo + w] = bits;
   }
 }
 
-// Finish: vis |= nxt; fr = nxt; nxt = 0; counters c, m_f (out-degree), m_fin (in-degree).
-template <typename Off>
-__global__ void __launch_bounds__(kBlock) k_dist_finish(
-    uint32_t* vis, uint32_t* fr, uint32_t* nxt, int64_t W, const Off* __restrict__ off,
-    const Off* __restrict__ coff, unsigned long long* cnt) {
-  unsigned long long c = 0, mf = 0, mfin = 0;
-  for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < W;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t x = nxt[w];
-    fr[w] = x;
-    if (x) {
-      vis[w] |= x;
-      nxt[w] = 0u;
-      c += __popc(x);
-      while (x) {
-        const int64_t v = w * 32 + (__ffs(x) - 1);
-        x &= x - 1;
-        mf += (unsigned long long)(off[v + 1] - off[v]);
-        mfin += (unsigned long long)(coff[v + 1] - coff[v]);
-      }
-    }
-  }
-  c = warp_sum(c);
-  mf = warp_sum(mf);
-  mfin = warp_sum(mfin);
-  if (lane_id() == 0 && c) {
-    atomicAdd(&cnt[0], c);
-    atomicAdd(&cnt[1], mf);
-    atomicAdd(&cnt[2], mfin);
-  }
+__global__ void k_odeg(const int64_t* __restrict__ off, int64_t rows, uint32_t* __restrict__ od) {
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows;
+       r += (int64_t)gridDim.x * blockDim.x)
+    od[r] = (uint32_t)(off[r + 1] - off[r]);
 }
 
-// ---------------------------------------------------------------------------- host -------
+// ---------------------------------------------------------------------------- launchers --
 
-template <typename Off>
-static cudaError_t ranges_t(pp_graph g) {
+struct DTmp {  // scratch device buffer freed on scope exit
+  void* p = nullptr;
+  ~DTmp() {
+    if (p) cudaFree(p);
+  }
+  cudaError_t alloc(size_t b) { return cudaMalloc(&p, b < 1 ? 1 : b); }
+};
+
+#define DS_CK(x)                              \
+  do {                                        \
+    cudaError_t _e = (x);                     \
+    if (_e != cudaSuccess) return _e;         \
+  } while (0)
+
+// Push structure of the block: poff64[n+1] (int64) and pidx[m] (global ids, rows sorted).
+cudaError_t launch_push_structure(pp_graph g, const int64_t* d_coff64, int64_t rows, int64_t m,
+                                  int64_t* poff64, uint32_t* pidx) {
+  cudaStream_t st = g->ctx->stream;
+  const int blocks = g->ctx->num_sms * 8;
+  const int64_t n = g->n;
+  DTmp cnt, cursor, tmp, pidx2;
+  DS_CK(cnt.alloc(sizeof(unsigned long long) * (size_t)(n + 1)));
+  DS_CK(cursor.alloc(sizeof(unsigned long long) * (size_t)(n + 1)));
+  DS_CK(cudaMemsetAsync(cnt.p, 0, sizeof(unsigned long long) * (size_t)(n + 1), st));
+  g->ctx->launches += 3;
+  k_count_src<<<blocks, kBlock, 0, st>>>(g->cidx, m, (unsigned long long*)cnt.p);
+  size_t tb = 0;
+  DS_CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, (unsigned long long*)cnt.p,
+                                      (unsigned long long*)poff64, (int)(n + 1), st));
+  DS_CK(tmp.alloc(tb));
+  DS_CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, (unsigned long long*)cnt.p,
+                                      (unsigned long long*)poff64, (int)(n + 1), st));
+  DS_CK(cudaMemcpyAsync(cursor.p, poff64, sizeof(int64_t) * (size_t)(n + 1),
+                        cudaMemcpyDeviceToDevice, st));
+  k_fill_push<<<blocks, kBlock, 0, st>>>(d_coff64, g->cidx, rows, (uint32_t)g->row_lo,
+                                         (unsigned long long*)cursor.p, pidx);
+  DS_CK(cudaGetLastError());
+  // sorted rows (ascending owned ids): deterministic layout, sequential visited words
+  if (m > 1 && m < (int64_t)0x7FFFFFFF && n < (int64_t)0x7FFFFFFF) {
+    DS_CK(pidx2.alloc(sizeof(uint32_t) * (size_t)m));
+    DS_CK(cudaMemcpyAsync(pidx2.p, pidx, sizeof(uint32_t) * (size_t)m, cudaMemcpyDeviceToDevice, st));
+    size_t sb = 0;
+    DS_CK(cub::DeviceSegmentedSort::SortKeys(nullptr, sb, (const uint32_t*)pidx2.p, pidx, (int)m,
+                                             (int)n, poff64, poff64 + 1, st));
+    DTmp stmp;
+    DS_CK(stmp.alloc(sb));
+    DS_CK(cub::DeviceSegmentedSort::SortKeys(stmp.p, sb, (const uint32_t*)pidx2.p, pidx, (int)m,
+                                             (int)n, poff64, poff64 + 1, st));
+    DS_CK(cudaStreamSynchronize(st));  // scratch freed on return
+  } else {
+    DS_CK(cudaStreamSynchronize(st));
+  }
+  return cudaSuccess;
+}
+
+cudaError_t launch_block_prepare(pp_graph g, const int64_t* d_off64, const int64_t* d_coff64,
+                                 int64_t rows) {
+  cudaStream_t st = g->ctx->stream;
   const int blocks = g->ctx->num_sms * 8;
   g->ctx->launches += 1;
-  k_push_ranges<Off><<<blocks, kBlock, 0, g->ctx->stream>>>(
-      (const Off*)g->off, g->idx, g->n, (uint32_t)g->row_lo, (uint32_t)g->row_hi, (Off*)g->pbeg,
-      (Off*)g->pend);
+  k_iso_block<<<blocks, kBlock, 0, st>>>(d_off64, d_coff64, rows,
+                                         (uint32_t)(g->me * g->chunk_words),
+                                         (uint32_t)g->chunk_words, g->isolated);
+  if (g->odeg) {
+    g->ctx->launches += 1;
+    k_odeg<<<blocks, kBlock, 0, st>>>(d_off64, rows, g->odeg);
+  }
   return cudaGetLastError();
-}
-
-cudaError_t launch_push_ranges(pp_graph g) {
-  return g->off64 ? ranges_t<uint64_t>(g) : ranges_t<uint32_t>(g);
-}
-
-static int host_decide(int rule, int dir, long long c_old, long long c_new, long long m_f,
-                       long long m_u, long long n, double alpha, double beta) {
-  // identical arithmetic to the device decide() and oracle_direction (IEEE double)
-  if (rule == 0) {
-    if (dir == 0) return (c_new > c_old && (double)m_f * alpha > (double)m_u) ? 1 : 0;
-    return (c_new < c_old && (double)c_new * beta < (double)n) ? 0 : 1;
-  }
-  const double cn = (double)c_new, nn = (double)n;
-  if (dir == 0) return (c_new > c_old && cn > alpha * nn) ? 1 : 0;
-  return (c_new < c_old && cn < beta * nn) ? 0 : 1;
-}
-
-template <typename Off, bool PARENTS>
-static int bfs_dist_t(pp_graph g, uint32_t s, int mode, int rule, double alpha, double beta,
-                      int32_t* depth, uint32_t* parent, DistLevel* levels, int cap,
-                      int* nlevels, long long* reached, const char** why) {
-  cudaStream_t st = g->ctx->stream;
-  const int blocks = g->ctx->num_sms * 4;
-  const int64_t W = g->dist_words;
-  const int64_t cw = g->chunk_words;
-  const int rank = g->ctx->rank;
-  uint64_t& L = g->ctx->launches;
-  L += 1;
-  k_dist_init<<<blocks, kBlock, 0, st>>>(g->dvis, g->dfr, g->dnxt, W, s, depth, parent, g->row_lo,
-                                         g->row_hi);
-  const Off* off = (const Off*)g->off;
-  const Off* coff = (const Off*)g->coff;
-  long long indeg_s = 0;
-  {
-    Off h[2];
-    cudaMemcpyAsync(h, coff + s, 2 * sizeof(Off), cudaMemcpyDeviceToHost, st);
-    cudaStreamSynchronize(st);
-    indeg_s = (long long)(h[1] - h[0]);
-  }
-  long long m_u = g->nnz - indeg_s, c_old = 1, reach = 1;
-  int dir = mode == 2 ? 1 : 0;
-  int d = 1;
-  for (;; ++d) {
-    cudaMemsetAsync(g->dcnt, 0, 4 * sizeof(unsigned long long), st);
-    L += 1;
-    if (dir == 0)
-      k_dist_push<Off, PARENTS><<<blocks, kBlock, 0, st>>>(g->dfr, g->dvis, g->dnxt, W,
-                                                           (const Off*)g->pbeg, (const Off*)g->pend,
-                                                           g->idx, g->row_lo, depth, parent, d + 1);
-    else
-      k_dist_pull<Off, PARENTS><<<blocks, kBlock, 0, st>>>(
-          g->dvis, g->diso, g->dnxt, g->row_lo / 32, (g->row_hi + 31) / 32, coff, g->cidx,
-          g->row_lo, g->n, depth, parent, d + 1);
-    // exchange: in-place all-gather of every rank's owned slice of the next bitmap
-    ncclResult_t r = g_nccl.allGather(g->dnxt + (size_t)rank * cw, g->dnxt, (size_t)cw * 4,
-                                      ncclUint8, (ncclComm_t)g->ctx->comm, st);
-    if (r != ncclSuccess) {
-      *why = g_nccl.getErrorString(r);
-      return -2;
-    }
-    L += 1;
-    k_dist_finish<Off><<<blocks, kBlock, 0, st>>>(g->dvis, g->dfr, g->dnxt, W, off, coff, g->dcnt);
-    cudaMemcpyAsync(g->dcnt_host, g->dcnt, 3 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                    st);
-    cudaError_t e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) {
-      *why = cudaGetErrorString(e);
-      return -1;
-    }
-    const long long c_new = (long long)g->dcnt_host[0], mf = (long long)g->dcnt_host[1],
-                    mfin = (long long)g->dcnt_host[2];
-    m_u -= g->symmetric ? mf : mfin;
-    reach += c_new;
-    if (d - 1 < cap) levels[d - 1] = DistLevel{dir, c_new, mf, m_u};
-    if (c_new == 0 || d >= g->n + 1) break;
-    int next = dir;
-    if (mode == 0) next = host_decide(rule, dir, c_old, c_new, mf, m_u, g->n, alpha, beta);
-    dir = next;
-    c_old = c_new;
-  }
-  *nlevels = d;
-  *reached = reach;
-  return 0;
-}
-
-int launch_bfs_dist(pp_graph g, uint32_t source, int mode, int rule, double alpha, double beta,
-                    int32_t* depth, uint32_t* parent, DistLevel* levels, int cap, int* nlevels,
-                    long long* reached, const char** why) {
-  if (g->off64)
-    return parent ? bfs_dist_t<uint64_t, true>(g, source, mode, rule, alpha, beta, depth, parent,
-                                               levels, cap, nlevels, reached, why)
-                  : bfs_dist_t<uint64_t, false>(g, source, mode, rule, alpha, beta, depth, parent,
-                                                levels, cap, nlevels, reached, why);
-  return parent ? bfs_dist_t<uint32_t, true>(g, source, mode, rule, alpha, beta, depth, parent,
-                                             levels, cap, nlevels, reached, why)
-                : bfs_dist_t<uint32_t, false>(g, source, mode, rule, alpha, beta, depth, parent,
-                                              levels, cap, nlevels, reached, why);
 }
 
 }  // namespace pp

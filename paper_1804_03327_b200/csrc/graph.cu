@@ -65,10 +65,11 @@ __global__ void k_hcap(const int64_t* __restrict__ off, int64_t n, unsigned long
   if (lane_id() == 0 && m) atomicMax(maxdeg, m);
 }
 
-// First offending row (or n+1 if none): non-monotone offsets, id >= n, unsorted / duplicate.
+// First offending row (or none): non-monotone offsets, id >= n, unsorted / duplicate.
+// rows = rows given (a rank's block in a multi-rank upload), n = bound on the ids.
 __global__ void k_validate(const int64_t* __restrict__ off, const uint32_t* __restrict__ idx,
-                           int64_t n, unsigned long long* bad) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+                           int64_t rows, int64_t n, unsigned long long* bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = off[i], e = off[i + 1];
     bool ok = b <= e;
@@ -82,10 +83,31 @@ __global__ void k_validate(const int64_t* __restrict__ off, const uint32_t* __re
 }
 
 cudaError_t launch_graph_validate(pp_graph g, const int64_t* d_off64, const uint32_t* d_idx,
-                                  unsigned long long* d_bad, uint64_t* launches) {
+                                  unsigned long long* d_bad, uint64_t* launches, int64_t rows) {
   const int blocks = g->ctx->num_sms * 8;
   *launches += 1;
-  k_validate<<<blocks, kBlock, 0, g->ctx->stream>>>(d_off64, d_idx, g->n, d_bad);
+  k_validate<<<blocks, kBlock, 0, g->ctx->stream>>>(d_off64, d_idx, rows < 0 ? g->n : rows, g->n,
+                                                     d_bad);
+  return cudaGetLastError();
+}
+
+// ---- pieces of the multi-rank (1D row partition) upload, dist.cu -------------------------
+cudaError_t launch_off_narrow(pp_graph g, const int64_t* in, void* out, int64_t m) {
+  const int blocks = g->ctx->num_sms * 8;
+  g->ctx->launches += 1;
+  if (g->off64) k_off_narrow<uint64_t><<<blocks, kBlock, 0, g->ctx->stream>>>(in, (uint64_t*)out, m);
+  else k_off_narrow<uint32_t><<<blocks, kBlock, 0, g->ctx->stream>>>(in, (uint32_t*)out, m);
+  return cudaGetLastError();
+}
+cudaError_t launch_head(pp_graph g, const int64_t* coff, const uint32_t* cidx, int64_t rows) {
+  g->ctx->launches += 1;
+  k_head<<<g->ctx->num_sms * 8, kBlock, 0, g->ctx->stream>>>(coff, cidx, rows, g->head);
+  return cudaGetLastError();
+}
+cudaError_t launch_hcap(pp_graph g, const int64_t* off, int64_t rows, unsigned long long* d_cap,
+                        unsigned long long* d_max) {
+  g->ctx->launches += 1;
+  k_hcap<<<g->ctx->num_sms * 8, kBlock, 0, g->ctx->stream>>>(off, rows, d_cap, d_max);
   return cudaGetLastError();
 }
 

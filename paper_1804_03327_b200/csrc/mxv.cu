@@ -47,7 +47,7 @@ __global__ void k_list_to_bitmap(const uint32_t* __restrict__ list, int64_t m,
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < m;
        k += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t x = list[k];
-    if ((int64_t)x >= n) {
+    if ((int64_t)x >= n || (k > 0 && list[k - 1] >= x)) {  // id range; sorted unique (R15)
       atomicMin(bad, (unsigned long long)k);
       continue;
     }
@@ -337,7 +337,8 @@ template <typename Off>
 __global__ void __launch_bounds__(kBlock) k_classify(int64_t n, const uint32_t* __restrict__ list, int64_t m,
                                                     const uint32_t* __restrict__ bits,
                                                     uint32_t nwords, const Off* __restrict__ roff,
-                                                    uint32_t* L, uint2* H, LevelCtr* ctr) {
+                                                    uint32_t* L, uint2* H, LevelCtr* ctr,
+                                                    unsigned long long* bad) {
   const unsigned lane = lane_id();
   const int64_t nitems = list ? (m + 31) / 32 : (n + 31) / 32;
   const int64_t wstride = (int64_t)gridDim.x * kWarps;
@@ -351,6 +352,12 @@ __global__ void __launch_bounds__(kBlock) k_classify(int64_t n, const uint32_t* 
       if (k < m) {
         single = list[k];
         has_single = (int64_t)single < n;
+        // the same PP_ERR_RANGE as the pull side's list->bitmap, and a duplicate or unsorted
+        // id (which would overflow the chunk buffers) is rejected too
+        if (!has_single || (k > 0 && list[k - 1] >= single)) {
+          has_single = false;
+          atomicMin(bad, (unsigned long long)k);
+        }
       }
     } else {
       pending = bits[item];  // word `item`: lane b takes vertex item*32+b
@@ -536,7 +543,7 @@ static cudaError_t mxv_t(pp_graph g, const MxvPlan& p) {
   if (e != cudaSuccess) return e;
   g->ctx->launches += 3;
   k_classify<Off><<<blocks, kBlock, 0, st>>>(g->n, p.u_list, p.u_nnz, p.u_bits, g->nwords, roff,
-                                             g->L[0], g->H[0], g->ctr);
+                                             g->L[0], g->H[0], g->ctr, g->scount + 2);
   k_mxv_push<Off><<<blocks, kBlock, 0, st>>>(roff, ridx, g->L[0], g->H[0], g->ctr, p.mask_bits,
                                              p.complement, t);
   k_combine<<<blocks, kBlock, 0, st>>>(g->n, uwords(g), t, p.mask_bits, p.complement, p.accum,

@@ -43,6 +43,7 @@ constexpr bool kInitVec = PP_INIT_VEC != 0;  // BFS init: 16-byte depth stores
 #define PP_VREC 1
 #endif
 constexpr bool kVrec = PP_VREC != 0;  // relabelled graphs: per-vertex {begin, deg, caller id}
+constexpr int kMaxRanks = 8;  // 1D row partition: ranks per multi-rank group (one node)
 
 // Per-level counters, written with atomics during a level, read after the grid barrier.
 struct LevelCtr {
@@ -100,14 +101,19 @@ struct BfsStatus {
 
 }  // namespace pp
 
+struct pp_team_s;  // single-device team of rank contexts (pp_team_create)
+
 struct pp_ctx_s {
   int device = 0;
   cudaStream_t stream = nullptr;
   int num_sms = 0;
   uint64_t launches = 0;
   int refs = 1;  // the caller's handle + one per live graph
-  int rank = 0, nranks = 0;  // nranks > 0: distributed context (NCCL communicator)
-  void* comm = nullptr;
+  int rank = 0, nranks = 0;  // nranks > 0: multi-rank context (one process per GPU, or a team)
+  void* comm = nullptr;      // NCCL communicator (bootstrap of the peer mappings), or nullptr
+  pp_team_s* team = nullptr;  // team member: the peers live on the same device
+  void* sssp_ws = nullptr;  // pp_sssp workspace (grown on demand, freed with the context)
+  size_t sssp_ws_bytes = 0;
 };
 
 struct pp_graph_s {
@@ -155,12 +161,33 @@ struct pp_graph_s {
   long long* dbg = nullptr;  // pp_bfs_debug_times: per level x CTA phase durations
   int dbg_levels = 0;
   int64_t device_bytes = 0;
-  // distributed (1D row partition): owned block, replicated bitmaps, push ranges
-  int64_t row_lo = 0, row_hi = 0, chunk_words = 0, dist_words = 0;
-  uint32_t *dvis = nullptr, *dfr = nullptr, *dnxt = nullptr, *diso = nullptr;
-  void *pbeg = nullptr, *pend = nullptr;
-  unsigned long long* dcnt = nullptr;
-  unsigned long long* dcnt_host = nullptr;
+  // multi-rank (1D row partition): rank `rank` of `nranks` owns vertices
+  // [row_lo, row_hi) = bitmap words [rank*chunk_words, (rank+1)*chunk_words).  off/idx hold
+  // the PUSH structure (for every global u, its out-neighbours inside the block), coff/cidx
+  // the CSC rows of the block (local row = v - row_lo), bitmaps are global (nwords words).
+  bool dist = false;
+  int me = 0, nranks = 1;  // this graph's rank index, ranks
+  int64_t row_lo = 0, row_hi = 0, chunk_words = 0, in_total = 0;
+  uint32_t* odeg = nullptr;  // directed: global out-degree of the owned rows
+  void* xbuf = nullptr;      // exchange buffer: frontier[2] bitmaps, counter records, flags
+  uint32_t* xfr[2] = {nullptr, nullptr};
+  unsigned long long* xcnt = nullptr;   // [2][kMaxRanks][4] counter records (by sender)
+  unsigned long long* xflag = nullptr;  // [kMaxRanks] arrival epochs (by sender)
+  uint32_t* pfr[pp::kMaxRanks][2] = {};  // every rank's frontier buffers (own at [me])
+  unsigned long long* pcnt[pp::kMaxRanks] = {};
+  unsigned long long* pflag[pp::kMaxRanks] = {};
+  void* ipc_base[pp::kMaxRanks] = {};  // peer xbufs opened through CUDA IPC (multi-process)
+  uint64_t xseq = 0;  // BFS calls so far (epoch of the cross-rank flags)
+  void* dargs = nullptr;  // device copy of the kernel arguments (multi-rank launch)
+  void* hargs = nullptr;  // pinned staging of the same
+};
+
+struct pp_team_s {
+  int device = 0;
+  int nranks = 0;
+  int refs = 0;  // member contexts alive
+  pp_ctx ctx[pp::kMaxRanks] = {};
+  pp_graph graphs[pp::kMaxRanks] = {};  // the graph most recently uploaded by each rank
 };
 
 namespace pp {
@@ -171,7 +198,11 @@ pp_status cuda_fail(cudaError_t e, const char* what);
 cudaError_t launch_graph_prepare(pp_graph g, const int64_t* d_off64, const int64_t* d_coff64,
                                  unsigned long long* d_scratch, uint64_t* launches);
 cudaError_t launch_graph_validate(pp_graph g, const int64_t* d_off64, const uint32_t* d_idx,
-                                  unsigned long long* d_bad, uint64_t* launches);
+                                  unsigned long long* d_bad, uint64_t* launches, int64_t rows = -1);
+cudaError_t launch_off_narrow(pp_graph g, const int64_t* in, void* out, int64_t m);
+cudaError_t launch_head(pp_graph g, const int64_t* coff, const uint32_t* cidx, int64_t rows);
+cudaError_t launch_hcap(pp_graph g, const int64_t* off, int64_t rows, unsigned long long* d_cap,
+                        unsigned long long* d_max);
 int bfs_grid_size(pp_graph g, bool parents);
 cudaError_t launch_bfs(pp_graph g, uint32_t source, int mode, int rule, double alpha, double beta,
                        uint32_t toggles, int32_t* depth, uint32_t* parent, int max_levels);
@@ -198,17 +229,21 @@ cudaError_t launch_bitmap_to_list(pp_graph g, const uint32_t* bits, uint32_t* li
                                   int64_t capacity, unsigned long long* d_count);
 
 // dist.cu
-struct DistLevel {
-  int dir;
-  long long c, m_f, m_u;
-};
 bool nccl_load(const char** why);
 int nccl_unique_id(void* out128, const char** why);
 int nccl_comm_init(void** comm, int nranks, const void* id128, int rank, const char** why);
+int nccl_allgather_host(void* comm, const void* send, void* recv, size_t bytes, int nranks,
+                        cudaStream_t st, const char** why);
 void nccl_comm_destroy(void* comm);
 void partition(int64_t n, int rank, int nranks, int64_t* lo, int64_t* hi, int64_t* chunk_words);
-cudaError_t launch_push_ranges(pp_graph g);
-int launch_bfs_dist(pp_graph g, uint32_t source, int mode, int rule, double alpha, double beta,
-                    int32_t* depth, uint32_t* parent, DistLevel* levels, int cap, int* nlevels,
-                    long long* reached, const char** why);
+cudaError_t launch_push_structure(pp_graph g, const int64_t* d_coff64, int64_t rows, int64_t m,
+                                  int64_t* poff64, uint32_t* pidx);
+cudaError_t launch_block_prepare(pp_graph g, const int64_t* d_off64, const int64_t* d_coff64,
+                                 int64_t rows);
+// bfs.cu: one cooperative launch, graphs[r] = rank r's state; nranks = 1 for one process per
+// GPU, nranks = P for a single-device team (P CTA groups)
+cudaError_t launch_bfs_ranks(pp_graph* graphs, int nranks, uint32_t source, int mode, int rule,
+                             double alpha, double beta, int32_t* const* depth,
+                             uint32_t* const* parent);
+size_t bfs_args_bytes();  // device buffer for kMaxRanks kernel-argument blocks
 }  // namespace pp

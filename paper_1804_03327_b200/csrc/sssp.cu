@@ -254,21 +254,47 @@ extern "C" pp_status pp_sssp(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* 
   int dir = 0;  // 0 push, 1 pull
   unsigned nf = 1;
   SS_CK(cudaSetDevice(ctx->device), "pp_sssp: cudaSetDevice");
-  {  // keep the stream-ordered workspace mapped across calls: with the default release
-     // threshold (0) every per-iteration stream sync would unmap it and the next call remap it
-    cudaMemPool_t pool;
-    uint64_t keep = UINT64_MAX;
-    SS_CK(cudaDeviceGetDefaultMemPool(&pool, ctx->device), "pp_sssp: default mem pool");
-    SS_CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep), "pp_sssp: pool threshold");
+  {  // structural check of the caller's arrays: off[0] = 0 and off[n] = nnz on both sides
+    int64_t ends[4] = {-1, -1, -1, -1};
+    SS_CK(cudaMemcpyAsync(&ends[0], csr_off, 8, cudaMemcpyDeviceToHost, s), "pp_sssp: read csr_off[0]");
+    SS_CK(cudaMemcpyAsync(&ends[1], csr_off + n, 8, cudaMemcpyDeviceToHost, s), "pp_sssp: read csr_off[n]");
+    SS_CK(cudaMemcpyAsync(&ends[2], csc_off, 8, cudaMemcpyDeviceToHost, s), "pp_sssp: read csc_off[0]");
+    SS_CK(cudaMemcpyAsync(&ends[3], csc_off + n, 8, cudaMemcpyDeviceToHost, s), "pp_sssp: read csc_off[n]");
+    SS_CK(cudaStreamSynchronize(s), "pp_sssp: read offsets");
+    if (ends[0] != 0 || ends[1] != nnz || ends[2] != 0 || ends[3] != nnz) {
+      set_error("pp_sssp: offsets off[0]=%lld off[n]=%lld coff[0]=%lld coff[n]=%lld, expected 0 and "
+                "nnz=%lld", (long long)ends[0], (long long)ends[1], (long long)ends[2],
+                (long long)ends[3], (long long)nnz);
+      st = PP_ERR_GRAPH;
+      goto out;
+    }
   }
-  SS_CK(cudaMallocAsync((void**)&t, sizeof(float) * n, s), "pp_sssp: alloc t");
-  SS_CK(cudaMallocAsync((void**)&la, sizeof(uint32_t) * n, s), "pp_sssp: alloc list");
-  SS_CK(cudaMallocAsync((void**)&lb, sizeof(uint32_t) * n, s), "pp_sssp: alloc list");
-  SS_CK(cudaMallocAsync((void**)&hrows, sizeof(uint32_t) * n, s), "pp_sssp: alloc heavy rows");
-  SS_CK(cudaMallocAsync((void**)&cand, sizeof(float) * n, s), "pp_sssp: alloc candidates");
-  SS_CK(cudaMallocAsync((void**)&pch, sizeof(uint2) * nch_max, s), "pp_sssp: alloc chunks");
-  SS_CK(cudaMallocAsync((void**)&hch, sizeof(uint2) * nch_max, s), "pp_sssp: alloc chunks");
-  SS_CK(cudaMallocAsync((void**)&cnt, sizeof(unsigned) * 5, s), "pp_sssp: alloc counters");
+  {  // workspace cached in the context (grown on demand, freed by pp_ctx_destroy): no
+     // per-call allocation and no change to any process-wide allocator state
+    const size_t need = sizeof(float) * n * 2 + sizeof(uint32_t) * n * 3 +
+                        sizeof(uint2) * (size_t)nch_max * 2 + 256 * 9;
+    if (ctx->sssp_ws_bytes < need) {
+      if (ctx->sssp_ws) cudaFree(ctx->sssp_ws);
+      ctx->sssp_ws = nullptr;
+      ctx->sssp_ws_bytes = 0;
+      SS_CK(cudaMalloc(&ctx->sssp_ws, need), "pp_sssp: workspace");
+      ctx->sssp_ws_bytes = need;
+    }
+    char* p = static_cast<char*>(ctx->sssp_ws);
+    auto carve = [&](size_t bytes) {
+      char* r = p;
+      p += (bytes + 255) & ~(size_t)255;
+      return (void*)r;
+    };
+    t = (float*)carve(sizeof(float) * n);
+    cand = (float*)carve(sizeof(float) * n);
+    la = (uint32_t*)carve(sizeof(uint32_t) * n);
+    lb = (uint32_t*)carve(sizeof(uint32_t) * n);
+    hrows = (uint32_t*)carve(sizeof(uint32_t) * n);
+    pch = (uint2*)carve(sizeof(uint2) * nch_max);
+    hch = (uint2*)carve(sizeof(uint2) * nch_max);
+    cnt = (unsigned*)carve(sizeof(unsigned) * 8);
+  }
   k_sssp_init<<<grid_for(n, kT, cap), kT, 0, s>>>(n, source, dist, t, la, cnt);
   ctx->launches++;
   if (nnz > 0) {
@@ -322,13 +348,5 @@ extern "C" pp_status pp_sssp(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* 
     stats->switch_iteration = sw;
   }
 out:
-  if (t) cudaFreeAsync(t, s);
-  if (la) cudaFreeAsync(la, s);
-  if (lb) cudaFreeAsync(lb, s);
-  if (hrows) cudaFreeAsync(hrows, s);
-  if (cand) cudaFreeAsync(cand, s);
-  if (pch) cudaFreeAsync(pch, s);
-  if (hch) cudaFreeAsync(hch, s);
-  if (cnt) cudaFreeAsync(cnt, s);
   return st;
 }

@@ -1,8 +1,11 @@
-"""Multi-GPU host logic on CPU: pp_partition tiling, and the 1D-partitioned BFS algorithm
-(tests/dist_model.py, the host-level model of csrc/dist.cu) run by world_size-2 gloo
-processes with a real all_gather exchange, checked against the oracle (depths, direction
-trace) — SURVEY.md 8e edge cases: source in the last block / on a block boundary, n not a
-multiple of 1024*P, a rank with nothing to discover, an isolated source."""
+"""Multi-rank host logic on CPU: pp_partition tiling, the binding's block slicing
+(block_rows: what each rank uploads), and the 1D-partitioned BFS algorithm (tests/dist_model.py:
+the level structure of bfs.cu's multi-rank path -- owned-block push / pull, per-level exchange of
+the owned frontier slices, replicated decision) run by world_size-2 gloo processes with a real
+all_gather exchange, checked against the oracle (depths, direction trace) -- SURVEY.md 8e edge
+cases: source in the last block / on a block boundary, n not a multiple of 1024*P, a rank with
+nothing to discover, an isolated source.  The CUDA kernels themselves are checked against the
+oracle for P = 1..8 by tests/test_gpu_dist.py (single-device team)."""
 import os
 import socket
 
@@ -34,6 +37,24 @@ def test_partition_tiles_and_aligns(n, P):
     assert all(a >= b for a, b in zip(sizes, sizes[1:]))            # full..., partial, 0...
     assert sum(1 for sz in sizes if 0 < sz < full) <= 1
     assert full - n / P < 1024 + 1
+
+
+@pytest.mark.parametrize("P", [1, 2, 3, 8])
+def test_block_rows_tile_the_graph(P):
+    """The rows each rank uploads (row-local offsets + global ids) reassemble the graph."""
+    for g in (synth.rmat(10, 8, seed=3), synth.random_graph(3001, 9000, seed=2, symmetrize=False),
+              synth.from_edges(40, [1], [2])):
+        offs, ids = [], []
+        for r in range(P):
+            lo, hi = pp.pp_partition(g.n, r, P)
+            boff, bidx = pp.block_rows(g.off, g.idx, lo, hi)
+            assert boff.dtype == np.int64 and bidx.dtype == np.uint32
+            assert len(boff) == hi - lo + 1 and boff[0] == 0 and boff[-1] == len(bidx)
+            offs.append(boff[1:] + (sum(len(x) for x in ids)))
+            ids.append(bidx)
+        full_off = np.concatenate([[0]] + offs)
+        assert np.array_equal(full_off, g.off)
+        assert np.array_equal(np.concatenate(ids), g.idx)
 
 
 def _free_port():

@@ -149,3 +149,25 @@ def test_c3_mask_density_sweep(ctx, config):
                 pp.mxv(G, wvec, uvec, mask=mvec, direction=pp.PP_DIR_PULL, early_exit=ee)
                 got = read_vec(wvec, wt, n)
                 assert np.array_equal(got, expected(g, g, u, m, 0, 0, 1, None, 1)), (uname, rho, ee)
+
+
+@pytest.mark.parametrize("direction", [pp.PP_DIR_PUSH, pp.PP_DIR_PULL])
+def test_mxv_bad_list_rejected_in_both_directions(ctx, direction):
+    """A LIST u holding an id >= n, a duplicate or an unsorted pair is PP_ERR_RANGE whichever
+    kernel the direction selects (results never depend on the direction, R25)."""
+    g = synth.rmat(10, 8, seed=2)
+    G = pp.Graph.from_csr(ctx, g)
+    out = torch.zeros((g.n + 31) // 32, dtype=torch.int32, device="cuda")
+    for ids in ([3, g.n], [5, 5], [9, 4]):
+        t = torch.tensor(np.array(ids, np.uint32).view(np.int32), device="cuda")
+        uvec = pp.make_vector(pp.PP_VEC_LIST, g.n, t, len(ids), len(ids))
+        wvec = pp.make_vector(pp.PP_VEC_BITMAP, g.n, out, 0)
+        with pytest.raises(pp.PPError) as e:
+            pp.mxv(G, wvec, uvec, direction=direction)
+        assert e.value.status == pp.PP_ERR_RANGE, ids
+    # an input list whose nnz exceeds its capacity is a dimension error
+    t = torch.zeros(4, dtype=torch.int32, device="cuda")
+    uvec = pp.make_vector(pp.PP_VEC_LIST, g.n, t, 5, 4)
+    with pytest.raises(pp.PPError) as e:
+        pp.mxv(G, pp.make_vector(pp.PP_VEC_BITMAP, g.n, out, 0), uvec)
+    assert e.value.status == pp.PP_ERR_DIM

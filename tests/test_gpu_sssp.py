@@ -109,3 +109,23 @@ def test_sssp_full_size_sampled(ctx):
     fin[s] = False
     assert np.all(tight[fin])
     del torch
+
+
+def test_sssp_malformed_offsets_rejected(ctx):
+    """pp_sssp checks off[0] = 0 and off[n] = nnz on both sides before any kernel runs."""
+    import torch
+    import paper_1804_03327_b200 as pp
+    g = synth.from_edges(4, [0, 1], [1, 2], symmetrize=False)
+    gT = synth.transpose(g)
+    dev = lambda a, dt: torch.from_numpy(np.ascontiguousarray(a).astype(dt)).cuda()
+    w = dev(np.ones(g.nnz), np.float32)
+    bad = g.off.copy()
+    bad[-1] += 1
+    with pytest.raises(pp.PPError) as e:
+        pp.pp_sssp(ctx.handle, g.n, g.nnz, dev(bad, np.int64), dev(g.idx, np.int32), w,
+                   dev(gT.off, np.int64), dev(gT.idx, np.int32), w, 0, 0.01,
+                   torch.empty(g.n, dtype=torch.float32, device="cuda"))
+    assert e.value.status == pp.PP_ERR_GRAPH
+    with pytest.raises(ValueError):   # the Python wrapper checks dtypes
+        pp.sssp(ctx, dev(g.off, np.int32), dev(g.idx, np.int32), w, dev(gT.off, np.int64),
+                dev(gT.idx, np.int32), w, 0)
