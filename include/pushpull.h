@@ -216,6 +216,12 @@ pp_status pp_bfs(pp_graph g, int64_t source, const pp_bfs_options* opts, int32_t
  * CTA's work time in that level's phase (ns, before the grid barrier).  A call with
  * out_ns != NULL copies the last BFS's records (levels x *nctas, level-major) to host. */
 pp_status pp_bfs_debug_times(pp_graph g, int32_t levels, int64_t* out_ns, int32_t* nctas);
+/* Diagnostics (profiling one level alone, e.g. the heaviest pull under ncu): runs levels
+ * 1 .. level-1 of the BFS from `source` in one cooperative launch, hands the loop state over,
+ * and runs level `level` ALONE in a second launch, then stops: depth (device int32[n]) holds
+ * the depths up to level+1 (deeper vertices 0).  Single-GPU graphs; no parents. */
+pp_status pp_bfs_debug_level(pp_graph g, int64_t source, int32_t level, const pp_bfs_options* opts,
+                             int32_t* depth);
 
 /* ---- multi-rank BFS: 1D row partition, exchange fused into the level kernel (SURVEY.md 8e,
  *      NEXT-1; P:516 names distributed GPUs as future work) --------------------------------

@@ -98,6 +98,7 @@ _SIGS = {
     "pp_bfs": ([_vp, _i64, ctypes.POINTER(pp_bfs_options), _vp, _vp,
                 ctypes.POINTER(pp_bfs_stats)], ctypes.c_int),
     "pp_bfs_debug_times": ([_vp, ctypes.c_int32, _vp, ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),
+    "pp_bfs_debug_level": ([_vp, _i64, ctypes.c_int32, ctypes.POINTER(pp_bfs_options), _vp], ctypes.c_int),
     "pp_nccl_unique_id": ([_vp], ctypes.c_int),
     "pp_ctx_create_dist": ([ctypes.c_int, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)],
                            ctypes.c_int),
@@ -199,6 +200,13 @@ def pp_bfs_debug_times(g, levels=0, fetch=False):
     out = np.zeros(levels * nct.value, np.int64)
     _check(_lib.pp_bfs_debug_times(g, 0, out.ctypes.data, ctypes.byref(nct)))
     return out.reshape(levels, nct.value)
+
+
+def pp_bfs_debug_level(g, source, level, depth_ptr, heuristic=PP_HEUR_EDGES, mode=PP_MODE_DO,
+                       toggles=0):
+    """Levels 1..level-1 in one launch, level `level` alone in a second (profiling)."""
+    o = pp_bfs_options(heuristic, mode, 0.0, 0.0, 0, toggles)
+    _check(_lib.pp_bfs_debug_level(g, int(source), int(level), ctypes.byref(o), depth_ptr))
 
 
 def pp_nccl_unique_id() -> bytes:

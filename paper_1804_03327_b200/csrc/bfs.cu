@@ -66,6 +66,8 @@ struct BfsArgs {
   BfsStatus* status;
   int narrow;  // 1: this launch is one thread-block cluster running the small levels
   int resume;  // 1: continue the loop state a narrow launch handed over (bar->rs)
+  int stop_level;  // > 0: hand the loop state over (bar->rs) before level stop_level + 1
+                   // (pp_bfs_debug_level: one level alone in its own launch, for ncu)
   uint32_t source;  // caller id
   int mode;  // 0 DO, 1 push only, 2 pull only
   int rule;  // 0 edges, 1 paper r
@@ -1321,7 +1323,8 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
   nB = (unsigned)sh.lvl[6];
   }
   for (;; ++d) {
-    if (a.narrow && (dir == 1 || (unsigned long long)mf_last > kNarrowMaxEdges)) {
+    if ((a.narrow && (dir == 1 || (unsigned long long)mf_last > kNarrowMaxEdges)) ||
+        (a.stop_level > 0 && d > a.stop_level)) {
       // this level is too wide for one cluster: hand the loop to the whole grid
       if (cta == 0 && threadIdx.x == 0) {
         BfsResume& r = a.bar->rs;
@@ -1444,7 +1447,7 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
     c_old = c_new;
     mf_last = mf;
   }
-  if (a.narrow && cta == 0 && threadIdx.x == 0) a.bar->rs.done = 1;
+  if ((a.narrow || a.stop_level > 0) && cta == 0 && threadIdx.x == 0) a.bar->rs.done = 1;
   if (cta == 0 && threadIdx.x == 0) {
     a.status->levels = d;
     a.status->reached = reached;
@@ -1571,7 +1574,7 @@ static bool use_narrow(pp_graph g, int mode) {
 template <typename Off>
 static cudaError_t launch_off(pp_graph g, uint32_t source, int mode, int rule, double alpha,
                               double beta, uint32_t toggles, int32_t* depth, uint32_t* parent,
-                              int max_levels) {
+                              int max_levels, int split_level) {
   BfsArgs<Off> a;
   memset(&a, 0, sizeof(a));
   a.n = g->n;
@@ -1624,17 +1627,30 @@ static cudaError_t launch_off(pp_graph g, uint32_t source, int mode, int rule, d
     a.narrow = 0;
     a.resume = 1;
   }
+  if (split_level > 0) {
+    // debug split: levels 1 .. split_level-1 in one launch, then level split_level alone in a
+    // second launch that resumes the handed-over loop state (its grid-barrier count restarts)
+    a.stop_level = split_level - 1;
+    cudaError_t e = parent ? launch_t<Off, true>(g, a) : launch_t<Off, false>(g, a);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(&g->bar->count, 0, sizeof(g->bar->count), g->ctx->stream);
+    if (e != cudaSuccess) return e;
+    a.stop_level = 0;
+    a.resume = 1;
+    a.max_levels = split_level;
+  }
   if (parent) return launch_t<Off, true>(g, a);
   return launch_t<Off, false>(g, a);
 }
 
 cudaError_t launch_bfs(pp_graph g, uint32_t source, int mode, int rule, double alpha, double beta,
-                       uint32_t toggles, int32_t* depth, uint32_t* parent, int max_levels) {
+                       uint32_t toggles, int32_t* depth, uint32_t* parent, int max_levels,
+                       int split_level) {
   if (g->off64)
     return launch_off<uint64_t>(g, source, mode, rule, alpha, beta, toggles, depth, parent,
-                                max_levels);
+                                max_levels, split_level);
   return launch_off<uint32_t>(g, source, mode, rule, alpha, beta, toggles, depth, parent,
-                              max_levels);
+                              max_levels, split_level);
 }
 
 }  // namespace pp

@@ -1001,6 +1001,30 @@ pp_status pp_bfs_team(const pp_graph* graphs, int32_t nranks, int64_t source,
   return PP_OK;
 }
 
+pp_status pp_bfs_debug_level(pp_graph g, int64_t source, int32_t level, const pp_bfs_options* opts,
+                             int32_t* depth) {
+  if (!g || !depth || level < 1) PP_FAIL(PP_ERR_ARG, "pp_bfs_debug_level: NULL graph/depth or level < 1");
+  if (g->dist) PP_FAIL(PP_ERR_UNSUPPORTED, "pp_bfs_debug_level: single-GPU graphs only");
+  if (source < 0 || source >= g->n)
+    PP_FAIL(PP_ERR_RANGE, "pp_bfs_debug_level: source %lld out of range", (long long)source);
+  if (!is_device_ptr(depth)) PP_FAIL(PP_ERR_ARG, "pp_bfs_debug_level: depth must be device memory");
+  pp_bfs_options o;
+  if (opts) o = *opts;
+  else pp_bfs_options_default(&o);
+  if (o.toggles & ~7u) PP_FAIL(PP_ERR_ARG, "pp_bfs_debug_level: unknown toggles 0x%x", o.toggles);
+  double alpha = o.alpha, beta = o.beta;
+  if (alpha <= 0) alpha = (o.heuristic == PP_HEUR_EDGES) ? 15.0 : 0.01;
+  if (beta <= 0) beta = (o.heuristic == PP_HEUR_EDGES) ? 18.0 : 0.01;
+  PP_CK(cudaSetDevice(g->ctx->device), "cudaSetDevice");
+  cudaStream_t st = g->ctx->stream;
+  PP_CK(cudaMemsetAsync(g->bar, 0, sizeof(GridBarrier) + sizeof(BfsStatus), st), "memset control");
+  const int max_levels = (int)std::min<int64_t>(g->n + 1, 0x7FFFFFFF);
+  PP_CK(launch_bfs(g, (uint32_t)source, o.mode, o.heuristic, alpha, beta, o.toggles, depth, nullptr,
+                   max_levels, level),
+        "bfs kernel launch");
+  return finish_bfs(g, nullptr, true);
+}
+
 pp_status pp_bfs_debug_times(pp_graph g, int32_t levels, int64_t* out_ns, int32_t* nctas) {
   if (!g) PP_FAIL(PP_ERR_ARG, "pp_bfs_debug_times: NULL graph");
   if (g->dist) PP_FAIL(PP_ERR_UNSUPPORTED, "pp_bfs_debug_times: single-GPU graphs only");

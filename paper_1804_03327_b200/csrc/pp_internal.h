@@ -205,7 +205,8 @@ cudaError_t launch_hcap(pp_graph g, const int64_t* off, int64_t rows, unsigned l
                         unsigned long long* d_max);
 int bfs_grid_size(pp_graph g, bool parents);
 cudaError_t launch_bfs(pp_graph g, uint32_t source, int mode, int rule, double alpha, double beta,
-                       uint32_t toggles, int32_t* depth, uint32_t* parent, int max_levels);
+                       uint32_t toggles, int32_t* depth, uint32_t* parent, int max_levels,
+                       int split_level = 0);
 
 struct MxvPlan {
   int pull;              // 1 = row-based (Alg. 2), 0 = column-based (Alg. 3)

@@ -262,3 +262,19 @@ def test_debug_times_and_level_ns(ctx):
     assert (st["ns"][:st["levels"]] > 0).all() and st["init_ns"] > 0
     exp, _ = oracle.bfs(g, s)
     assert np.array_equal(d.cpu().numpy(), exp)
+
+
+@pytest.mark.parametrize("relabel", [False, True])
+def test_debug_level_split_resumes_exactly(ctx, relabel):
+    """pp_bfs_debug_level: levels 1..k-1 in one launch, level k alone in a second launch that
+    resumes the handed-over loop state; depths up to k+1 must equal the oracle's."""
+    g = synth.make("C1")
+    G = pp.Graph.from_csr(ctx, g, relabel=relabel)
+    d = torch.zeros(g.n, dtype=torch.int32, device="cuda")
+    for s in synth.sources(g, 3, seed=4):
+        exp, L = oracle.bfs(g, int(s))
+        for k in range(1, L + 2):
+            pp.pp_bfs_debug_level(G.handle, int(s), k, d.data_ptr())
+            torch.cuda.synchronize()
+            want = np.where((exp > 0) & (exp <= k + 1), exp, 0)
+            assert np.array_equal(d.cpu().numpy(), want), (s, k)

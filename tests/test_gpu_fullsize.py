@@ -1,0 +1,76 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times
+(north star: bit-exact BFS depths vs the CPU oracle on every config; P:465 protocol).
+  - C2 (RMAT s22 ef16, the bench graph, relabelled as bench.py uploads it): all 64 seeded
+    sources, depths bit-exact vs O1.
+  - C4-road (percolated 4096^2 grid, the high-diameter config): one corner source, depths vs O1,
+    the direction trace vs O4 (almost every level push: the edge rule's growth condition).
+  - C5 (Kronecker/RMAT s26 ef16, 67M vertices, 2.1B edges; single GPU and 2- / 4-rank teams):
+    two sources bit-exact vs O1 (C5 row).
+Slow: the oracle needs ~2 s per s22 source and ~40 s per s26 source on one core."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+pp = pytest.importorskip("paper_1804_03327_b200")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    return pp.Context(0)
+
+
+def test_c2_all_64_sources_bit_exact(ctx):
+    g = synth.make("C2")
+    G = pp.Graph.from_csr(ctx, g, relabel=True)
+    d = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    for s in synth.sources(g, 64, seed=2):
+        pp.bfs(G, int(s), d)
+        exp, _ = oracle.bfs(g, int(s))
+        assert np.array_equal(d.cpu().numpy(), exp), int(s)
+    G.close()
+
+
+def test_c4_road_corner_bit_exact(ctx):
+    g = synth.make("C4_road")
+    G = pp.Graph.from_csr(ctx, g, relabel=True)
+    d = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    s = int(np.nonzero(np.diff(g.off) > 0)[0][0])
+    st = pp.bfs(G, s, d, stats_capacity=20000)
+    exp, L = oracle.bfs(g, s)
+    assert np.array_equal(d.cpu().numpy(), exp)
+    t = oracle.trace(g, g, exp)
+    assert st["levels"] == L and np.array_equal(st["dir"], t["dir"])
+    assert st["dir"].sum() < 0.01 * L                    # push-dominated (C4 row)
+    G.close()
+
+
+def test_c5_single_gpu_and_teams(ctx):
+    g = synth.make("C5")
+    srcs = [int(s) for s in synth.sources(g, 2, seed=2)]
+    exps = [oracle.bfs(g, s)[0] for s in srcs]
+    G = pp.Graph.from_csr(ctx, g, relabel=True)
+    d = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    for s, exp in zip(srcs, exps):
+        pp.bfs(G, s, d)
+        assert np.array_equal(d.cpu().numpy(), exp), s
+    G.close()
+    del G, d
+    torch.cuda.empty_cache()
+    for P in (2, 4):
+        team = pp.Team(P)
+        Gs = team.upload(g)
+        blocks = [pp.pp_partition(g.n, r, P) for r in range(P)]
+        ds = [torch.empty(hi - lo, dtype=torch.int32, device="cuda") for lo, hi in blocks]
+        for s, exp in zip(srcs, exps):
+            pp.bfs_team(Gs, s, ds)
+            got = np.concatenate([x.cpu().numpy() for x in ds])
+            assert np.array_equal(got, exp), (P, s)
+        for G in Gs:
+            G.close()
+        team.close()
+        del Gs, ds
+        torch.cuda.empty_cache()
