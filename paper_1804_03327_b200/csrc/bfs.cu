@@ -66,8 +66,8 @@ struct BfsArgs {
   BfsStatus* status;
   int narrow;  // 1: this launch is one thread-block cluster running the small levels
   int resume;  // 1: continue the loop state a narrow launch handed over (bar->rs)
-  int stop_level;  // > 0: hand the loop state over (bar->rs) before level stop_level + 1
-                   // (pp_bfs_debug_level: one level alone in its own launch, for ncu)
+  int stop_before;  // > 0: hand the loop state over (bar->rs) before level stop_before
+                    // (pp_bfs_debug_level: one level alone in its own launch, for ncu)
   uint32_t source;  // caller id
   int mode;  // 0 DO, 1 push only, 2 pull only
   int rule;  // 0 edges, 1 paper r
@@ -1324,7 +1324,7 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
   }
   for (;; ++d) {
     if ((a.narrow && (dir == 1 || (unsigned long long)mf_last > kNarrowMaxEdges)) ||
-        (a.stop_level > 0 && d > a.stop_level)) {
+        (a.stop_before > 0 && d >= a.stop_before)) {
       // this level is too wide for one cluster: hand the loop to the whole grid
       if (cta == 0 && threadIdx.x == 0) {
         BfsResume& r = a.bar->rs;
@@ -1447,7 +1447,7 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
     c_old = c_new;
     mf_last = mf;
   }
-  if ((a.narrow || a.stop_level > 0) && cta == 0 && threadIdx.x == 0) a.bar->rs.done = 1;
+  if ((a.narrow || a.stop_before > 0) && cta == 0 && threadIdx.x == 0) a.bar->rs.done = 1;
   if (cta == 0 && threadIdx.x == 0) {
     a.status->levels = d;
     a.status->reached = reached;
@@ -1630,12 +1630,12 @@ static cudaError_t launch_off(pp_graph g, uint32_t source, int mode, int rule, d
   if (split_level > 0) {
     // debug split: levels 1 .. split_level-1 in one launch, then level split_level alone in a
     // second launch that resumes the handed-over loop state (its grid-barrier count restarts)
-    a.stop_level = split_level - 1;
+    a.stop_before = split_level;
     cudaError_t e = parent ? launch_t<Off, true>(g, a) : launch_t<Off, false>(g, a);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(&g->bar->count, 0, sizeof(g->bar->count), g->ctx->stream);
     if (e != cudaSuccess) return e;
-    a.stop_level = 0;
+    a.stop_before = 0;
     a.resume = 1;
     a.max_levels = split_level;
   }

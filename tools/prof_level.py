@@ -2,7 +2,7 @@
   ncu --set full -k regex:bfs_persistent --launch-skip S --launch-count 1 \
       python tools/prof_level.py [CONFIG] [LEVEL|pull|push] [SOURCE_INDEX]
 The first call is a warm-up (2 launches), the second call's second launch is the level alone
-(--launch-skip 3).  Prints the level's direction, frontier and candidate counts."""
+(--launch-skip 4: launch 0 is the stats BFS).  Prints the level's direction, frontier and candidate counts."""
 import sys
 
 import numpy as np
