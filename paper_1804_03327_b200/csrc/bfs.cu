@@ -79,6 +79,7 @@ struct BfsArgs {
   // CTAs of this rank in the launch: [cta_base, cta_base + ncta) (a single-device team runs
   // its ranks as CTA groups of one cooperative launch; otherwise 0 and gridDim.x)
   int cta_base, ncta;
+  unsigned* gwork;  // [kRing][kMaxCtas] per-CTA pull item counters (PP_STEAL)
   // ---- multi-rank (1D row partition; D-template instantiations only) ----
   // rank owns vertices [lo, hi) = bitmap words [wlo, wlo + wcnt); off/idx = push structure
   // (global rows, owned targets), coff/cidx/head = CSC rows of the block (local row v - lo),
@@ -565,6 +566,13 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
 #ifndef PP_PULL_KC
 #define PP_PULL_KC 1
 #endif
+#ifndef PP_PULL_PF
+#define PP_PULL_PF 0  // 1: L2 prefetch of the next round's row head / offsets / caller id
+#endif
+#ifndef PP_STEAL
+#define PP_STEAL 0    // > 0: per-CTA item counters in global memory; a warp whose CTA ran out
+                      // of items claims items of up to PP_STEAL other CTAs (tail balance)
+#endif
 constexpr int kC = PP_PULL_KC;  // candidates in flight per lane
 constexpr int kLaneMax = 16;    // residual rows with <= this many ids left: one lane each
 constexpr int kGroupMax = 512;   // <= this many: 8-lane groups; longer: the whole warp
@@ -831,11 +839,15 @@ struct PullCtx {
 // Multi-rank (D): the items cover the owned words [wlo, wlo + wcnt) only; the rows' CSC
 // data is local (row i - lo), the probed in-neighbour ids are global and test the
 // replicated visited snapshot.
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
 template <typename Off, bool PARENTS, bool D>
 __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
                            uint32_t* __restrict__ vout, LevelCtr* out, int d, Acc& acc,
                            uint32_t* sfound, ResidualQ<Off>& rq, const uint32_t* ssum,
-                           unsigned* sctr, uint32_t* fr) {
+                           unsigned* sctr, uint32_t* fr, unsigned* gwork) {
   const unsigned lane = lane_id();
   const unsigned nitems = (D ? a.wcnt : a.nwords) / kPW;
   const unsigned wb0 = D ? a.wlo : 0u;
@@ -858,6 +870,44 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
     w0 = wb0 + (cta + k * G) * kPW;
     pw = kPW;
   };
+#if PP_STEAL
+  // claims an item: own CTA's counter first, then up to PP_STEAL victims' (an item is claimed
+  // by exactly one atomicAdd that returns j < K_v, so a thief may give up at any time: the
+  // owner processes whatever nobody claimed)
+  unsigned vic = cta, tries = 0;
+  auto grab = [&]() {
+    unsigned it = ~0u;
+    if (lane == 0) {
+      while (tries <= (unsigned)PP_STEAL) {
+        const unsigned j = atomicAdd(&gwork[vic], 1u);
+        const unsigned Kv = nitems > vic ? (nitems - vic + G - 1) / G : 0u;
+        if (j < Kv) {
+          it = vic + j * G;
+          break;
+        }
+        ++tries;
+        vic = (vic + 1u + tries * 37u) % G;
+      }
+    }
+    return __shfl_sync(kFull, it, 0);
+  };
+  auto mapi = [&](unsigned it, unsigned& w0, unsigned& pw) {
+    w0 = wb0 + it * kPW;
+    pw = kPW;
+  };
+  unsigned k = grab(), w0n = 0, pwn = 0;
+  if (k != ~0u) mapi(k, w0n, pwn);
+  uint32_t vw_next = (k != ~0u && lane < pwn) ? vin[w0n + lane] : 0xFFFFFFFFu;
+  while (k != ~0u) {
+    wbase = w0n;
+    const unsigned pw = pwn;
+    const bool own = lane < pw;
+    const uint32_t vw = vw_next;
+    k = grab();
+    if (k != ~0u) mapi(k, w0n, pwn);
+    vw_next = (k != ~0u && lane < pwn) ? vin[w0n + lane] : 0xFFFFFFFFu;
+#else
+  (void)gwork;
   auto grab = [&]() {
     unsigned j = 0;
     if (lane == 0) j = atomicAdd(sctr, 1u);
@@ -874,6 +924,7 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
     k = grab();
     if (k < K) map(k, w0n, pwn);
     vw_next = (k < K && lane < pwn) ? vin[w0n + lane] : 0xFFFFFFFFu;
+#endif
     const uint32_t unvisited = ~vw;
     // Masking (Opt. 2): only rows with !v(i) are computed.  Without it every
     // non-isolated row is computed and the result filtered afterwards.
@@ -904,6 +955,21 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
         par[t] = kNone;
         rb[t] = e[t] = 0;
       }
+#if PP_PULL_PF
+      {  // the next round's candidate rows: their head / offsets / caller-id lines into L2
+        const unsigned k2 = base + 32u * kC + lane;
+        const unsigned j2 = warp_owner(incl, k2);
+        const uint32_t m2 = __shfl_sync(kFull, cand, j2);
+        const unsigned x2 = __shfl_sync(kFull, excl, j2);
+        if (k2 < tot) {
+          const uint32_t i2 = wbase * 32u + j2 * 32u + __fns(m2, 0, (int)(k2 - x2) + 1);
+          const uint32_t l2 = i2 - lo;
+          prefetch_l2(a.head + (size_t)l2 * 8u);
+          prefetch_l2(a.coff + l2);
+          if (!D && a.perm) prefetch_l2(a.perm + i2);
+        }
+      }
+#endif
       // stage: offsets and the row's head (first 8 in-neighbours = one 32-byte sector, one
       // 256-bit load from a row-contiguous array: dense items stream it), all in flight
       V8 hd[kC];
@@ -1085,6 +1151,91 @@ struct BfsShared {  // static part; the residual queues live in dynamic shared m
   long long lvl[7];  // c, m_f, m_fin, nL, nH, nbig, nB of the level just finished
   unsigned work;     // CTA-local work counter (cta_grab)
 };
+
+#ifndef PP_FUSED_SYNC
+#define PP_FUSED_SYNC 1
+#endif
+
+__device__ __forceinline__ void red_add_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// End of a level, fused (tools/micro/gridbar.cu V5): the CTA's counter
+// partials are reduced (warps -> warp 0), thread 0 adds them to the level's counters and
+// arrives at the grid barrier with ONE red.release (ordering the counter atomics and every
+// write this CTA made before the first bar.sync), polls with ld.acquire (which invalidates
+// this SM's L1, so no trailing fence is needed), then lanes 0..6 of warp 0 read the seven
+// level counters in parallel.  Two CTA barriers instead of the four of flush_acc +
+// grid_barrier + read_level.
+template <typename Off>
+__device__ __forceinline__ bool level_sync(const BfsArgs<Off>& a, Acc& acc, LevelCtr* out,
+                                           BfsShared<Off>& sh, unsigned& epoch) {
+  __shared__ int s_ok;
+  const unsigned warp = threadIdx.x >> 5, lane = lane_id();
+  {
+    const unsigned long long c = warp_sum(acc.c), mf = warp_sum(acc.mf), mfin = warp_sum(acc.mfin),
+                             big = warp_sum(acc.big);
+    if (lane == 0) {
+      sh.red[warp][0] = c;
+      sh.red[warp][1] = mf;
+      sh.red[warp][2] = mfin;
+      sh.red[warp][3] = big;
+    }
+    acc.c = acc.mf = acc.mfin = acc.big = 0;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const bool in = lane < (unsigned)kBfsWarps;
+    const unsigned long long tc = warp_sum(in ? sh.red[lane][0] : 0ull),
+                             tm = warp_sum(in ? sh.red[lane][1] : 0ull),
+                             ti = warp_sum(in ? sh.red[lane][2] : 0ull),
+                             tb = warp_sum(in ? sh.red[lane][3] : 0ull);
+    int ok = 1;
+    if (lane == 0) {
+      if (tc) {
+        atomicAdd(&out->c, tc);
+        atomicAdd(&out->m_f, tm);
+        atomicAdd(&out->m_fin, ti);
+      }
+      if (tb) atomicAdd(&out->nbig, tb);
+      ++epoch;
+      const unsigned long long target = (unsigned long long)epoch * (unsigned)a.ncta;
+      unsigned long long* cnt = reinterpret_cast<unsigned long long*>(&a.bar->count);
+      red_add_release_u64(cnt, 1ull);
+      unsigned long long v;
+      const unsigned long long t0 = global_timer_ns();
+      while ((v = ld_acquire_u64(cnt)) < target) {
+        if (global_timer_ns() - t0 > kWatchdogNs) {
+          atomicExch(&a.status->error, (int)PP_ERR_TIMEOUT);
+          atomicOr(cnt, kAbortBit);
+          v = kAbortBit;
+          break;
+        }
+      }
+      ok = (v & kAbortBit) ? 0 : 1;
+    }
+    ok = __shfl_sync(kFull, ok, 0);  // also orders lanes 1..6 after lane 0's acquire
+    if (lane < 7) {
+      long long x = 0;
+      switch (lane) {
+        case 0: x = (long long)ld_relaxed_u64(&out->c); break;
+        case 1: x = (long long)ld_relaxed_u64(&out->m_f); break;
+        case 2: x = (long long)ld_relaxed_u64(&out->m_fin); break;
+        case 3: x = (long long)ld_relaxed_u32(&out->nL); break;
+        case 4: x = (long long)ld_relaxed_u32(&out->nH); break;
+        case 5: x = (long long)ld_relaxed_u64(&out->nbig); break;
+        default: x = (long long)ld_relaxed_u32(&out->nB); break;
+      }
+      sh.lvl[lane] = x;
+    }
+    if (lane == 0) {
+      s_ok = ok;
+      sh.work = 0u;
+    }
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
 
 // thread 0 reads a level's counters once (post-barrier) and broadcasts them via smem
 template <typename Off>
@@ -1297,6 +1448,8 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
   if (cta == 0) {
     for (int t = threadIdx.x; t < kRing * (int)(sizeof(LevelCtr) / 4); t += blockDim.x)
       reinterpret_cast<unsigned*>(a.ctr)[t] = 0u;
+    if (PP_STEAL)
+      for (int t = threadIdx.x; t < kRing * kMaxCtas; t += blockDim.x) a.gwork[t] = 0u;
     __syncthreads();
     const Off deg = a.off[s + 1] - a.off[s];  // multi-rank: s's edges into this block
     if (deg >= (Off)kHeavy) {
@@ -1348,6 +1501,8 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
     LevelCtr* out = &a.ctr[d & (kRing - 1)];
     if (cta == 0 && threadIdx.x < sizeof(LevelCtr) / 4)
       reinterpret_cast<unsigned*>(&a.ctr[(d + 1) & (kRing - 1)])[threadIdx.x] = 0u;
+    if (PP_STEAL && cta == 0 && threadIdx.x < (unsigned)kMaxCtas)
+      a.gwork[(size_t)((d + 1) & (kRing - 1)) * kMaxCtas + threadIdx.x] = 0u;
     uint32_t* vis = cur ? a.vis1 : a.vis0;
     uint32_t* vis_other = cur ? a.vis0 : a.vis1;
     // frontier bitmap this level writes (pull; multi-rank also push) and the previous one
@@ -1365,7 +1520,7 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
         __syncthreads();
       }
       pull_phase<Off, PARENTS, D>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp],
-                                  ssum, &sh.work, frout);
+                                  ssum, &sh.work, frout, a.gwork + (size_t)(d & (kRing - 1)) * kMaxCtas);
       if (!D && (a.toggles & PP_OPT_NO_EARLYEXIT)) {  // ablation arms: long rows grid-wide
         if (!level_barrier(a.narrow, a.bar, a.status, epoch, (unsigned)a.ncta)) return;
         const unsigned nch = ld_relaxed_u32(&out->work2);
@@ -1374,9 +1529,13 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
     }
     if (a.dbg && threadIdx.x == 0 && d - 1 < a.dbg_levels)
       a.dbg[(size_t)(d - 1) * a.ncta + cta] = (long long)global_timer_ns() - t_lvl;
-    flush_acc(acc, out, sh.red);
-    if (!level_barrier(a.narrow, a.bar, a.status, epoch, (unsigned)a.ncta)) return;
-    read_level(out, sh);
+    if (PP_FUSED_SYNC && !a.narrow) {
+      if (!level_sync(a, acc, out, sh, epoch)) return;
+    } else {
+      flush_acc(acc, out, sh.red);
+      if (!level_barrier(a.narrow, a.bar, a.status, epoch, (unsigned)a.ncta)) return;
+      read_level(out, sh);
+    }
     if (D && !exchange<Off>(a, sh, frout, d, epoch, (d == 1) ? indeg_s_own : 0, gtid, gsize)) return;
     const long long c_new = sh.lvl[0], mf = sh.lvl[1], mfin = sh.lvl[2];
     nL = (unsigned)sh.lvl[3];
@@ -1605,6 +1764,7 @@ static cudaError_t launch_off(pp_graph g, uint32_t source, int mode, int rule, d
   a.rank = g->rank;
   a.vrec = g->vrec;
   a.ctr = g->ctr;
+  a.gwork = g->gwork;
   a.stats = g->stats;
   a.stats_cap = g->stats_cap;
   a.bar = g->bar;
@@ -1695,6 +1855,7 @@ static cudaError_t launch_ranks_t(pp_graph* gs, int P, uint32_t source, int mode
     a.parent = parent ? parent[r] : nullptr;
     a.pout = a.parent;
     a.ctr = g->ctr;
+    a.gwork = g->gwork;
     a.stats = g->stats;
     a.stats_cap = g->stats_cap;
     a.bar = g->bar;

@@ -81,7 +81,7 @@ void free_graph(pp_graph g) {
                   g->sbits[0], g->sbits[1], g->sbits[2], g->sbits[3], g->sblock, g->hubq, g->scount,
                   g->dtmp[0], g->dtmp[1], g->dbg, g->perm, g->rank, g->pint, g->vrec,
                   g->rbits[0], g->rbits[1], g->rbits[2], g->rbits[3],
-                  g->odeg, g->xbuf, g->dargs};
+                  g->odeg, g->xbuf, g->dargs, g->gwork};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (g->status_host) cudaFreeHost(g->status_host);
@@ -318,6 +318,7 @@ pp_status upload_block(pp_ctx ctx, int64_t n, int64_t row_lo, int64_t row_hi, in
       return s;
   }
   if ((s = dalloc(&g->ctr, kRing, &bytes, "level counters")) != PP_OK) return s;
+  if ((s = dalloc(&g->gwork, (size_t)kRing * kMaxCtas, &bytes, "work counters")) != PP_OK) return s;
   g->stats_cap = (int)std::min<int64_t>(n + 1, 1 << 16);
   if ((s = dalloc(&g->stats, (size_t)g->stats_cap, &bytes, "level stats")) != PP_OK) return s;
   if ((s = dalloc(&g->bar, 2, &bytes, "barrier")) != PP_OK) return s;
@@ -610,6 +611,7 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t row_lo, int64_t row_hi,
   g->sum_words = (uint32_t)((((n + ((int64_t)1 << g->sum_shift) - 1) >> g->sum_shift) + 31) / 32);
   if ((s = dalloc(&g->sumv, g->sum_words, &bytes, "visited summary")) != PP_OK) return s;
   if ((s = dalloc(&g->ctr, kRing, &bytes, "level counters")) != PP_OK) return s;
+  if ((s = dalloc(&g->gwork, (size_t)kRing * kMaxCtas, &bytes, "work counters")) != PP_OK) return s;
   g->stats_cap = (int)std::min<int64_t>(n + 1, 1 << 16);
   if ((s = dalloc(&g->stats, (size_t)g->stats_cap, &bytes, "level stats")) != PP_OK) return s;
   if ((s = dalloc(&g->bar, 2, &bytes, "barrier")) != PP_OK) return s;  // [bar][status]

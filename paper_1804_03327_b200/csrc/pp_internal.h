@@ -44,6 +44,7 @@ constexpr bool kInitVec = PP_INIT_VEC != 0;  // BFS init: 16-byte depth stores
 #endif
 constexpr bool kVrec = PP_VREC != 0;  // relabelled graphs: per-vertex {begin, deg, caller id}
 constexpr int kMaxRanks = 8;  // 1D row partition: ranks per multi-rank group (one node)
+constexpr int kMaxCtas = 1024;  // persistent grid size bound (per-CTA work counters)
 
 // Per-level counters, written with atomics during a level, read after the grid barrier.
 struct LevelCtr {
@@ -147,6 +148,7 @@ struct pp_graph_s {
   int stats_cap = 0;
   pp::GridBarrier* bar = nullptr;
   pp::BfsStatus* status = nullptr;
+  unsigned* gwork = nullptr;  // [kRing][kMaxCtas] per-CTA pull item counters
   pp::BfsStatus* status_host = nullptr;  // pinned
   // mxv scratch
   uint32_t* sbits[4] = {nullptr, nullptr, nullptr, nullptr};  // t, u, mask, w (bitmaps)

@@ -1,4 +1,8 @@
-"""Per-level, per-CTA phase durations of one BFS (load-balance diagnostic)."""
+"""Per-level, per-CTA phase durations of a BFS (load-balance / fixed-cost diagnostic).
+For each level: the level's barrier-to-barrier time (CTA 0), the CTAs' work-phase times
+(loop top to the counter flush; min / median / max), and the remainder = level time - max
+work = counter flush + grid barrier + counter read + decision (the per-level fixed cost).
+Usage: python tools/cta_balance.py [CONFIG] [NSOURCES] [norelabel]"""
 import sys
 import numpy as np
 import torch
@@ -6,17 +10,26 @@ sys.path.insert(0, ".")
 import synth
 import paper_1804_03327_b200 as pp
 
-src = int(sys.argv[1]) if len(sys.argv) > 1 else 2764614
-g = synth.make(sys.argv[2] if len(sys.argv) > 2 else "C2")
+cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
+nsrc = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+g = synth.make(cfg)
 ctx = pp.Context(0)
-G = pp.Graph.from_csr(ctx, g)
+G = pp.Graph.from_csr(ctx, g, relabel="norelabel" not in sys.argv)
 depth = torch.empty(g.n, dtype=torch.int32, device="cuda")
-LV = 16
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+LV = 64
 pp.pp_bfs_debug_times(G.handle, LV)
-for _ in range(3):
-    st = pp.bfs(G, src, depth, stats_capacity=64)
-t = pp.pp_bfs_debug_times(G.handle, LV, fetch=True)
-for k in range(st["levels"]):
-    row = t[k] / 1e3
-    print(f"L{k+1} {'HL'[st['dir'][k]]} level {st['ns'][k]/1e3:7.1f} us | CTA work min {row.min():6.1f} "
-          f"p50 {np.median(row):6.1f} p90 {np.percentile(row,90):6.1f} max {row.max():6.1f} (cta {row.argmax()})")
+for s in synth.sources(g, nsrc, seed=2):
+    s = int(s)
+    for _ in range(2):
+        pp.bfs(G, s, depth)
+    flush.zero_()
+    torch.cuda.synchronize()
+    st = pp.bfs(G, s, depth, stats_capacity=LV)
+    t = pp.pp_bfs_debug_times(G.handle, LV, fetch=True)
+    print(f"{cfg} source {s}: init {st['init_ns']/1e3:.1f} us")
+    for k in range(min(st["levels"], LV)):
+        row = t[k] / 1e3
+        lv = st["ns"][k] / 1e3
+        print(f"  L{k+1} {'HL'[st['dir'][k]]} c={st['c'][k]:>8} level {lv:6.1f} us | CTA work min "
+              f"{row.min():6.1f} p50 {np.median(row):6.1f} max {row.max():6.1f} | rest {lv - row.max():5.1f}")
