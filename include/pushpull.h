@@ -216,6 +216,10 @@ pp_status pp_bfs(pp_graph g, int64_t source, const pp_bfs_options* opts, int32_t
  * CTA's work time in that level's phase (ns, before the grid barrier).  A call with
  * out_ns != NULL copies the last BFS's records (levels x *nctas, level-major) to host. */
 pp_status pp_bfs_debug_times(pp_graph g, int32_t levels, int64_t* out_ns, int32_t* nctas);
+/* Diagnostics: after pp_bfs_debug_times(g, levels > 0, ...) enabled the records, copies three
+ * planes of levels x nctas int64 (ns from each level's loop top, per CTA): [0] warp 0's work
+ * done, [1] every warp of the CTA done (counters reduced), [2] the grid barrier released. */
+pp_status pp_bfs_debug_phases(pp_graph g, int64_t* out_ns);
 /* Diagnostics (profiling one level alone, e.g. the heaviest pull under ncu): runs levels
  * 1 .. level-1 of the BFS from `source` in one cooperative launch, hands the loop state over,
  * and runs level `level` ALONE in a second launch, then stops: depth (device int32[n]) holds
@@ -247,6 +251,16 @@ pp_status pp_ctx_create_dist(int device, void* cuda_stream, const void* nccl_uni
                              int nranks, pp_ctx* out);
 pp_status pp_partition(int64_t n, int32_t rank, int32_t nranks, int64_t* row_lo, int64_t* row_hi);
 pp_status pp_graph_partition(pp_graph g, int64_t* row_lo, int64_t* row_hi);
+
+/* External bootstrap (one process per GPU without NCCL): pp_ctx_create_dist with
+ * nccl_unique_id = NULL creates a multi-rank context without a communicator; after each rank's
+ * pp_graph_upload (then not collective), every rank exports its 128-byte record
+ * (pp_graph_export), the caller all-gathers them in rank order over any transport (e.g.
+ * torch.distributed with gloo) and passes the nranks x 128 bytes to pp_graph_import, which
+ * checks that the ranks agree and maps the peers' exchange buffers (CUDA IPC).  pp_bfs fails
+ * with PP_ERR_ARG until then.  (With an NCCL communicator the upload does this itself.) */
+pp_status pp_graph_export(pp_graph g, void* record128);
+pp_status pp_graph_import(pp_graph g, const void* records);
 
 /* Single-device team: nranks (<= 8) rank contexts on ONE device and stream, ctxs[r] = rank r.
  * Each rank uploads its block with pp_graph_upload (not collective); pp_bfs_team then runs

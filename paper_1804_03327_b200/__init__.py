@@ -99,12 +99,15 @@ _SIGS = {
                 ctypes.POINTER(pp_bfs_stats)], ctypes.c_int),
     "pp_bfs_debug_times": ([_vp, ctypes.c_int32, _vp, ctypes.POINTER(ctypes.c_int32)], ctypes.c_int),
     "pp_bfs_debug_level": ([_vp, _i64, ctypes.c_int32, ctypes.POINTER(pp_bfs_options), _vp], ctypes.c_int),
+    "pp_bfs_debug_phases": ([_vp, _vp], ctypes.c_int),
     "pp_nccl_unique_id": ([_vp], ctypes.c_int),
     "pp_ctx_create_dist": ([ctypes.c_int, _vp, _vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(_vp)],
                            ctypes.c_int),
     "pp_partition": ([_i64, ctypes.c_int32, ctypes.c_int32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)],
                      ctypes.c_int),
     "pp_graph_partition": ([_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)], ctypes.c_int),
+    "pp_graph_export": ([_vp, _vp], ctypes.c_int),
+    "pp_graph_import": ([_vp, _vp], ctypes.c_int),
     "pp_team_create": ([ctypes.c_int, _vp, ctypes.c_int32, ctypes.POINTER(_vp)], ctypes.c_int),
     "pp_bfs_team": ([ctypes.POINTER(_vp), ctypes.c_int32, _i64, ctypes.POINTER(pp_bfs_options),
                      ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(pp_bfs_stats)],
@@ -202,6 +205,13 @@ def pp_bfs_debug_times(g, levels=0, fetch=False):
     return out.reshape(levels, nct.value)
 
 
+def pp_bfs_debug_phases(g, levels, nctas):
+    """The three per-level, per-CTA phase planes (ns) of the last BFS (see pushpull.h)."""
+    out = np.zeros(3 * levels * nctas, np.int64)
+    _check(_lib.pp_bfs_debug_phases(g, out.ctypes.data))
+    return out.reshape(3, levels, nctas)
+
+
 def pp_bfs_debug_level(g, source, level, depth_ptr, heuristic=PP_HEUR_EDGES, mode=PP_MODE_DO,
                        toggles=0):
     """Levels 1..level-1 in one launch, level `level` alone in a second (profiling)."""
@@ -215,12 +225,27 @@ def pp_nccl_unique_id() -> bytes:
     return buf.raw
 
 
-def pp_ctx_create_dist(device: int, cuda_stream: int, nccl_id: bytes, rank: int, nranks: int):
-    assert len(nccl_id) == 128
+def pp_ctx_create_dist(device: int, cuda_stream: int, nccl_id, rank: int, nranks: int):
+    """nccl_id: the 128-byte NCCL unique id, or None (external bootstrap: pp_graph_export /
+    pp_graph_import)."""
     out = _vp()
-    buf = ctypes.create_string_buffer(nccl_id, 128)
+    buf = None
+    if nccl_id is not None:
+        assert len(nccl_id) == 128
+        buf = ctypes.create_string_buffer(nccl_id, 128)
     _check(_lib.pp_ctx_create_dist(device, cuda_stream, buf, rank, nranks, ctypes.byref(out)))
     return out.value
+
+
+def pp_graph_export(g) -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.pp_graph_export(g, buf))
+    return buf.raw
+
+
+def pp_graph_import(g, records: bytes):
+    buf = ctypes.create_string_buffer(records, len(records))
+    _check(_lib.pp_graph_import(g, buf))
 
 
 def pp_partition(n: int, rank: int, nranks: int):
@@ -425,6 +450,14 @@ class Graph:
 
     def partition(self):
         return pp_graph_partition(self.handle)
+
+    def export(self) -> bytes:
+        """This rank's 128-byte peer record (external bootstrap)."""
+        return pp_graph_export(self.handle)
+
+    def import_peers(self, records):
+        """Map the peers from every rank's record, in rank order (external bootstrap)."""
+        pp_graph_import(self.handle, b"".join(records))
 
     def close(self):
         if self.handle:

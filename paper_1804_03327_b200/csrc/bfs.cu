@@ -289,7 +289,19 @@ __device__ __forceinline__ void append_frontier(bool valid, uint32_t v, Off deg,
   }
 }
 
-constexpr int kU = 4;  // edges (push) in flight per lane
+#ifndef PP_PUSH_KU
+#define PP_PUSH_KU 4
+#endif
+constexpr int kU = PP_PUSH_KU;  // edges (push) in flight per lane
+#ifndef PP_LOWLAT_VREC
+#define PP_LOWLAT_VREC 0  // measured neutral; doubles the spills
+#endif
+#ifndef PP_PF_ROWS
+#define PP_PF_ROWS 0  // measured neutral
+#endif
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 
 // The same for kU candidates per lane, with one atomic per list per warp.
 template <typename Off>
@@ -351,17 +363,27 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
   uint32_t cur[kU];
   bool disc[kU];
   Off sb[kU], se[kU];
+  uint32_t sp[kU];  // lowlat + relabelled: the caller id, from the same speculative record
   if (lowlat) {
     // small level: latency matters more than traffic — atomicOr without the pre-test, and
-    // the head's offsets loaded speculatively in parallel (one round trip instead of three)
+    // the head's offsets (relabelled graph: its whole 16-byte vertex record, offsets AND
+    // caller id) loaded speculatively in parallel: one round trip instead of three
 #pragma unroll
     for (int t = 0; t < kU; ++t) {
       cur[t] = 0xFFFFFFFFu;
       sb[t] = se[t] = 0;
+      sp[t] = w[t];
       if (valid[t]) {
         cur[t] = atomicOr(&vis[w[t] >> 5], 1u << (w[t] & 31u));
-        sb[t] = a.off[w[t]];
-        se[t] = a.off[w[t] + 1];
+        if (PP_LOWLAT_VREC && !D && a.vrec) {
+          const uint4 r = __ldg(a.vrec + w[t]);
+          sb[t] = (Off)(((unsigned long long)r.y << 32) | r.x);
+          se[t] = sb[t] + (Off)r.z;
+          sp[t] = r.w;
+        } else {
+          sb[t] = a.off[w[t]];
+          se[t] = a.off[w[t] + 1];
+        }
       }
     }
 #pragma unroll
@@ -399,7 +421,10 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
       if (fresh) atomicMin(&a.parent[slot], u[t]);
     }
   }
-  if (!__any_sync(kFull, disc[0] || disc[1] || disc[2] || disc[3])) return;
+  bool any = false;
+#pragma unroll
+  for (int t = 0; t < kU; ++t) any = any || disc[t];
+  if (!__any_sync(kFull, any)) return;
   if (D) {
 #pragma unroll
     for (int t = 0; t < kU; ++t) {
@@ -429,6 +454,10 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
         beg[t] = (Off)(((unsigned long long)r.y << 32) | r.x);
         deg[t] = (Off)r.z;
         dpos[t] = r.w;
+      } else if (PP_LOWLAT_VREC && a.vrec) {  // lowlat: the speculative record
+        beg[t] = sb[t];
+        deg[t] = se[t] - sb[t];
+        dpos[t] = sp[t];
       } else {
         if (a.perm) dpos[t] = a.perm[w[t]];  // loaded in the same batch as the offsets
         beg[t] = lowlat ? sb[t] : a.off[w[t]];
@@ -438,6 +467,9 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
       acc.c += 1;
       acc.mf += (unsigned long long)deg[t];
       acc.mfin += (unsigned long long)degin;
+      // the next push (if any) reads this row: pull its first ids into L2 now, off the
+      // critical path of the next level's dependent chain (entry -> ids -> visited word)
+      if (PP_PF_ROWS && deg[t] > 0) prefetch_l2(a.idx + beg[t]);
     }
   }
 #pragma unroll
@@ -515,15 +547,18 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
       const Off rb = a.off[h.x], re = a.off[h.x + 1];
       const Off b = rb + (Off)h.y * (Off)kChunk;  // past the row end for a hub's last slots
       const Off e = min(re, b + (Off)kChunk);
+      static_assert(kChunk % (32 * kU) == 0, "chunk = whole warp iterations");
+      for (Off sb = b; sb < e; sb += (Off)(32 * kU)) {
 #pragma unroll
-      for (int t = 0; t < kU; ++t) {
-        const Off p = b + (Off)(t * 32) + lane;
-        valid[t] = p < e;
-        u[t] = h.x;
-        w[t] = valid[t] ? a.idx[p] : 0u;
+        for (int t = 0; t < kU; ++t) {
+          const Off p = sb + (Off)(t * 32) + lane;
+          valid[t] = p < e;
+          u[t] = h.x;
+          w[t] = valid[t] ? a.idx[p] : 0u;
+        }
+        push_visit4<Off, PARENTS, D>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat,
+                                     frout);
       }
-      push_visit4<Off, PARENTS, D>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat,
-                                   frout);
     } else if (!fr) {
       const unsigned i = (item - nHC) * R + lane;
       uint32_t v = 0;
@@ -839,10 +874,6 @@ struct PullCtx {
 // Multi-rank (D): the items cover the owned words [wlo, wlo + wcnt) only; the rows' CSC
 // data is local (row i - lo), the probed in-neighbour ids are global and test the
 // replicated visited snapshot.
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-
 template <typename Off, bool PARENTS, bool D>
 __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
                            uint32_t* __restrict__ vout, LevelCtr* out, int d, Acc& acc,
@@ -1169,7 +1200,8 @@ __device__ __forceinline__ void red_add_release_u64(unsigned long long* p, unsig
 // grid_barrier + read_level.
 template <typename Off>
 __device__ __forceinline__ bool level_sync(const BfsArgs<Off>& a, Acc& acc, LevelCtr* out,
-                                           BfsShared<Off>& sh, unsigned& epoch) {
+                                           BfsShared<Off>& sh, unsigned& epoch, long long t_lvl,
+                                           int d) {
   __shared__ int s_ok;
   const unsigned warp = threadIdx.x >> 5, lane = lane_id();
   {
@@ -1184,6 +1216,12 @@ __device__ __forceinline__ bool level_sync(const BfsArgs<Off>& a, Acc& acc, Leve
     acc.c = acc.mf = acc.mfin = acc.big = 0;
   }
   __syncthreads();
+  // debug phases (pp_bfs_debug_phases): plane 1 = every warp of the CTA done, plane 2 = the
+  // grid barrier released (times from the level's loop top)
+  const bool dbg = a.dbg && threadIdx.x == 0 && d - 1 < a.dbg_levels;
+  const size_t plane = (size_t)a.dbg_levels * (size_t)a.ncta;
+  const size_t slot = (size_t)(d - 1) * a.ncta + (blockIdx.x - a.cta_base);
+  if (dbg) a.dbg[plane + slot] = (long long)global_timer_ns() - t_lvl;
   if (warp == 0) {
     const bool in = lane < (unsigned)kBfsWarps;
     const unsigned long long tc = warp_sum(in ? sh.red[lane][0] : 0ull),
@@ -1213,6 +1251,7 @@ __device__ __forceinline__ bool level_sync(const BfsArgs<Off>& a, Acc& acc, Leve
         }
       }
       ok = (v & kAbortBit) ? 0 : 1;
+      if (dbg) a.dbg[2 * plane + slot] = (long long)global_timer_ns() - t_lvl;
     }
     ok = __shfl_sync(kFull, ok, 0);  // also orders lanes 1..6 after lane 0's acquire
     if (lane < 7) {
@@ -1499,7 +1538,7 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
     }
     const long long t_lvl = (a.dbg && threadIdx.x == 0) ? (long long)global_timer_ns() : 0;
     LevelCtr* out = &a.ctr[d & (kRing - 1)];
-    if (cta == 0 && threadIdx.x < sizeof(LevelCtr) / 4)
+    if (cta == 0 && threadIdx.x < (unsigned)(sizeof(LevelCtr) / 4))
       reinterpret_cast<unsigned*>(&a.ctr[(d + 1) & (kRing - 1)])[threadIdx.x] = 0u;
     if (PP_STEAL && cta == 0 && threadIdx.x < (unsigned)kMaxCtas)
       a.gwork[(size_t)((d + 1) & (kRing - 1)) * kMaxCtas + threadIdx.x] = 0u;
@@ -1530,7 +1569,7 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
     if (a.dbg && threadIdx.x == 0 && d - 1 < a.dbg_levels)
       a.dbg[(size_t)(d - 1) * a.ncta + cta] = (long long)global_timer_ns() - t_lvl;
     if (PP_FUSED_SYNC && !a.narrow) {
-      if (!level_sync(a, acc, out, sh, epoch)) return;
+      if (!level_sync(a, acc, out, sh, epoch, t_lvl, d)) return;
     } else {
       flush_acc(acc, out, sh.red);
       if (!level_barrier(a.narrow, a.bar, a.status, epoch, (unsigned)a.ncta)) return;

@@ -127,31 +127,25 @@ struct BootRec {
 };
 static_assert(sizeof(BootRec) == 128, "BootRec layout");
 
-// Multi-process: map every peer's exchange buffer (CUDA IPC over NVLink) and check that the
-// ranks agree on the graph and tile it.
-pp_status bootstrap_ipc(pp_graph g) {
-  pp_ctx ctx = g->ctx;
-  const int P = ctx->nranks;
-  BootRec me;
-  memset(&me, 0, sizeof(me));
-  if (P > 1) PP_CK(cudaIpcGetMemHandle(&me.h, g->xbuf), "cudaIpcGetMemHandle");
-  me.n = g->n;
-  me.lo = g->row_lo;
-  me.hi = g->row_hi;
-  me.nnz = g->nnz;
-  me.rank = ctx->rank;
-  me.nranks = P;
-  me.off64 = g->off64 ? 1 : 0;
-  me.symmetric = g->symmetric ? 1 : 0;
-  BootRec all[kMaxRanks];
-  const char* why = "";
-  if (P > 1 || ctx->comm) {
-    if (!ctx->comm) PP_FAIL(PP_ERR_NCCL, "pp_graph_upload: multi-rank context without a communicator");
-    const int rc = nccl_allgather_host(ctx->comm, &me, all, sizeof(BootRec), P, ctx->stream, &why);
-    if (rc != 0) PP_FAIL(rc == -2 ? PP_ERR_NCCL : PP_ERR_CUDA, "pp_graph_upload: bootstrap: %s", why);
-  } else {
-    all[0] = me;
-  }
+// This rank's bootstrap record.
+pp_status make_record(pp_graph g, BootRec* me) {
+  memset(me, 0, sizeof(*me));
+  if (g->nranks > 1) PP_CK(cudaIpcGetMemHandle(&me->h, g->xbuf), "cudaIpcGetMemHandle");
+  me->n = g->n;
+  me->lo = g->row_lo;
+  me->hi = g->row_hi;
+  me->nnz = g->nnz;
+  me->rank = g->me;
+  me->nranks = g->nranks;
+  me->off64 = g->off64 ? 1 : 0;
+  me->symmetric = g->symmetric ? 1 : 0;
+  return PP_OK;
+}
+
+// Check that the ranks agree on the graph and tile it, then map every peer's exchange buffer
+// (CUDA IPC: NVLink / NVSwitch peer memory, or the same device).
+pp_status attach_records(pp_graph g, const BootRec* all) {
+  const int P = g->nranks;
   const XLayout L = xlayout(g->nwords);
   int64_t in_total = 0;
   for (int q = 0; q < P; ++q) {
@@ -159,19 +153,36 @@ pp_status bootstrap_ipc(pp_graph g) {
     int64_t lo, hi, cw;
     partition(g->n, q, P, &lo, &hi, &cw);
     if (r.n != g->n || r.rank != q || r.nranks != P || r.lo != lo || r.hi != hi ||
-        r.off64 != me.off64 || r.symmetric != me.symmetric)
+        r.off64 != (g->off64 ? 1 : 0) || r.symmetric != (g->symmetric ? 1 : 0))
       PP_FAIL(PP_ERR_ARG, "pp_graph_upload: rank %d disagrees on the graph or its block (n=%lld, "
               "rows [%lld, %lld), offsets %s, %s)", q, (long long)r.n, (long long)r.lo,
               (long long)r.hi, r.off64 ? "64-bit" : "32-bit", r.symmetric ? "symmetric" : "directed");
     in_total += r.nnz;
-    if (q == ctx->rank) continue;
+  }
+  for (int q = 0; q < P; ++q) {
+    if (q == g->me || g->ipc_base[q]) continue;
     void* base = nullptr;
-    PP_CK(cudaIpcOpenMemHandle(&base, r.h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    PP_CK(cudaIpcOpenMemHandle(&base, all[q].h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
     g->ipc_base[q] = base;
     set_peer(g, q, (char*)base, L);
   }
   g->in_total = in_total;
+  g->attached = true;
   return PP_OK;
+}
+
+// One process per GPU with an NCCL communicator: all-gather the records over NCCL.
+pp_status bootstrap_ipc(pp_graph g) {
+  pp_ctx ctx = g->ctx;
+  const int P = ctx->nranks;
+  BootRec me;
+  pp_status s = make_record(g, &me);
+  if (s != PP_OK) return s;
+  BootRec all[kMaxRanks];
+  const char* why = "";
+  const int rc = nccl_allgather_host(ctx->comm, &me, all, sizeof(BootRec), P, ctx->stream, &why);
+  if (rc != 0) PP_FAIL(rc == -2 ? PP_ERR_NCCL : PP_ERR_CUDA, "pp_graph_upload: bootstrap: %s", why);
+  return attach_records(g, all);
 }
 
 // pp_graph_upload on a multi-rank context: the rank's CSR / CSC rows [row_lo, row_hi) with
@@ -336,11 +347,15 @@ pp_status upload_block(pp_ctx ctx, int64_t n, int64_t row_lo, int64_t row_hi, in
   PP_CK(cudaMalloc(&g->dargs, bfs_args_bytes()), "kernel arguments");
   PP_CK(cudaStreamSynchronize(st), "sync");
   g->in_total = m;
-  if (!ctx->team) {  // one process per GPU: map the peers now (collective)
-    if ((s = bootstrap_ipc(g)) != PP_OK) return s;
-  } else {
+  if (ctx->team) {
     ctx->team->graphs[ctx->rank] = g;
-  }
+  } else if (ctx->comm) {  // one process per GPU: map the peers now (collective)
+    if ((s = bootstrap_ipc(g)) != PP_OK) return s;
+  } else if (ctx->nranks == 1) {  // a single rank has no peers
+    BootRec me;
+    if ((s = make_record(g, &me)) != PP_OK) return s;
+    if ((s = attach_records(g, &me)) != PP_OK) return s;
+  }  // else: external bootstrap (pp_graph_export / pp_graph_import)
   guard.g = nullptr;
   ctx->refs += 1;
   *out = g;
@@ -403,14 +418,14 @@ pp_status pp_nccl_unique_id(void* out128) {
 
 pp_status pp_ctx_create_dist(int device, void* cuda_stream, const void* nccl_unique_id_,
                              int rank, int nranks, pp_ctx* out) {
-  if (!out || !nccl_unique_id_) PP_FAIL(PP_ERR_ARG, "pp_ctx_create_dist: NULL argument");
-  if (nranks < 1 || rank < 0 || rank >= nranks)
-    PP_FAIL(PP_ERR_ARG, "pp_ctx_create_dist: rank %d of %d", rank, nranks);
+  if (!out) PP_FAIL(PP_ERR_ARG, "pp_ctx_create_dist: NULL argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks || nranks > kMaxRanks)
+    PP_FAIL(PP_ERR_ARG, "pp_ctx_create_dist: rank %d of %d (at most %d ranks)", rank, nranks, kMaxRanks);
   pp_status s = pp_ctx_create(device, cuda_stream, out);
   if (s != PP_OK) return s;
   const char* why = "";
   void* comm = nullptr;
-  if (nccl_comm_init(&comm, nranks, nccl_unique_id_, rank, &why) != 0) {
+  if (nccl_unique_id_ && nccl_comm_init(&comm, nranks, nccl_unique_id_, rank, &why) != 0) {
     delete *out;
     *out = nullptr;
     PP_FAIL(PP_ERR_NCCL, "pp_ctx_create_dist: ncclCommInitRank: %s", why);
@@ -651,6 +666,25 @@ pp_status pp_graph_partition(pp_graph g, int64_t* row_lo, int64_t* row_hi) {
   *row_lo = g->dist ? g->row_lo : 0;
   *row_hi = g->dist ? g->row_hi : g->n;
   return PP_OK;
+}
+
+pp_status pp_graph_export(pp_graph g, void* record128) {
+  if (!g || !record128 || !g->dist) PP_FAIL(PP_ERR_ARG, "pp_graph_export: NULL or not a multi-rank graph");
+  PP_CK(cudaSetDevice(g->ctx->device), "cudaSetDevice");
+  BootRec me;
+  pp_status s = make_record(g, &me);
+  if (s != PP_OK) return s;
+  memcpy(record128, &me, sizeof(me));
+  return PP_OK;
+}
+
+pp_status pp_graph_import(pp_graph g, const void* records) {
+  if (!g || !records || !g->dist || g->ctx->team)
+    PP_FAIL(PP_ERR_ARG, "pp_graph_import: NULL, not a multi-rank graph, or a team member");
+  PP_CK(cudaSetDevice(g->ctx->device), "cudaSetDevice");
+  std::vector<BootRec> all((size_t)g->nranks);
+  memcpy(all.data(), records, sizeof(BootRec) * (size_t)g->nranks);
+  return attach_records(g, all.data());
 }
 
 pp_status pp_team_create(int device, void* cuda_stream, int32_t nranks, pp_ctx* ctxs) {
@@ -917,6 +951,8 @@ pp_status pp_bfs(pp_graph g, int64_t source, const pp_bfs_options* opts, int32_t
     PP_FAIL(PP_ERR_UNSUPPORTED, "pp_bfs: ablation toggles are single-GPU only");
   if (g->dist && g->ctx->team)
     PP_FAIL(PP_ERR_ARG, "pp_bfs: a team member's graph runs through pp_bfs_team");
+  if (g->dist && !g->attached)
+    PP_FAIL(PP_ERR_ARG, "pp_bfs: the peers' exchange buffers are not mapped (pp_graph_import)");
   if (g->dist) {  // collective 1D-partitioned BFS; depth/parent are the block's slices
     PP_CK(cudaMemsetAsync(g->bar, 0, sizeof(GridBarrier) + sizeof(BfsStatus), st), "memset control");
     uint32_t* pp_ = (uint32_t*)d_parent;
@@ -1003,6 +1039,15 @@ pp_status pp_bfs_team(const pp_graph* graphs, int32_t nranks, int64_t source,
   return PP_OK;
 }
 
+pp_status pp_bfs_debug_phases(pp_graph g, int64_t* out_ns) {
+  if (!g || !out_ns || !g->dbg) PP_FAIL(PP_ERR_ARG, "pp_bfs_debug_phases: NULL or not enabled");
+  PP_CK(cudaSetDevice(g->ctx->device), "cudaSetDevice");
+  PP_CK(cudaStreamSynchronize(g->ctx->stream), "sync");
+  PP_CK(cudaMemcpy(out_ns, g->dbg, sizeof(long long) * (size_t)g->dbg_levels * g->bfs_grid * 3,
+                   cudaMemcpyDeviceToHost), "copy debug phases");
+  return PP_OK;
+}
+
 pp_status pp_bfs_debug_level(pp_graph g, int64_t source, int32_t level, const pp_bfs_options* opts,
                              int32_t* depth) {
   if (!g || !depth || level < 1) PP_FAIL(PP_ERR_ARG, "pp_bfs_debug_level: NULL graph/depth or level < 1");
@@ -1033,9 +1078,9 @@ pp_status pp_bfs_debug_times(pp_graph g, int32_t levels, int64_t* out_ns, int32_
   PP_CK(cudaSetDevice(g->ctx->device), "cudaSetDevice");
   if (nctas) *nctas = g->bfs_grid;
   if (levels > 0 && !g->dbg) {
-    pp_status s = dalloc(&g->dbg, (size_t)levels * g->bfs_grid, &g->device_bytes, "debug times");
+    pp_status s = dalloc(&g->dbg, (size_t)levels * g->bfs_grid * 3, &g->device_bytes, "debug times");
     if (s != PP_OK) return s;
-    PP_CK(cudaMemset(g->dbg, 0, sizeof(long long) * (size_t)levels * g->bfs_grid), "memset");
+    PP_CK(cudaMemset(g->dbg, 0, sizeof(long long) * (size_t)levels * g->bfs_grid * 3), "memset");
     g->dbg_levels = levels;
     return PP_OK;
   }

@@ -220,34 +220,45 @@ __global__ void __launch_bounds__(kBlock) k_mxv_pull(
 }
 
 // Row-based mxv WITHOUT early exit (Eq. 2 / Eq. 4 evaluated in full): every passing row's
-// ids must be read, so a warp streams its 32 rows' ids as one packed, warp-balanced sequence
-// (warp scan of the passing rows' degrees, 4 coalesced loads per lane per step) and ORs the
-// hits per row with a warp reduction.  Rows longer than kHubIds go to k_mxv_pull_hubs.
+// ids must be read.  Warp item = ONE 32-row bitmap word (so every warp of the grid has work:
+// n/32 items), its passing rows' ids streamed as one packed, warp-balanced sequence (warp
+// scan of the degrees, kStreamU coalesced id loads per lane in flight per step), hits OR-ed
+// per row by a warp reduction; the next item's pass word and offsets are loaded while the
+// current one streams (one dependent step less per item).  Rows longer than kHubIds go to
+// k_mxv_pull_hubs.  (Round 1's item of 32 words processed them one after another on only
+// n/1024 warps: a 32-deep chain per warp, 14% of the copy peak.)
 template <typename Off>
 __global__ void __launch_bounds__(kBlock) k_mxv_pull_stream(
     int64_t n, uint32_t nwords, const Off* __restrict__ roff, const uint32_t* __restrict__ ridx,
     const uint32_t* __restrict__ ubits, const uint32_t* __restrict__ mask, int complement,
     int accum, int replace, const uint32_t* win, uint32_t* out, uint4* hubq, unsigned* nhub) {
   const unsigned lane = lane_id();
-  const unsigned nitems = (nwords + 31) / 32;  // warp item = 32 words; lane l owns word l
   const unsigned wstride = gridDim.x * kWarps;
-  for (unsigned item = blockIdx.x * kWarps + (threadIdx.x >> 5); item < nitems; item += wstride) {
-    const uint32_t myw = item * 32u + lane;
-    const uint32_t mypass = myw < nwords ? pass_word(mask, complement, n, myw) : 0u;
-    uint32_t myt = 0;
-    unsigned todo = __ballot_sync(kFull, mypass != 0);
-    while (todo) {  // stream the words that have passing rows, one at a time
-      const unsigned wl = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const uint32_t w = item * 32u + wl;
-      const uint32_t pass = __shfl_sync(kFull, mypass, wl);
-      const uint32_t i = w * 32u + lane;
-      const bool mine = (pass >> lane) & 1u;
-      Off b = 0, e = 0;
-      if (mine) {
+  unsigned w = blockIdx.x * kWarps + (threadIdx.x >> 5);
+  // item state one step ahead: pass word (all lanes), row offsets (lane = row)
+  auto load = [&](unsigned wn, uint32_t& pass, Off& b, Off& e) {
+    pass = 0u;
+    b = e = 0;
+    if (wn < nwords) {
+      pass = pass_word(mask, complement, n, wn);
+      if ((pass >> lane) & 1u) {
+        const uint32_t i = wn * 32u + lane;
         b = roff[i];
         e = roff[i + 1];
       }
+    }
+  };
+  uint32_t pass_n;
+  Off b_n, e_n;
+  load(w, pass_n, b_n, e_n);
+  for (; w < nwords; w += wstride) {
+    const uint32_t pass = pass_n;
+    const Off b = b_n, e = e_n;
+    load(w + wstride, pass_n, b_n, e_n);
+    const uint32_t i = w * 32u + lane;
+    const bool mine = (pass >> lane) & 1u;
+    uint32_t t = 0;
+    if (pass) {
       const bool hub = mine && (e - b) > (Off)kHubIds;
       const unsigned hm = __ballot_sync(kFull, hub);
       if (hm) {  // hub rows: chunks for the grid-wide kernel
@@ -268,7 +279,6 @@ __global__ void __launch_bounds__(kBlock) k_mxv_pull_stream(
       const unsigned incl = warp_incl_scan(deg);
       const unsigned excl = incl - deg;
       const unsigned tot = __shfl_sync(kFull, incl, 31);
-      uint32_t t = 0;
       // kStreamU coalesced id loads per lane in flight per step, then their probes
       for (unsigned base = 0; base < tot; base += 32u * kStreamU) {
         uint32_t x[kStreamU];
@@ -290,13 +300,12 @@ __global__ void __launch_bounds__(kBlock) k_mxv_pull_stream(
           t |= __reduce_or_sync(kFull, hit ? (1u << jj[s2]) : 0u);
         }
       }
-      if (lane == wl) myt = t;
     }
-    if (myw < nwords) {
-      const uint32_t wi = (accum || !replace) ? win[myw] : 0u;
-      const uint32_t z = accum ? (wi | myt) : myt;
+    if (lane == 0) {
+      const uint32_t wi = (accum || !replace) ? win[w] : 0u;
+      const uint32_t z = accum ? (wi | t) : t;
       const uint32_t keep = replace ? 0u : wi;
-      out[myw] = ((mypass & z) | (~mypass & keep)) & valid_bits(n, myw);
+      out[w] = ((pass & z) | (~pass & keep)) & valid_bits(n, w);
     }
   }
 }
@@ -526,7 +535,7 @@ static cudaError_t mxv_t(pp_graph g, const MxvPlan& p) {
                                                  p.complement, p.accum, p.replace, p.early_exit,
                                                  p.win_bits, p.out_bits, g->hubq, nhub);
     else
-      k_mxv_pull_stream<Off><<<blocks, kBlock, 0, st>>>(g->n, (uint32_t)((g->n + 31) / 32), roff,
+      k_mxv_pull_stream<Off><<<g->ctx->num_sms * 8, kBlock, 0, st>>>(g->n, (uint32_t)((g->n + 31) / 32), roff,
                                                         ridx, p.u_bits, p.mask_bits, p.complement,
                                                         p.accum, p.replace, p.win_bits, p.out_bits,
                                                         g->hubq, nhub);

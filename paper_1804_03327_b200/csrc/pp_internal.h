@@ -47,17 +47,22 @@ constexpr int kMaxRanks = 8;  // 1D row partition: ranks per multi-rank group (o
 constexpr int kMaxCtas = 1024;  // persistent grid size bound (per-CTA work counters)
 
 // Per-level counters, written with atomics during a level, read after the grid barrier.
+// The three atomic populations sit on separate 128-byte L2 lines: the per-CTA counter flush
+// (c, m_f, m_fin, nbig), the per-warp light-list appends (nL), and the heavy-chunk appends /
+// work counters — same-line atomics serialise in one L2 slice.
 struct LevelCtr {
   unsigned long long c;      // vertices discovered by the level
   unsigned long long m_f;    // sum of their out-degrees (Eq. 1)
   unsigned long long m_fin;  // sum of their in-degrees (m_u update, directed graphs)
-  unsigned int nL, nH;       // next frontier: light-list length, heavy-chunk count
-  unsigned int work, work2;  // dynamic work counters (phase, convert phase)
   unsigned long long nbig;   // discoveries with out-degree >= kBig (pull levels)
-  unsigned int nB;           // next frontier: hub block descriptors (32 chunks each)
-  unsigned int pad[3];
+  unsigned int pad0[24];
+  unsigned int nL;           // next frontier: light-list length
+  unsigned int pad1[31];
+  unsigned int nH, nB;       // next frontier: heavy-chunk count, hub block descriptors
+  unsigned int work, work2;  // dynamic work counters (phase, convert phase)
+  unsigned int pad2[28];
 };
-static_assert(sizeof(LevelCtr) == 64, "LevelCtr layout");
+static_assert(sizeof(LevelCtr) == 384, "LevelCtr layout");
 
 struct LevelStat {
   int dir;
@@ -180,6 +185,7 @@ struct pp_graph_s {
   unsigned long long* pflag[pp::kMaxRanks] = {};
   void* ipc_base[pp::kMaxRanks] = {};  // peer xbufs opened through CUDA IPC (multi-process)
   uint64_t xseq = 0;  // BFS calls so far (epoch of the cross-rank flags)
+  bool attached = false;  // peers mapped (bootstrap done)
   void* dargs = nullptr;  // device copy of the kernel arguments (multi-rank launch)
   void* hargs = nullptr;  // pinned staging of the same
 };

@@ -18,13 +18,15 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C3")
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--out", default=None)
+ap.add_argument("--relabel", action="store_true", help="upload with PP_GRAPH_RELABEL (degree order)")
+ap.add_argument("--unmasked-only", action="store_true", help="only the unmasked arm, u = ones (ncu)")
 args = ap.parse_args()
 
 g = synth.make(args.config)
 n, nnz = g.n, g.nnz
 deg = np.diff(g.off)
 ctx = pp.Context(0)
-G = pp.Graph.from_csr(ctx, g)
+G = pp.Graph.from_csr(ctx, g, relabel=args.relabel)
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 nw = (n + 31) // 32
 peak = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"]
@@ -72,7 +74,10 @@ for uname, u in (("ones", np.ones(n, np.uint8)), ("rand1pct", (rng.random(n) < 0
     by = 4 * (n + 1) + 4 * nnz + n // 8 + n // 8
     line = dict(config=args.config, u=uname, arm="unmasked", rho=1.0, us=t * 1e6, bytes=by,
                 gbs=by / t / 1e9, frac=by / t / 1e9 / peak)
+    line["relabel"] = args.relabel
     print(json.dumps(line), flush=True); out_lines.append(line)
+    if args.unmasked_only:
+        break
     for rho in (0.001, 0.002, 0.005, 0.01, 0.02, 0.05, 0.1, 0.2, 0.5, 1.0):
         ids = synth.random_subset(n, int(round(rho * n)), 11)
         m = synth.dense_from_ids(n, ids)

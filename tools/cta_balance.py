@@ -2,7 +2,7 @@
 For each level: the level's barrier-to-barrier time (CTA 0), the CTAs' work-phase times
 (loop top to the counter flush; min / median / max), and the remainder = level time - max
 work = counter flush + grid barrier + counter read + decision (the per-level fixed cost).
-Usage: python tools/cta_balance.py [CONFIG] [NSOURCES] [norelabel]"""
+Usage: python tools/cta_balance.py [CONFIG] [NSOURCES] [norelabel] [noflush]"""
 import sys
 import numpy as np
 import torch
@@ -23,13 +23,17 @@ for s in synth.sources(g, nsrc, seed=2):
     s = int(s)
     for _ in range(2):
         pp.bfs(G, s, depth)
-    flush.zero_()
+    if "noflush" not in sys.argv:
+        flush.zero_()
     torch.cuda.synchronize()
     st = pp.bfs(G, s, depth, stats_capacity=LV)
     t = pp.pp_bfs_debug_times(G.handle, LV, fetch=True)
-    print(f"{cfg} source {s}: init {st['init_ns']/1e3:.1f} us")
+    ph = pp.pp_bfs_debug_phases(G.handle, LV, t.shape[1])
+    print(f"{cfg} source {s}: init {st['init_ns']/1e3:.1f} us; per level: barrier-to-barrier time (CTA 0), "
+          f"warp-0 work max, CTA-wide work (all warps) p50/max, barrier release seen p50/max")
     for k in range(min(st["levels"], LV)):
         row = t[k] / 1e3
+        cw, br = ph[1][k] / 1e3, ph[2][k] / 1e3
         lv = st["ns"][k] / 1e3
-        print(f"  L{k+1} {'HL'[st['dir'][k]]} c={st['c'][k]:>8} level {lv:6.1f} us | CTA work min "
-              f"{row.min():6.1f} p50 {np.median(row):6.1f} max {row.max():6.1f} | rest {lv - row.max():5.1f}")
+        print(f"  L{k+1} {'HL'[st['dir'][k]]} c={st['c'][k]:>8} level {lv:6.1f} | warp0 {row.max():5.1f} | "
+              f"CTA {np.median(cw):5.1f}/{cw.max():5.1f} | released {np.median(br):5.1f}/{br.max():5.1f}")
