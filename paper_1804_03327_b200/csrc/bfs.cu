@@ -45,6 +45,7 @@ struct BfsArgs {
   uint32_t* vis1;
   uint32_t* fr;  // frontier bitmap written by pull levels (push-from-bitmap)
   const uint32_t* __restrict__ head;  // first 8 in-neighbours of every row (pull), 32 B each
+  const uint4* __restrict__ prec;     // PP_PULL_REC: {first in-neighbour, deg, caller id, begin}
   uint32_t* sumv;      // visited summary: bit per 2^sum_shift vertices, isolated excluded
   int sum_shift;
   uint32_t sum_words;
@@ -1001,6 +1002,47 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
         }
       }
 #endif
+#if PP_PULL_REC
+      if (!D && a.prec) {
+        // one 16-byte record per candidate: first in-neighbour, in-degree, caller id, begin;
+        // rows whose first in-neighbour misses continue from begin + 1 in the residual tiers
+        uint4 rc[kC];
+#pragma unroll
+        for (int t = 0; t < kC; ++t)
+          if (valid[t]) rc[t] = __ldg(a.prec + i[t]);
+#pragma unroll
+        for (int t = 0; t < kC; ++t) {
+          if (!valid[t]) continue;
+          const Off deg = (Off)rc[t].y;
+          rb[t] = (Off)rc[t].w;
+          e[t] = rb[t] + deg;
+          if (deg > 0 && C.hit(rc[t].x)) {
+            found[t] = true;
+            par[t] = rc[t].x;
+          }
+          p[t] = (deg > 1) ? rb[t] + 1 : e[t];
+        }
+#pragma unroll
+        for (int t = 0; t < kC; ++t) {
+          if (found[t] && fresh[t]) C.commit(i[t], par[t], e[t] - rb[t], wbase, true, rc[t].z);
+          const bool park = valid[t] && p[t] < e[t] && !(found[t] && C.early_exit) &&
+                            (fresh[t] || !found[t]);
+          const unsigned pm = __ballot_sync(kFull, park);
+          if (park) {
+            const int slot = qn + __popc(pm & lanemask_lt());
+            rq.i[slot] = fresh[t] ? i[t] : kNone - 1;
+            rq.par[slot] = (found[t] || !fresh[t]) ? (found[t] ? par[t] : 0u) : kNone;
+            rq.p[slot] = p[t];
+            rq.rem[slot] = (uint32_t)(e[t] - p[t]);
+            rq.degin[slot] = (uint32_t)(e[t] - rb[t]);
+          }
+          qn += __popc(pm);
+        }
+        __syncwarp();
+        while (qn >= 32) C.residual_batch(qn, 32, wbase, pw);
+        continue;
+      }
+#endif
       // stage: offsets and the row's head (first 8 in-neighbours = one 32-byte sector, one
       // 256-bit load from a row-contiguous array: dense items stream it), all in flight
       V8 hd[kC];
@@ -1789,6 +1831,7 @@ static cudaError_t launch_off(pp_graph g, uint32_t source, int mode, int rule, d
   a.fr = g->fr;
   a.sumv = g->sumv;
   a.head = g->head;
+  a.prec = g->prec;
   a.sum_shift = g->sum_shift;
   a.sum_words = g->sum_words;
   a.L0 = reinterpret_cast<uint4*>(g->L[0]);

@@ -81,7 +81,7 @@ void free_graph(pp_graph g) {
                   g->sbits[0], g->sbits[1], g->sbits[2], g->sbits[3], g->sblock, g->hubq, g->scount,
                   g->dtmp[0], g->dtmp[1], g->dbg, g->perm, g->rank, g->pint, g->vrec,
                   g->rbits[0], g->rbits[1], g->rbits[2], g->rbits[3],
-                  g->odeg, g->xbuf, g->dargs, g->gwork};
+                  g->odeg, g->xbuf, g->dargs, g->gwork, g->prec};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (g->status_host) cudaFreeHost(g->status_host);
@@ -604,6 +604,7 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t row_lo, int64_t row_hi,
   }
   if ((s = dalloc(&g->isolated, g->nwords, &bytes, "isolated")) != PP_OK) return s;
   if ((s = dalloc(&g->head, (size_t)n * 8, &bytes, "row heads")) != PP_OK) return s;
+  if (kPullRec && !g->off64 && (s = dalloc(&g->prec, (size_t)n, &bytes, "row records")) != PP_OK) return s;
   PP_CK(cudaMemsetAsync(g->scount, 0, 4 * sizeof(unsigned long long), st), "memset");
   PP_CK(launch_graph_prepare(g, d_off64, d_coff64, g->scount, &ctx->launches), "prepare kernels");
   PP_CK(cudaMemcpyAsync(g->scount_host, g->scount, 32, cudaMemcpyDeviceToHost, st), "copy");

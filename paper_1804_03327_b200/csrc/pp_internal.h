@@ -43,6 +43,10 @@ constexpr bool kInitVec = PP_INIT_VEC != 0;  // BFS init: 16-byte depth stores
 #define PP_VREC 1
 #endif
 constexpr bool kVrec = PP_VREC != 0;  // relabelled graphs: per-vertex {begin, deg, caller id}
+#ifndef PP_PULL_REC
+#define PP_PULL_REC 0
+#endif
+constexpr bool kPullRec = PP_PULL_REC != 0;  // pull: 16-byte row records instead of 32-byte heads
 constexpr int kMaxRanks = 8;  // 1D row partition: ranks per multi-rank group (one node)
 constexpr int kMaxCtas = 1024;  // persistent grid size bound (per-CTA work counters)
 
@@ -134,6 +138,8 @@ struct pp_graph_s {
   uint32_t* cidx = nullptr;
   uint32_t* isolated = nullptr;  // nwords: bit = no in- and no out-edges, or padding
   uint32_t* head = nullptr;      // 8n: first 8 in-neighbours of every row (pull heads)
+  uint4* prec = nullptr;         // PP_PULL_REC: per row {first in-neighbour, in-degree, caller id,
+                                 // row begin} (32-bit offsets only)
   // PP_GRAPH_RELABEL: internal id = rank by decreasing degree (relabel.cu)
   uint32_t* perm = nullptr;  // internal -> caller id (nullptr: ids are the caller's)
   uint32_t* rank = nullptr;  // caller -> internal id
