@@ -206,6 +206,8 @@ typedef struct {
   int64_t* m_u;
   int64_t* ns;
   int64_t init_ns;
+  int64_t exchanged_bytes; /* multi-rank: bytes this rank stored into its peers' exchange
+                              buffers over the BFS (frontier slices / id lists + records) */
 } pp_bfs_stats;
 
 pp_status pp_bfs(pp_graph g, int64_t source, const pp_bfs_options* opts, int32_t* depth,

@@ -92,7 +92,11 @@ struct BfsArgs {
   int me, nranks;  // this rank's index, ranks in the group
   uint32_t* xfr0;
   uint32_t* xfr1;
-  unsigned long long* xcnt;   // own [2][kMaxRanks][4]
+  unsigned long long* xcnt;   // own [2][kMaxRanks][8]
+  uint32_t* xlst0;            // own id-list receive areas (parity 0 / 1; sender q at q*wcnt)
+  uint32_t* xlst1;
+  uint32_t* xown;             // this rank's push discoveries of the level (first wcnt ids)
+  uint32_t* plst[kMaxRanks][2];
   unsigned long long* xflag;  // own [kMaxRanks]
   uint32_t* pfr[kMaxRanks][2];
   unsigned long long* pcnt[kMaxRanks];
@@ -435,6 +439,9 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
       const Off dg = a.symmetric ? degin : (Off)a.odeg[r];
       a.depth[r] = newdepth;
       atomicOr(&frout[w[t] >> 5], 1u << (w[t] & 31u));
+      // the id list the exchange sends instead of the bitmap slice when it is shorter
+      const unsigned slot = atomicAdd(&out->nX, 1u);
+      if (slot < a.wcnt) a.xown[slot] = w[t];
       acc.c += 1;
       acc.mf += (unsigned long long)dg;
       acc.mfin += (unsigned long long)degin;
@@ -588,7 +595,7 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
         Off b = 0;
         unsigned deg = 0;
         if (k < tot) {
-          v = (wbase + j) * 32u + __fns(mj, 0, (int)(k - xj) + 1);
+          v = (wbase + j) * 32u + nth_set_bit(mj, k - xj);
           b = a.off[v];
           deg = (unsigned)(a.off[v + 1] - b);
         }
@@ -667,6 +674,9 @@ struct PullCtx {
   // bit is confirmed against the exact snapshot bitmap).
   __device__ __forceinline__ bool hit(uint32_t x) const {
     if (!D && no_reuse) return a.depth[a.perm ? a.perm[x] : x] == d;
+#ifdef PP_KO_PROBE  // timing-only knockout: every probed neighbour counts as visited
+    return x != 0xFFFFFFFFu;
+#endif
     if (kSumWordsMax) {
       const uint32_t gi = x >> a.sum_shift;
       if (!((ssum[gi >> 5] >> (gi & 31u)) & 1u)) return false;
@@ -717,7 +727,9 @@ struct PullCtx {
       atomicOr(&vout[i >> 5], bit);
       atomicOr(&fr[i >> 5], bit);
     }
+#ifndef PP_KO_DEPTH  // timing-only knockout: results invalid when defined
     a.depth[dpos] = d + 1;  // caller id of i (multi-rank: the block's slot i - lo)
+#endif
     if (PARENTS) a.parent[D ? i - (uint32_t)a.lo : i] = par;
     if (kSumWordsMax && !in_item) {  // in-item finds reach the summary at item close
       const uint32_t gi = i >> a.sum_shift;
@@ -771,7 +783,7 @@ struct PullCtx {
       }
       m1 &= ~pick;
       const bool has = g < (unsigned)__popc(pick);
-      const unsigned rl = has ? (unsigned)__fns(pick, 0, (int)g + 1) : 0u;
+      const unsigned rl = has ? nth_set_bit(pick, g) : 0u;
       Off gp = __shfl_sync(kFull, p, rl);
       const Off ge = __shfl_sync(kFull, e, rl);
       bool gf = __shfl_sync(kFull, found ? 1 : 0, rl) != 0;
@@ -979,7 +991,7 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
         const uint32_t mj = __shfl_sync(kFull, cand, j);
         const unsigned xj = __shfl_sync(kFull, excl, j);
         const uint32_t uj = __shfl_sync(kFull, unvisited, j);
-        const unsigned bitpos = valid[t] ? __fns(mj, 0, (int)(k - xj) + 1) : 0u;
+        const unsigned bitpos = valid[t] ? nth_set_bit(mj, k - xj) : 0u;
         const unsigned r = j * 32u + bitpos;  // row within the item
         i[t] = wbase * 32u + r;
         fresh[t] = valid[t] && ((uj >> bitpos) & 1u);
@@ -994,7 +1006,7 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
         const uint32_t m2 = __shfl_sync(kFull, cand, j2);
         const unsigned x2 = __shfl_sync(kFull, excl, j2);
         if (k2 < tot) {
-          const uint32_t i2 = wbase * 32u + j2 * 32u + __fns(m2, 0, (int)(k2 - x2) + 1);
+          const uint32_t i2 = wbase * 32u + j2 * 32u + nth_set_bit(m2, k2 - x2);
           const uint32_t l2 = i2 - lo;
           prefetch_l2(a.head + (size_t)l2 * 8u);
           prefetch_l2(a.coff + l2);
@@ -1102,6 +1114,9 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
         qn += __popc(pm);
       }
       __syncwarp();
+#ifdef PP_KO_RESID  // timing-only knockout: undecided rows are dropped
+      qn = 0;
+#endif
       while (qn >= 32) C.residual_batch(qn, 32, wbase, pw);
     }
     if (qn > 0) C.residual_batch(qn, qn, wbase, pw);
@@ -1223,6 +1238,8 @@ struct BfsShared {  // static part; the residual queues live in dynamic shared m
   unsigned long long red[kBfsWarps][4];
   long long lvl[7];  // c, m_f, m_fin, nL, nH, nbig, nB of the level just finished
   unsigned work;     // CTA-local work counter (cta_grab)
+  unsigned xlmask;   // multi-rank: senders whose last exchange was an id list ...
+  unsigned xlen[kMaxRanks];  // ... and the lists' lengths
 };
 
 #ifndef PP_FUSED_SYNC
@@ -1387,44 +1404,68 @@ __device__ __forceinline__ bool rank_rendezvous(const BfsArgs<Off>& a, unsigned 
 template <typename Off>
 __device__ bool exchange(const BfsArgs<Off>& a, BfsShared<Off>& sh, const uint32_t* frout, int d,
                          unsigned& epoch, long long extra_mfin, unsigned long long gtid,
-                         unsigned long long gsize) {
+                         unsigned long long gsize, bool was_push, const LevelCtr* out) {
   const int P = a.nranks, me = a.me;
   const unsigned par = (unsigned)d & 1u;
+  // hybrid encoding: after a push level whose discoveries are fewer than
+  // the slice's words, the id list (4 bytes per discovery) replaces the bitmap slice
+  const unsigned nx = was_push ? ld_relaxed_u32(&out->nX) : ~0u;
+  const bool lst = was_push && nx < a.wcnt;
   if (P > 1) {
-    const unsigned nv = a.wcnt / 4u;
-    const uint4* src = reinterpret_cast<const uint4*>(frout + a.wlo);
-    const unsigned long long tot = (unsigned long long)nv * (unsigned)(P - 1);
-    for (unsigned long long k = gtid; k < tot; k += gsize) {
-      const int qi = (int)(k / nv);
-      const unsigned j = (unsigned)(k - (unsigned long long)qi * nv);
-      const int q = qi >= me ? qi + 1 : qi;
-      reinterpret_cast<uint4*>(a.pfr[q][par] + a.wlo)[j] = src[j];
+    if (lst) {
+      const unsigned long long tot = (unsigned long long)nx * (unsigned)(P - 1);
+      for (unsigned long long k = gtid; k < tot; k += gsize) {
+        const int qi = (int)(k / nx);
+        const unsigned j = (unsigned)(k - (unsigned long long)qi * nx);
+        const int q = qi >= me ? qi + 1 : qi;
+        a.plst[q][par][(size_t)me * a.wcnt + j] = a.xown[j];
+      }
+    } else {
+      const unsigned nv = a.wcnt / 4u;
+      const uint4* src = reinterpret_cast<const uint4*>(frout + a.wlo);
+      const unsigned long long tot = (unsigned long long)nv * (unsigned)(P - 1);
+      for (unsigned long long k = gtid; k < tot; k += gsize) {
+        const int qi = (int)(k / nv);
+        const unsigned j = (unsigned)(k - (unsigned long long)qi * nv);
+        const int q = qi >= me ? qi + 1 : qi;
+        reinterpret_cast<uint4*>(a.pfr[q][par] + a.wlo)[j] = src[j];
+      }
     }
   }
   if (cta_of(a) == 0 && threadIdx.x < (unsigned)P) {
-    unsigned long long* rec = a.pcnt[threadIdx.x] + ((size_t)par * kMaxRanks + (size_t)me) * 4u;
+    unsigned long long* rec = a.pcnt[threadIdx.x] + ((size_t)par * kMaxRanks + (size_t)me) * 8u;
     rec[0] = (unsigned long long)sh.lvl[0];
     rec[1] = (unsigned long long)sh.lvl[1];
     rec[2] = (unsigned long long)(sh.lvl[2] + extra_mfin);
     rec[3] = (unsigned long long)sh.lvl[5];
+    rec[4] = lst ? (unsigned long long)nx : ~0ull;  // list length, or ~0: bitmap slice
   }
+  if (cta_of(a) == 0 && threadIdx.x == 0 && P > 1)
+    a.status->xbytes += (long long)(P - 1) * ((lst ? 4ll * nx : 4ll * a.wcnt) + 40);
   __syncthreads();
   if (threadIdx.x == 0) __threadfence_system();
   if (!grid_barrier(a.bar, a.status, epoch, (unsigned)a.ncta)) return false;
   if (P > 1 && !rank_rendezvous(a, a.xseq + (unsigned long long)d)) return false;
   if (threadIdx.x == 0) {
     long long c = 0, mf = 0, mfin = 0, big = 0;
+    unsigned lmask = 0;
     for (int q = 0; q < P; ++q) {
-      const unsigned long long* rec = a.xcnt + ((size_t)par * kMaxRanks + (size_t)q) * 4u;
+      const unsigned long long* rec = a.xcnt + ((size_t)par * kMaxRanks + (size_t)q) * 8u;
       c += (long long)ld_relaxed_u64(rec + 0);
       mf += (long long)ld_relaxed_u64(rec + 1);
       mfin += (long long)ld_relaxed_u64(rec + 2);
       big += (long long)ld_relaxed_u64(rec + 3);
+      const unsigned long long ln = ld_relaxed_u64(rec + 4);
+      if (q != me && ln != ~0ull) {
+        lmask |= 1u << q;
+        sh.xlen[q] = (unsigned)ln;
+      }
     }
     sh.lvl[0] = c;
     sh.lvl[1] = mf;
     sh.lvl[2] = mfin;
     sh.lvl[5] = big;
+    sh.xlmask = lmask;
   }
   __syncthreads();
   return true;
@@ -1617,7 +1658,9 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
       if (!level_barrier(a.narrow, a.bar, a.status, epoch, (unsigned)a.ncta)) return;
       read_level(out, sh);
     }
-    if (D && !exchange<Off>(a, sh, frout, d, epoch, (d == 1) ? indeg_s_own : 0, gtid, gsize)) return;
+    if (D && !exchange<Off>(a, sh, frout, d, epoch, (d == 1) ? indeg_s_own : 0, gtid, gsize,
+                            dir == 0, out))
+      return;
     const long long c_new = sh.lvl[0], mf = sh.lvl[1], mfin = sh.lvl[2];
     nL = (unsigned)sh.lvl[3];
     nH = (unsigned)sh.lvl[4];
@@ -1651,11 +1694,28 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
       uint32_t* vnext = cur ? a.vis1 : a.vis0;       // bitmap the next level reads
       uint32_t* frnext = (d & 1) ? a.xfr0 : a.xfr1;  // output of level d + 1
       const unsigned long long wlo = a.wlo, whi = (unsigned long long)a.wlo + a.wcnt;
+      const unsigned lmask = sh.xlmask;
       for (unsigned long long w = gtid; w < a.nwords; w += gsize) {
         if (w >= wlo && w < whi) {
           if (next == 0) frnext[w] = 0u;
+        } else if ((lmask >> (unsigned)(w / a.wcnt)) & 1u) {
+          frout[w] = 0u;  // this sender sent an id list: its slice is rebuilt below
         } else {
           vnext[w] = vbase[w] | frout[w];
+        }
+      }
+      if (lmask) {  // id lists: set their bits in the frontier and visited bitmaps
+        if (!level_barrier(false, a.bar, a.status, epoch, (unsigned)a.ncta)) return;
+        const uint32_t* lst = (d & 1) ? a.xlst1 : a.xlst0;
+        for (int q = 0; q < a.nranks; ++q) {
+          if (!((lmask >> q) & 1u)) continue;
+          const unsigned len = sh.xlen[q];
+          for (unsigned long long k = gtid; k < len; k += gsize) {
+            const uint32_t v = lst[(size_t)q * a.wcnt + k];
+            const uint32_t bit = 1u << (v & 31u);
+            atomicOr(&frout[v >> 5], bit);
+            atomicOr(&vnext[v >> 5], bit);
+          }
         }
       }
       if (next == 0 && sh.lvl[5] != 0) {
@@ -1961,10 +2021,15 @@ static cudaError_t launch_ranks_t(pp_graph* gs, int P, uint32_t source, int mode
     a.xfr1 = g->xfr[1];
     a.xcnt = g->xcnt;
     a.xflag = g->xflag;
+    a.xlst0 = g->xlst[0];
+    a.xlst1 = g->xlst[1];
+    a.xown = g->xown;
     for (int q = 0; q < kMaxRanks; ++q) {
       a.pfr[q][0] = g->pfr[q][0];
       a.pfr[q][1] = g->pfr[q][1];
       a.pcnt[q] = g->pcnt[q];
+      a.plst[q][0] = g->plst[q][0];
+      a.plst[q][1] = g->plst[q][1];
       a.pflag[q] = g->pflag[q];
     }
     g->xseq += 1;  // identical on every rank: pp_bfs is collective

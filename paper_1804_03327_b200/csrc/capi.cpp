@@ -98,22 +98,27 @@ struct Guard {  // frees a half-built graph on early return
 // ---- multi-rank residency (dist.cu) -----------------------------------------
 // Layout of the exchange buffer every peer writes into (identical on every rank).
 struct XLayout {
-  size_t fr0, fr1, cnt, flag, bytes;
+  size_t fr0, fr1, l0, l1, cnt, flag, own, bytes;
 };
 XLayout xlayout(int64_t nwords) {
   XLayout L;
   const size_t fb = sizeof(uint32_t) * (size_t)nwords;  // multiple of 128 bytes
   L.fr0 = 0;
   L.fr1 = fb;
-  L.cnt = 2 * fb;
-  L.flag = L.cnt + sizeof(unsigned long long) * 2 * kMaxRanks * 4;
-  L.bytes = L.flag + sizeof(unsigned long long) * kMaxRanks;
+  L.l0 = 2 * fb;  // id lists, same geometry as the bitmap slices (a list is sent only when it
+  L.l1 = 3 * fb;  // is shorter than the sender's slice in words)
+  L.cnt = 4 * fb;
+  L.flag = L.cnt + sizeof(unsigned long long) * 2 * kMaxRanks * 8;
+  L.own = L.flag + sizeof(unsigned long long) * kMaxRanks;
+  L.bytes = L.own + fb;  // own list (local only), >= one slice
   return L;
 }
 
 void set_peer(pp_graph g, int q, char* base, const XLayout& L) {
   g->pfr[q][0] = (uint32_t*)(base + L.fr0);
   g->pfr[q][1] = (uint32_t*)(base + L.fr1);
+  g->plst[q][0] = (uint32_t*)(base + L.l0);
+  g->plst[q][1] = (uint32_t*)(base + L.l1);
   g->pcnt[q] = (unsigned long long*)(base + L.cnt);
   g->pflag[q] = (unsigned long long*)(base + L.flag);
 }
@@ -343,6 +348,9 @@ pp_status upload_block(pp_ctx ctx, int64_t n, int64_t row_lo, int64_t row_hi, in
   g->xfr[1] = (uint32_t*)((char*)g->xbuf + L.fr1);
   g->xcnt = (unsigned long long*)((char*)g->xbuf + L.cnt);
   g->xflag = (unsigned long long*)((char*)g->xbuf + L.flag);
+  g->xlst[0] = (uint32_t*)((char*)g->xbuf + L.l0);
+  g->xlst[1] = (uint32_t*)((char*)g->xbuf + L.l1);
+  g->xown = (uint32_t*)((char*)g->xbuf + L.own);
   set_peer(g, g->me, (char*)g->xbuf, L);
   PP_CK(cudaMalloc(&g->dargs, bfs_args_bytes()), "kernel arguments");
   PP_CK(cudaStreamSynchronize(st), "sync");
@@ -897,6 +905,7 @@ static pp_status finish_bfs(pp_graph g, pp_bfs_stats* stats, bool sync) {
     stats->levels = g->status_host->levels;
     stats->init_ns = g->status_host->t_init - g->status_host->t_start;
     stats->reached = g->status_host->reached;
+    stats->exchanged_bytes = g->dist ? g->status_host->xbytes : 0;
     const int m = std::min(std::min(stats->capacity, g->status_host->levels), g->stats_cap);
     if (m > 0) {
       std::vector<LevelStat> hs((size_t)m);

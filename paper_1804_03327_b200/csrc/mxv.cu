@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kBlock) k_mxv_pull(
       const unsigned j = warp_owner(incl, k);
       const uint32_t mj = __shfl_sync(kFull, pass, j);
       const unsigned xj = __shfl_sync(kFull, excl, j);
-      const unsigned bitpos = valid ? __fns(mj, 0, (int)(k - xj) + 1) : 0u;
+      const unsigned bitpos = valid ? nth_set_bit(mj, k - xj) : 0u;
       const uint32_t i = (item * 32u + j) * 32u + bitpos;
       Off p = 0, e = 0;
       bool t = false;

@@ -8,6 +8,9 @@
 namespace pp {
 
 constexpr unsigned kFull = 0xFFFFFFFFu;
+#ifndef PP_FAST_NTH
+#define PP_FAST_NTH 1
+#endif
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ unsigned lanemask_lt() {
@@ -84,6 +87,28 @@ __device__ __forceinline__ unsigned long long global_timer_ns() {
 // Read-only (non-coherent) loads for data that no thread writes during the kernel.
 template <typename T>
 __device__ __forceinline__ T ldg(const T* p) { return __ldg(p); }
+
+// Position of the k-th (0-based) set bit of m, k < popc(m): a branch-free 5-step popcount
+// search.  (__fns compiles to a ~50-instruction sequence with divergent branches on sm_100a;
+// the warp-balanced candidate enumerations call this once per candidate.)
+__device__ __forceinline__ unsigned nth_set_bit(uint32_t m, unsigned k) {
+#if PP_FAST_NTH
+  unsigned pos = 0, c;
+  c = __popc(m & 0xFFFFu);
+  if (k >= c) { k -= c; m >>= 16; pos += 16; }
+  c = __popc(m & 0xFFu);
+  if (k >= c) { k -= c; m >>= 8; pos += 8; }
+  c = __popc(m & 0xFu);
+  if (k >= c) { k -= c; m >>= 4; pos += 4; }
+  c = __popc(m & 0x3u);
+  if (k >= c) { k -= c; m >>= 2; pos += 2; }
+  c = m & 1u;
+  if (k >= c) pos += 1;
+  return pos;
+#else
+  return __fns(m, 0, (int)k + 1);
+#endif
+}
 
 // Bit test in a bitmap.
 __device__ __forceinline__ bool bit_test(const uint32_t* bits, uint32_t x) {

@@ -64,7 +64,8 @@ struct LevelCtr {
   unsigned int pad1[31];
   unsigned int nH, nB;       // next frontier: heavy-chunk count, hub block descriptors
   unsigned int work, work2;  // dynamic work counters (phase, convert phase)
-  unsigned int pad2[28];
+  unsigned int nX;           // multi-rank push: discoveries appended to the rank's id list
+  unsigned int pad2[27];
 };
 static_assert(sizeof(LevelCtr) == 384, "LevelCtr layout");
 
@@ -107,6 +108,7 @@ struct BfsStatus {
   int levels;  // levels executed
   long long reached;
   long long t_start, t_init;  // %globaltimer at kernel entry / after the init barrier
+  long long xbytes;           // multi-rank: bytes this rank stored into its peers' buffers
 };
 
 }  // namespace pp
@@ -184,10 +186,13 @@ struct pp_graph_s {
   uint32_t* odeg = nullptr;  // directed: global out-degree of the owned rows
   void* xbuf = nullptr;      // exchange buffer: frontier[2] bitmaps, counter records, flags
   uint32_t* xfr[2] = {nullptr, nullptr};
-  unsigned long long* xcnt = nullptr;   // [2][kMaxRanks][4] counter records (by sender)
+  unsigned long long* xcnt = nullptr;   // [2][kMaxRanks][8] counter records (by sender)
+  uint32_t* xlst[2] = {nullptr, nullptr};  // id-list receive areas (sender q: words [q*cw, (q+1)*cw))
+  uint32_t* xown = nullptr;  // this rank's discoveries of the current push level (<= cw ids)
   unsigned long long* xflag = nullptr;  // [kMaxRanks] arrival epochs (by sender)
   uint32_t* pfr[pp::kMaxRanks][2] = {};  // every rank's frontier buffers (own at [me])
   unsigned long long* pcnt[pp::kMaxRanks] = {};
+  uint32_t* plst[pp::kMaxRanks][2] = {};
   unsigned long long* pflag[pp::kMaxRanks] = {};
   void* ipc_base[pp::kMaxRanks] = {};  // peer xbufs opened through CUDA IPC (multi-process)
   uint64_t xseq = 0;  // BFS calls so far (epoch of the cross-rank flags)

@@ -214,3 +214,26 @@ def test_dist_rejects_toggles_and_mxv(graphs, dctx):
     with pytest.raises(pp.PPError) as e:
         pp.mxv(G, pp.make_vector(pp.PP_VEC_BITMAP, g.n, w, 0), pp.make_vector(pp.PP_VEC_BITMAP, g.n, w, 0))
     assert e.value.status == pp.PP_ERR_UNSUPPORTED
+
+
+def test_team_hybrid_exchange_bytes(graphs):
+    """NEXT-1 hybrid encoding: after a push level whose discoveries are fewer than a rank's
+    slice words the rank sends an id list instead of its bitmap slice, so a DO BFS stores
+    fewer bytes into its peers than bitmap-every-level would ((P-1) x (slice + record) per
+    level); results stay bit-exact (test_team_matches_oracle runs the same path)."""
+    g = graphs["C1"]
+    P = 4
+    team = pp.Team(P)
+    Gs = team.upload(g)
+    lo0, hi0 = pp.pp_partition(g.n, 0, P)
+    cw = (hi0 - lo0) // 32
+    for s in synth.sources(g, 3, seed=8):
+        d, _, st = _run_team(team, Gs, g, int(s), pp.PP_MODE_DO, pp.PP_HEUR_EDGES, parents=False)
+        assert np.array_equal(d, oracle.bfs(g, int(s))[0])
+        bitmap_only = st["levels"] * (P - 1) * (4 * cw + 40)
+        assert 0 < st["exchanged_bytes"] < bitmap_only, (st["exchanged_bytes"], bitmap_only)
+        # push-only: every level sends a list whenever it is shorter than the slice
+        d, _, st2 = _run_team(team, Gs, g, int(s), pp.PP_MODE_PUSH_ONLY, pp.PP_HEUR_EDGES,
+                              parents=False)
+        assert np.array_equal(d, oracle.bfs(g, int(s))[0])
+    team.close()

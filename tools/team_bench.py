@@ -64,7 +64,9 @@ for P in Ps:
     lv = " ".join(f"{'HL'[x]}{t / 1e3:.1f}" for x, t in zip(st["dir"], st["ns"]))
     print(f"team P={P}: {np.mean(ts):.3f} ms/BFS = {g.nnz / np.mean(ts) / 1e6:.1f} GTEPS "
           f"(median {np.median(ts):.3f}); upload {up:.1f} s; bytes/rank "
-          f"{max(G.info()[2] for G in Gs) / 1e9:.2f} GB; init {st['init_ns'] / 1e3:.1f} us; "
+          f"{max(G.info()[2] for G in Gs) / 1e9:.2f} GB; exchanged {st['exchanged_bytes'] / 1e6:.2f} MB "
+          f"(rank 0; bitmap-every-level {st['levels'] * (P - 1) * (4 * ((blocks[0][1] - blocks[0][0]) // 32) + 40) / 1e6:.2f}); "
+          f"init {st['init_ns'] / 1e3:.1f} us; "
           f"levels(us) {lv}" + ("; depths == oracle" if exp is not None else ""))
     for G in Gs:
         G.close()
