@@ -295,7 +295,7 @@ __device__ __forceinline__ void append_frontier(bool valid, uint32_t v, Off deg,
 }
 
 #ifndef PP_PUSH_KU
-#define PP_PUSH_KU 4
+#define PP_PUSH_KU 2  // measured: +7% on C2, -14% per C4 level vs 4 (half the spills)
 #endif
 constexpr int kU = PP_PUSH_KU;  // edges (push) in flight per lane
 #ifndef PP_LOWLAT_VREC
@@ -408,7 +408,7 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
   }
 #pragma unroll
   for (int t = 0; t < kU; ++t) {
-    if (disc[t] && kSumWordsMax) {
+    if (disc[t] && kSumWordsMax && !D) {
       const uint32_t gi = w[t] >> a.sum_shift;
       atomicOr(&a.sumv[gi >> 5], 1u << (gi & 31u));
     }
@@ -609,6 +609,9 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
 #ifndef PP_PULL_KC
 #define PP_PULL_KC 1
 #endif
+#ifndef PP_SUM_RESID
+#define PP_SUM_RESID 0  // with PP_SUM_WORDS > 0: the summary serves the residual tiers only
+#endif
 #ifndef PP_PULL_PF
 #define PP_PULL_PF 0  // 1: L2 prefetch of the next round's row head / offsets / caller id
 #endif
@@ -677,7 +680,18 @@ struct PullCtx {
 #ifdef PP_KO_PROBE  // timing-only knockout: every probed neighbour counts as visited
     return x != 0xFFFFFFFFu;
 #endif
-    if (kSumWordsMax) {
+    if (kSumWordsMax && !PP_SUM_RESID && !D) {
+      const uint32_t gi = x >> a.sum_shift;
+      if (!((ssum[gi >> 5] >> (gi & 31u)) & 1u)) return false;
+    }
+    return bit_test(vin, x);
+  }
+  // The residual tiers' probe (rows the 8-id head did not decide, mostly rows with no visited
+  // in-neighbour at all, whose every probe is negative): with PP_SUM_RESID the shared-memory
+  // summary answers "not visited" for a whole 2^sum_shift-vertex group without a global load.
+  __device__ __forceinline__ bool hit_res(uint32_t x) const {
+    if (!D && no_reuse) return a.depth[a.perm ? a.perm[x] : x] == d;
+    if (kSumWordsMax && !D) {
       const uint32_t gi = x >> a.sum_shift;
       if (!((ssum[gi >> 5] >> (gi & 31u)) & 1u)) return false;
     }
@@ -695,7 +709,7 @@ struct PullCtx {
 #pragma unroll
     for (int t = 1; t < 8; ++t)
       if ((Off)t == f0) xf = v.x[t];
-    if (hit(xf)) {
+    if (hit_res(xf)) {
       if (!found) {
         found = true;
         par = xf;
@@ -704,7 +718,7 @@ struct PullCtx {
     }
     bool h[8];
 #pragma unroll
-    for (int t = 1; t < 8; ++t) h[t] = (Off)t > f0 && q0 + (Off)t < e && hit(v.x[t]);
+    for (int t = 1; t < 8; ++t) h[t] = (Off)t > f0 && q0 + (Off)t < e && hit_res(v.x[t]);
 #pragma unroll
     for (int t = 1; t < 8; ++t) {
       if (h[t] && !found) {
@@ -731,7 +745,7 @@ struct PullCtx {
     a.depth[dpos] = d + 1;  // caller id of i (multi-rank: the block's slot i - lo)
 #endif
     if (PARENTS) a.parent[D ? i - (uint32_t)a.lo : i] = par;
-    if (kSumWordsMax && !in_item) {  // in-item finds reach the summary at item close
+    if (kSumWordsMax && !D && !in_item) {  // in-item finds reach the summary at item close
       const uint32_t gi = i >> a.sum_shift;
       atomicOr(&a.sumv[gi >> 5], 1u << (gi & 31u));
     }
@@ -1126,12 +1140,12 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
       vout[wbase + lane] = vw | fw;
       fr[wbase + lane] = fw;
     }
-    if (kSumWordsMax && a.sum_shift >= 5) {
+    if (kSumWordsMax && !D && a.sum_shift >= 5) {
       // the item's rows map into one summary word: one aggregated atomic per item
       const uint32_t gi = ((wbase + lane) * 32u) >> a.sum_shift;
       const uint32_t bits = __reduce_or_sync(kFull, fw ? (1u << (gi & 31u)) : 0u);
       if (lane == 0 && bits) atomicOr(&a.sumv[(((wbase * 32u) >> a.sum_shift)) >> 5], bits);
-    } else if (kSumWordsMax && fw) {
+    } else if (kSumWordsMax && !D && fw) {
       for (uint32_t x = fw; x; x &= x - 1) {
         const uint32_t gi = ((wbase + lane) * 32u + (__ffs(x) - 1)) >> a.sum_shift;
         atomicOr(&a.sumv[gi >> 5], 1u << (gi & 31u));
@@ -1243,7 +1257,7 @@ struct BfsShared {  // static part; the residual queues live in dynamic shared m
 };
 
 #ifndef PP_FUSED_SYNC
-#define PP_FUSED_SYNC 1
+#define PP_FUSED_SYNC 0  // measured: the unfused sync is ~1% faster
 #endif
 
 __device__ __forceinline__ void red_add_release_u64(unsigned long long* p, unsigned long long v) {
@@ -1302,6 +1316,7 @@ __device__ __forceinline__ bool level_sync(const BfsArgs<Off>& a, Acc& acc, Leve
       unsigned long long v;
       const unsigned long long t0 = global_timer_ns();
       while ((v = ld_acquire_u64(cnt)) < target) {
+        __nanosleep(16);  // back off: the pollers share the line the arrivals update
         if (global_timer_ns() - t0 > kWatchdogNs) {
           atomicExch(&a.status->error, (int)PP_ERR_TIMEOUT);
           atomicOr(cnt, kAbortBit);
@@ -1717,6 +1732,8 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
             atomicOr(&vnext[v >> 5], bit);
           }
         }
+        // every list bit must be in place before the convert below reads the bitmap
+        if (!level_barrier(false, a.bar, a.status, epoch, (unsigned)a.ncta)) return;
       }
       if (next == 0 && sh.lvl[5] != 0) {
         convert_phase<Off>(a, frout, nullptr, sel ? a.L1 : a.L0, sel ? a.H1 : a.H0, out, &sh.work);
