@@ -195,7 +195,7 @@ pp_status pp_bfs_options_default(pp_bfs_options* o);
  * level (GPU %globaltimer between grid barriers, incl. a following convert).
  * Arrays are caller-owned host memory of `capacity` entries (any may be NULL).
  * levels = number of levels executed (= max depth); reached = #vertices with
- * depth > 0; init_ns = device time of the initialisation phase. */
+ * depth > 0; init_ns = device time of the initialisation phase; cand / reached_nnz below. */
 typedef struct {
   int32_t levels;
   int64_t reached;
@@ -208,6 +208,10 @@ typedef struct {
   int64_t init_ns;
   int64_t exchanged_bytes; /* multi-rank: bytes this rank stored into its peers' exchange
                               buffers over the BFS (frontier slices / id lists + records) */
+  int64_t* cand;       /* per level: a pull's candidate rows (unvisited, not isolated: the rows
+                          its masked mxv computes), a push's frontier size */
+  int64_t reached_nnz; /* in-degree mass of the reached vertices = nnz of their rows of A^T
+                          (undirected: the traversed component's edge entries) */
 } pp_bfs_stats;
 
 pp_status pp_bfs(pp_graph g, int64_t source, const pp_bfs_options* opts, int32_t* depth,

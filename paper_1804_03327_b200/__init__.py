@@ -76,7 +76,8 @@ class pp_bfs_stats(ctypes.Structure):
                 ("capacity", ctypes.c_int32), ("dir", ctypes.POINTER(ctypes.c_int8)),
                 ("c", ctypes.POINTER(ctypes.c_int64)), ("m_f", ctypes.POINTER(ctypes.c_int64)),
                 ("m_u", ctypes.POINTER(ctypes.c_int64)), ("ns", ctypes.POINTER(ctypes.c_int64)),
-                ("init_ns", ctypes.c_int64), ("exchanged_bytes", ctypes.c_int64)]
+                ("init_ns", ctypes.c_int64), ("exchanged_bytes", ctypes.c_int64),
+                ("cand", ctypes.POINTER(ctypes.c_int64)), ("reached_nnz", ctypes.c_int64)]
 
 
 _vp, _i64, _u32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint32
@@ -486,13 +487,14 @@ def _stats(cap):
         return None, None
     arrays = dict(dir=np.zeros(cap, np.int8), c=np.zeros(cap, np.int64),
                   m_f=np.zeros(cap, np.int64), m_u=np.zeros(cap, np.int64),
-                  ns=np.zeros(cap, np.int64))
+                  ns=np.zeros(cap, np.int64), cand=np.zeros(cap, np.int64))
     st = pp_bfs_stats(0, 0, cap,
                       arrays["dir"].ctypes.data_as(ctypes.POINTER(ctypes.c_int8)),
                       arrays["c"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                       arrays["m_f"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                       arrays["m_u"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
-                      arrays["ns"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), 0, 0)
+                      arrays["ns"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), 0, 0,
+                      arrays["cand"].ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), 0)
     return st, arrays
 
 
@@ -502,7 +504,8 @@ def _stats_dict(st, arrays, cap):
     L = min(st.levels, cap)
     return dict(levels=st.levels, reached=st.reached, dir=arrays["dir"][:L], c=arrays["c"][:L],
                 m_f=arrays["m_f"][:L], m_u=arrays["m_u"][:L], ns=arrays["ns"][:L],
-                init_ns=st.init_ns, exchanged_bytes=st.exchanged_bytes)
+                init_ns=st.init_ns, exchanged_bytes=st.exchanged_bytes, cand=arrays["cand"][:L],
+                reached_nnz=st.reached_nnz)
 
 
 def make_vector(fmt: int, n: int, data=None, nnz: int = -1, capacity: int = 0) -> pp_vector:

@@ -46,6 +46,8 @@ struct BfsArgs {
   uint32_t* fr;  // frontier bitmap written by pull levels (push-from-bitmap)
   const uint32_t* __restrict__ head;  // first 8 in-neighbours of every row (pull), 32 B each
   const uint4* __restrict__ prec;     // PP_PULL_REC: {first in-neighbour, deg, caller id, begin}
+  const uint32_t* __restrict__ drec;  // PP_DENSE: 32-byte rows {6 in-neighbours, caller, in-degree}
+  long long n_noniso;                 // rows not pre-marked visited (isolated / padding)
   uint32_t* sumv;      // visited summary: bit per 2^sum_shift vertices, isolated excluded
   int sum_shift;
   uint32_t sum_words;
@@ -175,28 +177,30 @@ __device__ __forceinline__ bool level_barrier(bool narrow, GridBarrier* b, BfsSt
 
 // Per-lane accumulators of a level's counters, flushed once per phase.
 struct Acc {
-  unsigned long long c, mf, mfin, big;
+  unsigned long long c, mf, mfin, big, cand;  // cand: rows a pull computed (pp_bfs_stats.cand)
 };
 
 // CTA-level reduction, then one set of atomics per CTA (single-address L2 atomics
 // serialise; per-warp flushing cost ~3 x #warps atomics per level).
 __device__ __forceinline__ void flush_acc(Acc& acc, LevelCtr* out,
-                                          unsigned long long (*red)[4]) {
+                                          unsigned long long (*red)[5]) {
   const unsigned warp = threadIdx.x >> 5;
   unsigned long long c = warp_sum(acc.c), mf = warp_sum(acc.mf), mfin = warp_sum(acc.mfin),
-                     big = warp_sum(acc.big);
+                     big = warp_sum(acc.big), cd = warp_sum(acc.cand);
   if (lane_id() == 0) {
     red[warp][0] = c;
     red[warp][1] = mf;
     red[warp][2] = mfin;
     red[warp][3] = big;
+    red[warp][4] = cd;
   }
   __syncthreads();
   if (warp == 0) {  // warp 0 reduces the CTA's per-warp partials, lane 0 publishes
     const unsigned l = lane_id();
     const bool in = l < (unsigned)kBfsWarps;
     unsigned long long tc = warp_sum(in ? red[l][0] : 0ull), tm = warp_sum(in ? red[l][1] : 0ull),
-                       ti = warp_sum(in ? red[l][2] : 0ull), tb = warp_sum(in ? red[l][3] : 0ull);
+                       ti = warp_sum(in ? red[l][2] : 0ull), tb = warp_sum(in ? red[l][3] : 0ull),
+                       td = warp_sum(in ? red[l][4] : 0ull);
     if (l == 0) {
       if (tc) {
         atomicAdd(&out->c, tc);
@@ -204,9 +208,10 @@ __device__ __forceinline__ void flush_acc(Acc& acc, LevelCtr* out,
         atomicAdd(&out->m_fin, ti);
       }
       if (tb) atomicAdd(&out->nbig, tb);
+      if (td) atomicAdd(&out->cand, td);
     }
   }
-  acc.c = acc.mf = acc.mfin = acc.big = 0;
+  acc.c = acc.mf = acc.mfin = acc.big = acc.cand = 0;
 }
 
 // Work assignment: CTA b owns items b, b+G, b+2G, ... (interleaved, so every CTA sees the
@@ -622,8 +627,15 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
 constexpr int kC = PP_PULL_KC;  // candidates in flight per lane
 constexpr int kLaneMax = 16;    // residual rows with <= this many ids left: one lane each
 constexpr int kGroupMax = 512;   // <= this many: 8-lane groups; longer: the whole warp
-constexpr int kQ = 32 * kC + 64;  // residual-queue entries per warp (31 + 32*kC fits)
+#ifndef PP_RQ_EXTRA
+#define PP_RQ_EXTRA 32
+#endif
+// residual-queue entries per warp: a round parks at most 32*kC rows on top of <= 31 left over
+// (shared memory is carved out of L1, whose hits serve the visited-bitmap probes: keep it small)
+constexpr int kQ = 32 * kC + PP_RQ_EXTRA;
+static_assert(PP_RQ_EXTRA >= 31, "residual queue: 31 + 32*kC entries must fit");
 constexpr uint32_t kNone = 0xFFFFFFFFu;
+constexpr uint32_t kRelP = 0x80000000u;  // ResidualQ::rem flag: p is relative to coff[i]
 
 // Rows whose first sector did not decide them, parked per warp in shared memory and
 // processed 32 at a time so no lane idles behind one long row.
@@ -767,7 +779,12 @@ struct PullCtx {
       i = q.i[slot];
       par = q.par[slot];
       p = q.p[slot];
-      e = p + (Off)q.rem[slot];
+      uint32_t rem = q.rem[slot];
+      if (rem & kRelP) {  // dense pull: p is relative to the row's begin
+        rem &= ~kRelP;
+        p += a.coff[i];
+      }
+      e = p + (Off)rem;
       degin = q.degin[slot];
     }
     __syncwarp();
@@ -989,6 +1006,7 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
     const uint32_t cand = no_mask ? (own ? ~a.isolated[wbase + lane] : 0u) : unvisited;
     sfound[lane] = 0u;
     const unsigned cnt = __popc(cand);
+    acc.cand += cnt;
     const unsigned incl = warp_incl_scan(cnt);
     const unsigned excl = incl - cnt;
     const unsigned tot = __shfl_sync(kFull, incl, 31);
@@ -1155,6 +1173,226 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
   }
 }
 
+// ---- dense pull (PP_DENSE) ---------------------------------------------------------------
+// A pull level whose candidates are a large fraction of the rows (C2's heavy levels: ~100% and
+// 15-40% of the non-isolated rows) is bound by how many bytes of row data each SM keeps in
+// flight, not by the bytes themselves (one row per lane in flight, ~44 B, left
+// the heavy pull at ~2.6 TB/s even with every probe knocked out).  Here the row data is a
+// 32-byte record per row {in-neighbours 0..5, caller id, in-degree} streamed by the copy
+// engine: every warp owns a ring of kDenseR one-KB slots in shared memory; one lane issues a
+// cp.async.bulk of a bitmap word's 32 records into a free slot (completion counted on the
+// slot's mbarrier), so kDenseR KB per warp are in flight without holding registers.  Words
+// whose rows are all visited (or isolated / padding, pre-marked) are never fetched.  A step
+// takes kDenseU landed words: lane l owns row l of each, probes the visited snapshot for the
+// record's first in-neighbour, then (on a miss) the other five (Alg. 2 with masking, early
+// exit and operand reuse; first hit in sorted order = min-id parent, R14); rows
+// longer than 6 that no record id decides go to the residual tiers.  The word's found bits
+// come from one ballot, so v' and the frontier bitmap are written as whole words.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred P;\n mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, P;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+
+// Per-warp ring (shared memory): kDenseR slots of 32 records, their mbarriers, and the word
+// index / visited word each slot holds.
+struct DenseRing {
+  uint32_t* rec;             // [kDenseR][256]
+  unsigned long long* bar;   // [kDenseR]
+  uint32_t* word;            // [kDenseR]
+  uint32_t* vw;              // [kDenseR]
+};
+
+template <typename Off, bool PARENTS>
+__device__ void pull_dense(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
+                           uint32_t* __restrict__ vout, LevelCtr* out, int d, Acc& acc,
+                           uint32_t* sfound, ResidualQ<Off>& rq, unsigned* sctr, uint32_t* fr,
+                           const DenseRing& R, unsigned& seq) {
+  const unsigned lane = lane_id();
+  PullCtx<Off, PARENTS, false> C{a, vin, vout, d, true, false, acc, sfound, rq, nullptr,
+                                 a.H0, &out->work2, fr};
+  int qn = 0;
+  const unsigned nitems = a.nwords / kDenseIW;
+  const unsigned G = (unsigned)a.ncta;
+  const unsigned cta = cta_of(a);
+  const unsigned K = nitems > cta ? (nitems - cta + G - 1) / G : 0u;
+  // producer: the item whose words are being issued (CTA-interleaved items, grabbed by the
+  // CTA's warps in order), the words of it still to fetch, and their visited words (lane j < kPW)
+  unsigned pk = 0, pbase = 0, pneed = 0;
+  uint32_t pvw = 0xFFFFFFFFu;
+  bool more = true;
+  unsigned issued = seq, cons = seq;
+  // the item after the producer's is grabbed, and its visited words loaded, one item ahead
+  auto grab_item = [&](uint32_t& vw_out) {
+    unsigned j = 0;
+    if (lane == 0) j = atomicAdd(sctr, 1u);
+    j = __shfl_sync(kFull, j, 0);
+    vw_out = (j < K && lane < kDenseIW) ? vin[(cta + j * G) * kDenseIW + lane] : 0xFFFFFFFFu;
+    return j;
+  };
+  uint32_t nvw;
+  unsigned nk = grab_item(nvw);
+  auto next_item = [&]() {  // warp-uniform; false when the CTA has no items left
+    while (pneed == 0) {
+      if (nk >= K) return false;
+      pk = nk;
+      pbase = (cta + pk * G) * kDenseIW;
+      pvw = nvw;
+      nk = grab_item(nvw);
+      const bool need = pvw != 0xFFFFFFFFu;
+      pneed = __ballot_sync(kFull, need);
+      if (lane < kDenseIW && !need) {  // nothing to compute: v' = v, no discoveries
+        vout[pbase + lane] = 0xFFFFFFFFu;
+        fr[pbase + lane] = 0u;
+      }
+    }
+    return true;
+  };
+  auto issue = [&]() {  // fills the free slots; warp-uniform
+    while (more && issued - cons < (unsigned)kDenseR) {
+      if (pneed == 0 && !next_item()) {
+        more = false;
+        break;
+      }
+      const unsigned j = __ffs(pneed) - 1;
+      pneed &= pneed - 1;
+      const uint32_t vwj = __shfl_sync(kFull, pvw, j);
+      const unsigned slot = issued % (unsigned)kDenseR;
+      if (lane == 0) {
+        R.word[slot] = pbase + j;
+        R.vw[slot] = vwj;
+        mbar_arrive_tx(&R.bar[slot], 1024u);
+        bulk_g2s(R.rec + slot * 256u, a.drec + (size_t)(pbase + j) * 256u, 1024u, &R.bar[slot]);
+      }
+      ++issued;
+    }
+    __syncwarp();
+  };
+  issue();
+  while (cons != issued) {
+    const unsigned u = min((unsigned)kDenseU, issued - cons);
+    uint4 r0[kDenseU], r1[kDenseU];
+    uint32_t w[kDenseU], vw[kDenseU];
+#pragma unroll
+    for (int t = 0; t < kDenseU; ++t) {
+      if ((unsigned)t < u) {
+        const unsigned q = cons + t, slot = q % (unsigned)kDenseR;
+        if (!mbar_try(&R.bar[slot], (q / (unsigned)kDenseR) & 1u)) {
+          const unsigned long long t0 = global_timer_ns();
+          while (!mbar_try(&R.bar[slot], (q / (unsigned)kDenseR) & 1u))
+            if (global_timer_ns() - t0 > kWatchdogNs) __trap();  // a lost copy: fail, never hang
+        }
+        w[t] = R.word[slot];
+        vw[t] = R.vw[slot];
+        const uint4* rp = reinterpret_cast<const uint4*>(R.rec + slot * 256u) + 2 * lane;
+        r0[t] = rp[0];
+        r1[t] = rp[1];
+      } else {
+        w[t] = 0;
+        vw[t] = 0xFFFFFFFFu;
+        r0[t] = make_uint4(0, 0, 0, 0);
+        r1[t] = make_uint4(0, 0, 0, 0);
+      }
+    }
+    cons += u;
+    __syncwarp();  // every lane has its records: the slots may be refilled
+    issue();
+    bool cand[kDenseU], found[kDenseU];
+    uint32_t par[kDenseU];
+#pragma unroll
+    for (int t = 0; t < kDenseU; ++t) {
+      cand[t] = !((vw[t] >> lane) & 1u);
+      acc.cand += cand[t] ? 1u : 0u;
+      found[t] = cand[t] && r1[t].w > 0u && C.hit(r0[t].x);
+      par[t] = r0[t].x;
+    }
+#pragma unroll
+    for (int t = 0; t < kDenseU; ++t) {
+      const uint32_t dg = r1[t].w;
+      // PP_DENSE_SPEC: the other five ids are probed in the same round as the first (more
+      // probes, one dependent round less); else only for rows whose first id missed
+      if (cand[t] && (PP_DENSE_SPEC || !found[t]) && dg > 1u) {
+        const uint32_t x[5] = {r0[t].y, r0[t].z, r0[t].w, r1[t].x, r1[t].y};
+        constexpr int kX = kDenseHead - 1;  // ids after the first in the record
+        bool h[kX];
+#pragma unroll
+        for (int q = 0; q < kX; ++q) h[q] = dg > (uint32_t)(q + 1) && C.hit(x[q]);
+        const bool hit0 = found[t];  // the first id decides alone when it hits
+#pragma unroll
+        for (int q = kX - 1; q >= 0; --q)
+          if (h[q] && !hit0) {
+            found[t] = true;
+            par[t] = x[q];
+          }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < kDenseU; ++t) {
+      const uint32_t fb = __ballot_sync(kFull, found[t]);
+      if ((unsigned)t < u && lane == 0) {
+        vout[w[t]] = vw[t] | fb;
+        fr[w[t]] = fb;
+      }
+      const uint32_t i = w[t] * 32u + lane;
+      const uint32_t dg = r1[t].w;
+      if (found[t]) {
+        a.depth[r1[t].z] = d + 1;
+        if (PARENTS) a.parent[i] = par[t];
+        const Off odg = a.symmetric ? (Off)dg : (Off)(a.off[i + 1] - a.off[i]);
+        acc.c += 1;
+        acc.mf += (unsigned long long)odg;
+        acc.mfin += (unsigned long long)dg;
+        acc.big += odg >= (Off)kBig ? 1u : 0u;
+      }
+      // rows longer than the record that no record id decided: the residual tiers
+      const bool park = cand[t] && !found[t] && dg > (uint32_t)kDenseHead;
+      const unsigned pm = __ballot_sync(kFull, park);
+      if (park) {
+        const int slot = qn + __popc(pm & lanemask_lt());
+        rq.i[slot] = i;
+        rq.par[slot] = kNone;
+        if (PP_DENSE_RB) {  // the record carries the row begin
+          rq.p[slot] = (Off)r1[t].y + (Off)kDenseHead;
+          rq.rem[slot] = dg - (uint32_t)kDenseHead;
+        } else {  // relative: the batch adds coff[i] (one round trip per batch, not per step)
+          rq.p[slot] = (Off)kDenseHead;
+          rq.rem[slot] = (dg - (uint32_t)kDenseHead) | kRelP;
+        }
+        rq.degin[slot] = dg;
+      }
+      qn += __popc(pm);
+      __syncwarp();
+      while (qn >= 32) C.residual_batch(qn, 32, 0u, 0u);
+    }
+  }
+  if (qn > 0) C.residual_batch(qn, qn, 0u, 0u);
+  seq = issued;
+  __syncwarp();
+}
+
 // No-early-exit pull, second part: the long-row chunks emitted by tier 2, grabbed by every
 // warp of the grid (global counter: few chunks).  A chunk scans its ids in full (no early
 // exit), takes its first hit in sorted order, and the row's commit happens once, by the
@@ -1249,106 +1487,14 @@ __device__ __forceinline__ int decide(int rule, int dir, long long c_old, long l
 template <typename Off>
 struct BfsShared {  // static part; the residual queues live in dynamic shared memory
   uint32_t sfound[kBfsWarps][32];
-  unsigned long long red[kBfsWarps][4];
-  long long lvl[7];  // c, m_f, m_fin, nL, nH, nbig, nB of the level just finished
+  unsigned long long red[kBfsWarps][5];
+  long long lvl[8];  // c, m_f, m_fin, nL, nH, nbig, nB, cand of the level just finished
   unsigned work;     // CTA-local work counter (cta_grab)
   unsigned xlmask;   // multi-rank: senders whose last exchange was an id list ...
   unsigned xlen[kMaxRanks];  // ... and the lists' lengths
 };
 
-#ifndef PP_FUSED_SYNC
-#define PP_FUSED_SYNC 0  // measured: the unfused sync is ~1% faster
-#endif
 
-__device__ __forceinline__ void red_add_release_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-// End of a level, fused (tools/micro/gridbar.cu V5): the CTA's counter
-// partials are reduced (warps -> warp 0), thread 0 adds them to the level's counters and
-// arrives at the grid barrier with ONE red.release (ordering the counter atomics and every
-// write this CTA made before the first bar.sync), polls with ld.acquire (which invalidates
-// this SM's L1, so no trailing fence is needed), then lanes 0..6 of warp 0 read the seven
-// level counters in parallel.  Two CTA barriers instead of the four of flush_acc +
-// grid_barrier + read_level.
-template <typename Off>
-__device__ __forceinline__ bool level_sync(const BfsArgs<Off>& a, Acc& acc, LevelCtr* out,
-                                           BfsShared<Off>& sh, unsigned& epoch, long long t_lvl,
-                                           int d) {
-  __shared__ int s_ok;
-  const unsigned warp = threadIdx.x >> 5, lane = lane_id();
-  {
-    const unsigned long long c = warp_sum(acc.c), mf = warp_sum(acc.mf), mfin = warp_sum(acc.mfin),
-                             big = warp_sum(acc.big);
-    if (lane == 0) {
-      sh.red[warp][0] = c;
-      sh.red[warp][1] = mf;
-      sh.red[warp][2] = mfin;
-      sh.red[warp][3] = big;
-    }
-    acc.c = acc.mf = acc.mfin = acc.big = 0;
-  }
-  __syncthreads();
-  // debug phases (pp_bfs_debug_phases): plane 1 = every warp of the CTA done, plane 2 = the
-  // grid barrier released (times from the level's loop top)
-  const bool dbg = a.dbg && threadIdx.x == 0 && d - 1 < a.dbg_levels;
-  const size_t plane = (size_t)a.dbg_levels * (size_t)a.ncta;
-  const size_t slot = (size_t)(d - 1) * a.ncta + (blockIdx.x - a.cta_base);
-  if (dbg) a.dbg[plane + slot] = (long long)global_timer_ns() - t_lvl;
-  if (warp == 0) {
-    const bool in = lane < (unsigned)kBfsWarps;
-    const unsigned long long tc = warp_sum(in ? sh.red[lane][0] : 0ull),
-                             tm = warp_sum(in ? sh.red[lane][1] : 0ull),
-                             ti = warp_sum(in ? sh.red[lane][2] : 0ull),
-                             tb = warp_sum(in ? sh.red[lane][3] : 0ull);
-    int ok = 1;
-    if (lane == 0) {
-      if (tc) {
-        atomicAdd(&out->c, tc);
-        atomicAdd(&out->m_f, tm);
-        atomicAdd(&out->m_fin, ti);
-      }
-      if (tb) atomicAdd(&out->nbig, tb);
-      ++epoch;
-      const unsigned long long target = (unsigned long long)epoch * (unsigned)a.ncta;
-      unsigned long long* cnt = reinterpret_cast<unsigned long long*>(&a.bar->count);
-      red_add_release_u64(cnt, 1ull);
-      unsigned long long v;
-      const unsigned long long t0 = global_timer_ns();
-      while ((v = ld_acquire_u64(cnt)) < target) {
-        __nanosleep(16);  // back off: the pollers share the line the arrivals update
-        if (global_timer_ns() - t0 > kWatchdogNs) {
-          atomicExch(&a.status->error, (int)PP_ERR_TIMEOUT);
-          atomicOr(cnt, kAbortBit);
-          v = kAbortBit;
-          break;
-        }
-      }
-      ok = (v & kAbortBit) ? 0 : 1;
-      if (dbg) a.dbg[2 * plane + slot] = (long long)global_timer_ns() - t_lvl;
-    }
-    ok = __shfl_sync(kFull, ok, 0);  // also orders lanes 1..6 after lane 0's acquire
-    if (lane < 7) {
-      long long x = 0;
-      switch (lane) {
-        case 0: x = (long long)ld_relaxed_u64(&out->c); break;
-        case 1: x = (long long)ld_relaxed_u64(&out->m_f); break;
-        case 2: x = (long long)ld_relaxed_u64(&out->m_fin); break;
-        case 3: x = (long long)ld_relaxed_u32(&out->nL); break;
-        case 4: x = (long long)ld_relaxed_u32(&out->nH); break;
-        case 5: x = (long long)ld_relaxed_u64(&out->nbig); break;
-        default: x = (long long)ld_relaxed_u32(&out->nB); break;
-      }
-      sh.lvl[lane] = x;
-    }
-    if (lane == 0) {
-      s_ok = ok;
-      sh.work = 0u;
-    }
-  }
-  __syncthreads();
-  return s_ok != 0;
-}
 
 // thread 0 reads a level's counters once (post-barrier) and broadcasts them via smem
 template <typename Off>
@@ -1361,6 +1507,7 @@ __device__ __forceinline__ void read_level(const LevelCtr* out, BfsShared<Off>& 
     sh.lvl[4] = (long long)ld_relaxed_u32(&out->nH);
     sh.lvl[5] = (long long)ld_relaxed_u64(&out->nbig);
     sh.lvl[6] = (long long)ld_relaxed_u32(&out->nB);
+    sh.lvl[7] = (long long)ld_relaxed_u64(&out->cand);
     sh.work = 0u;
   }
   __syncthreads();
@@ -1454,6 +1601,7 @@ __device__ bool exchange(const BfsArgs<Off>& a, BfsShared<Off>& sh, const uint32
     rec[2] = (unsigned long long)(sh.lvl[2] + extra_mfin);
     rec[3] = (unsigned long long)sh.lvl[5];
     rec[4] = lst ? (unsigned long long)nx : ~0ull;  // list length, or ~0: bitmap slice
+    rec[5] = (unsigned long long)sh.lvl[7];
   }
   if (cta_of(a) == 0 && threadIdx.x == 0 && P > 1)
     a.status->xbytes += (long long)(P - 1) * ((lst ? 4ll * nx : 4ll * a.wcnt) + 40);
@@ -1462,7 +1610,7 @@ __device__ bool exchange(const BfsArgs<Off>& a, BfsShared<Off>& sh, const uint32
   if (!grid_barrier(a.bar, a.status, epoch, (unsigned)a.ncta)) return false;
   if (P > 1 && !rank_rendezvous(a, a.xseq + (unsigned long long)d)) return false;
   if (threadIdx.x == 0) {
-    long long c = 0, mf = 0, mfin = 0, big = 0;
+    long long c = 0, mf = 0, mfin = 0, big = 0, cd = 0;
     unsigned lmask = 0;
     for (int q = 0; q < P; ++q) {
       const unsigned long long* rec = a.xcnt + ((size_t)par * kMaxRanks + (size_t)q) * 8u;
@@ -1470,6 +1618,7 @@ __device__ bool exchange(const BfsArgs<Off>& a, BfsShared<Off>& sh, const uint32
       mf += (long long)ld_relaxed_u64(rec + 1);
       mfin += (long long)ld_relaxed_u64(rec + 2);
       big += (long long)ld_relaxed_u64(rec + 3);
+      cd += (long long)ld_relaxed_u64(rec + 5);
       const unsigned long long ln = ld_relaxed_u64(rec + 4);
       if (q != me && ln != ~0ull) {
         lmask |= 1u << q;
@@ -1480,10 +1629,23 @@ __device__ bool exchange(const BfsArgs<Off>& a, BfsShared<Off>& sh, const uint32
     sh.lvl[1] = mf;
     sh.lvl[2] = mfin;
     sh.lvl[5] = big;
+    sh.lvl[7] = cd;
     sh.xlmask = lmask;
   }
   __syncthreads();
   return true;
+}
+
+// dynamic shared memory: residual queues, visited summary, then (PP_DENSE, 128-byte aligned)
+// the warps' bulk-copy rings, their mbarriers and slot metadata
+template <typename Off>
+__host__ __device__ constexpr size_t dense_ring_offset() {
+  return (sizeof(ResidualQ<Off>) * kBfsWarps + sizeof(uint32_t) * kSumWordsMax + 127) & ~(size_t)127;
+}
+template <typename Off, bool D = false>
+__host__ __device__ constexpr size_t dyn_smem_bytes() {  // D (multi-rank): no dense rings
+  return (kDenseR && !D) ? dense_ring_offset<Off>() + (size_t)kBfsWarps * kDenseR * (1024 + 8 + 4 + 4)
+                         : sizeof(ResidualQ<Off>) * kBfsWarps + sizeof(uint32_t) * kSumWordsMax;
 }
 
 // The BFS loop (Algorithm 1) run by the CTAs of one rank.  D = multi-rank (1D
@@ -1496,6 +1658,23 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
   ResidualQ<Off>* rqs = reinterpret_cast<ResidualQ<Off>*>(dyn_smem);
   uint32_t* ssum = reinterpret_cast<uint32_t*>(dyn_smem + sizeof(ResidualQ<Off>) * kBfsWarps);
   const unsigned warp = threadIdx.x >> 5;
+  DenseRing ring{nullptr, nullptr, nullptr, nullptr};
+  unsigned dseq = 0;  // this warp's bulk copies issued (= consumed between levels)
+  if constexpr (!D && kDenseR > 0) {
+    unsigned char* rb = dyn_smem + dense_ring_offset<Off>();
+    ring.rec = reinterpret_cast<uint32_t*>(rb) + (size_t)warp * kDenseR * 256;
+    unsigned char* mb = rb + (size_t)kBfsWarps * kDenseR * 1024;
+    ring.bar = reinterpret_cast<unsigned long long*>(mb) + (size_t)warp * kDenseR;
+    uint32_t* meta = reinterpret_cast<uint32_t*>(mb + (size_t)kBfsWarps * kDenseR * 8);
+    ring.word = meta + (size_t)warp * kDenseR;
+    ring.vw = meta + (size_t)kBfsWarps * kDenseR + (size_t)warp * kDenseR;
+    if (a.drec && lane_id() == 0) {
+      for (int r = 0; r < kDenseR; ++r) mbar_init(&ring.bar[r], 1u);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncwarp();
+  }
   const unsigned cta = cta_of(a);
   const unsigned long long gtid = (unsigned long long)cta * blockDim.x + threadIdx.x;
   const unsigned long long gsize = (unsigned long long)a.ncta * blockDim.x;
@@ -1526,7 +1705,7 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
     m_u = a.nnz - (long long)indeg_s;
   }
   long long reached = 1;
-  Acc acc{0, 0, 0, 0};
+  Acc acc{0, 0, 0, 0, 0};
   bool from_bits = false;  // next push reads the previous level's frontier bitmap
   // edges the next push expands (a latency heuristic only; multi-rank: this rank's part)
   long long mf_last = (long long)(a.off[s + 1] - a.off[s]);
@@ -1656,8 +1835,18 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
         for (unsigned t = threadIdx.x; t < a.sum_words; t += blockDim.x) ssum[t] = a.sumv[t];
         __syncthreads();
       }
-      pull_phase<Off, PARENTS, D>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp],
-                                  ssum, &sh.work, frout, a.gwork + (size_t)(d & (kRing - 1)) * kMaxCtas);
+      bool dense = false;
+      if constexpr (!D && kDenseR > 0)
+        dense = a.drec != nullptr && a.toggles == 0u && !a.narrow &&
+                (a.n_noniso - reached) * 8 >= a.n_noniso * (long long)PP_DENSE_MIN8;
+      if (dense) {
+        if constexpr (!D && kDenseR > 0)
+          pull_dense<Off, PARENTS>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp],
+                                   &sh.work, frout, ring, dseq);
+      } else {
+        pull_phase<Off, PARENTS, D>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp],
+                                    ssum, &sh.work, frout, a.gwork + (size_t)(d & (kRing - 1)) * kMaxCtas);
+      }
       if (!D && (a.toggles & PP_OPT_NO_EARLYEXIT)) {  // ablation arms: long rows grid-wide
         if (!level_barrier(a.narrow, a.bar, a.status, epoch, (unsigned)a.ncta)) return;
         const unsigned nch = ld_relaxed_u32(&out->work2);
@@ -1666,13 +1855,9 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
     }
     if (a.dbg && threadIdx.x == 0 && d - 1 < a.dbg_levels)
       a.dbg[(size_t)(d - 1) * a.ncta + cta] = (long long)global_timer_ns() - t_lvl;
-    if (PP_FUSED_SYNC && !a.narrow) {
-      if (!level_sync(a, acc, out, sh, epoch, t_lvl, d)) return;
-    } else {
-      flush_acc(acc, out, sh.red);
-      if (!level_barrier(a.narrow, a.bar, a.status, epoch, (unsigned)a.ncta)) return;
-      read_level(out, sh);
-    }
+    flush_acc(acc, out, sh.red);
+    if (!level_barrier(a.narrow, a.bar, a.status, epoch, (unsigned)a.ncta)) return;
+    read_level(out, sh);
     if (D && !exchange<Off>(a, sh, frout, d, epoch, (d == 1) ? indeg_s_own : 0, gtid, gsize,
                             dir == 0, out))
       return;
@@ -1692,6 +1877,7 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
       st.c = c_new;
       st.m_f = mf;
       st.m_u = m_u;
+      st.cand = dir ? sh.lvl[7] : c_old;  // pull: rows computed; push: frontier expanded
       st.t_ns = (long long)global_timer_ns();
       a.stats[d - 1] = st;
     }
@@ -1768,6 +1954,7 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
   if (cta == 0 && threadIdx.x == 0) {
     a.status->levels = d;
     a.status->reached = reached;
+    a.status->reached_nnz = (D ? a.in_total : a.nnz) - m_u;  // in-degree mass of the reached
   }
   if (D && a.nranks > 1) {
     // no rank leaves while a peer may still read its own buffers for this BFS: a fast rank's
@@ -1807,10 +1994,7 @@ __global__ void __launch_bounds__(kBfsBlock, 1) bfs_ranks(const BfsArgs<Off>* __
   bfs_body<Off, PARENTS, true>(sa);
 }
 
-template <typename Off>
-constexpr size_t dyn_smem_bytes() {
-  return sizeof(ResidualQ<Off>) * kBfsWarps + sizeof(uint32_t) * kSumWordsMax;
-}
+
 
 // Cooperative grid size per (device, kernel) (and the dynamic shared-memory attribute, which
 // is per device too): computed once, guarded by a mutex.
@@ -1909,6 +2093,8 @@ static cudaError_t launch_off(pp_graph g, uint32_t source, int mode, int rule, d
   a.sumv = g->sumv;
   a.head = g->head;
   a.prec = g->prec;
+  a.drec = g->drec;
+  a.n_noniso = g->n_noniso;
   a.sum_shift = g->sum_shift;
   a.sum_words = g->sum_words;
   a.L0 = reinterpret_cast<uint4*>(g->L[0]);
@@ -1982,7 +2168,7 @@ static cudaError_t launch_ranks_t(pp_graph* gs, int P, uint32_t source, int mode
                                   uint32_t* const* parent) {
   pp_graph g0 = gs[0];
   const void* fn = (const void*)bfs_ranks<Off, PARENTS>;
-  const int grid = coop_grid(fn, dyn_smem_bytes<Off>());
+  const int grid = coop_grid(fn, dyn_smem_bytes<Off, true>());
   if (grid < P) return cudaErrorInvalidConfiguration;
   BfsArgs<Off> h[kMaxRanks];
   memset(h, 0, sizeof(h));
@@ -2061,7 +2247,7 @@ static cudaError_t launch_ranks_t(pp_graph* gs, int P, uint32_t source, int mode
   const BfsArgs<Off>* dall = (const BfsArgs<Off>*)g0->dargs;
   void* params[] = {(void*)&dall, (void*)&P};
   g0->ctx->launches += 1;
-  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBfsBlock), params, dyn_smem_bytes<Off>(), st);
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kBfsBlock), params, dyn_smem_bytes<Off, true>(), st);
 }
 
 cudaError_t launch_bfs_ranks(pp_graph* graphs, int nranks, uint32_t source, int mode, int rule,

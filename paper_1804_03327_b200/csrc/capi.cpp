@@ -81,7 +81,7 @@ void free_graph(pp_graph g) {
                   g->sbits[0], g->sbits[1], g->sbits[2], g->sbits[3], g->sblock, g->hubq, g->scount,
                   g->dtmp[0], g->dtmp[1], g->dbg, g->perm, g->rank, g->pint, g->vrec,
                   g->rbits[0], g->rbits[1], g->rbits[2], g->rbits[3],
-                  g->odeg, g->xbuf, g->dargs, g->gwork, g->prec};
+                  g->odeg, g->xbuf, g->dargs, g->gwork, g->prec, g->drec};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (g->status_host) cudaFreeHost(g->status_host);
@@ -613,12 +613,18 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t row_lo, int64_t row_hi,
   if ((s = dalloc(&g->isolated, g->nwords, &bytes, "isolated")) != PP_OK) return s;
   if ((s = dalloc(&g->head, (size_t)n * 8, &bytes, "row heads")) != PP_OK) return s;
   if (kPullRec && !g->off64 && (s = dalloc(&g->prec, (size_t)n, &bytes, "row records")) != PP_OK) return s;
-  PP_CK(cudaMemsetAsync(g->scount, 0, 4 * sizeof(unsigned long long), st), "memset");
+  if (kDense && !g->off64) {
+    const size_t words = (size_t)g->nwords * 32 * 8;  // 32 B per row incl. padding rows
+    if ((s = dalloc(&g->drec, words, &bytes, "dense pull records")) != PP_OK) return s;
+    PP_CK(cudaMemsetAsync(g->drec, 0, words * 4, st), "memset dense records");
+  }
+  PP_CK(cudaMemsetAsync(g->scount, 0, 5 * sizeof(unsigned long long), st), "memset");
   PP_CK(launch_graph_prepare(g, d_off64, d_coff64, g->scount, &ctx->launches), "prepare kernels");
-  PP_CK(cudaMemcpyAsync(g->scount_host, g->scount, 32, cudaMemcpyDeviceToHost, st), "copy");
+  PP_CK(cudaMemcpyAsync(g->scount_host, g->scount, 40, cudaMemcpyDeviceToHost, st), "copy");
   PP_CK(cudaStreamSynchronize(st), "sync");
   g->hcap = (int64_t)std::max(g->scount_host[0], g->scount_host[1]);
   g->max_out_deg = (int64_t)g->scount_host[2];
+  g->n_noniso = (int64_t)g->nwords * 32 - (int64_t)g->scount_host[4];
 
   // BFS / mxv working set
   for (int k = 0; k < 2; ++k) {
@@ -905,6 +911,7 @@ static pp_status finish_bfs(pp_graph g, pp_bfs_stats* stats, bool sync) {
     stats->levels = g->status_host->levels;
     stats->init_ns = g->status_host->t_init - g->status_host->t_start;
     stats->reached = g->status_host->reached;
+    stats->reached_nnz = g->status_host->reached_nnz;
     stats->exchanged_bytes = g->dist ? g->status_host->xbytes : 0;
     const int m = std::min(std::min(stats->capacity, g->status_host->levels), g->stats_cap);
     if (m > 0) {
@@ -916,6 +923,7 @@ static pp_status finish_bfs(pp_graph g, pp_bfs_stats* stats, bool sync) {
         if (stats->c) stats->c[k] = hs[k].c;
         if (stats->m_f) stats->m_f[k] = hs[k].m_f;
         if (stats->m_u) stats->m_u[k] = hs[k].m_u;
+        if (stats->cand) stats->cand[k] = hs[k].cand;
       }
     }
   }

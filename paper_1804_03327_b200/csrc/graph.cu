@@ -13,7 +13,9 @@ __global__ void k_off_narrow(const int64_t* __restrict__ in, Off* __restrict__ o
 
 // bit v of word w: 1 when v >= n (padding) or v has neither in- nor out-edges.
 __global__ void k_isolated(const int64_t* __restrict__ off, const int64_t* __restrict__ coff,
-                           int64_t n, uint32_t nwords, uint32_t* __restrict__ iso) {
+                           int64_t n, uint32_t nwords, uint32_t* __restrict__ iso,
+                           unsigned long long* __restrict__ niso) {
+  unsigned long long cnt = 0;
   for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < nwords;
        w += gridDim.x * blockDim.x) {
     uint32_t bits = 0;
@@ -24,6 +26,30 @@ __global__ void k_isolated(const int64_t* __restrict__ off, const int64_t* __res
       bits |= (isolated ? 1u : 0u) << b;
     }
     iso[w] = bits;
+    cnt += (unsigned long long)__popc(bits);
+  }
+  if (cnt) atomicAdd(niso, cnt);
+}
+
+// PP_DENSE: the dense pull's row record {in-neighbours 0..5 (0xFFFFFFFF-padded), caller id,
+// in-degree}, 32 bytes, so one 1 KB bulk copy brings a bitmap word's 32 rows.  Rows >= n
+// (padding of the last words) stay zero (in-degree 0; they are pre-marked visited anyway).
+__global__ void k_drec(const int64_t* __restrict__ coff, const uint32_t* __restrict__ cidx,
+                       const uint32_t* __restrict__ perm, int64_t n, uint32_t* __restrict__ drec) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = coff[v], d = coff[v + 1] - b;
+    uint4 r0, r1;
+    r0.x = d > 0 ? cidx[b] : 0xFFFFFFFFu;
+    r0.y = d > 1 ? cidx[b + 1] : 0xFFFFFFFFu;
+    r0.z = d > 2 ? cidx[b + 2] : 0xFFFFFFFFu;
+    r0.w = d > 3 ? cidx[b + 3] : 0xFFFFFFFFu;
+    r1.x = d > 4 ? cidx[b + 4] : 0xFFFFFFFFu;
+    r1.y = PP_DENSE_RB ? (uint32_t)b : (d > 5 ? cidx[b + 5] : 0xFFFFFFFFu);
+    r1.z = perm ? perm[v] : (uint32_t)v;
+    r1.w = (uint32_t)d;
+    reinterpret_cast<uint4*>(drec)[2 * v] = r0;
+    reinterpret_cast<uint4*>(drec)[2 * v + 1] = r1;
   }
 }
 
@@ -165,7 +191,12 @@ cudaError_t launch_graph_prepare(pp_graph g, const int64_t* d_off64, const int64
     *launches += 1;
     k_prec<<<blocks, kBlock, 0, st>>>(d_coff64, g->cidx, g->perm, g->n, g->prec);
   }
-  k_isolated<<<blocks, kBlock, 0, st>>>(d_off64, d_coff64, g->n, g->nwords, g->isolated);
+  if (g->drec) {
+    *launches += 1;
+    k_drec<<<blocks, kBlock, 0, st>>>(d_coff64, g->cidx, g->perm, g->n, g->drec);
+  }
+  k_isolated<<<blocks, kBlock, 0, st>>>(d_off64, d_coff64, g->n, g->nwords, g->isolated,
+                                        d_scratch + 4);
   k_hcap<<<blocks, kBlock, 0, st>>>(d_off64, g->n, d_scratch + 0, d_scratch + 2);
   k_hcap<<<blocks, kBlock, 0, st>>>(d_coff64, g->n, d_scratch + 1, d_scratch + 3);
   return cudaGetLastError();

@@ -12,8 +12,14 @@ namespace pp {
 // ---- tunables ---------------------------------------------------------------
 constexpr int kBlock = 256;        // threads per CTA of every kernel
 constexpr int kWarps = kBlock / 32;
-constexpr unsigned kHeavy = 128;   // out-degree >= kHeavy: expanded as kChunk-edge chunks
-constexpr unsigned kChunk = 128;   // edges per heavy chunk = one 4-deep warp iteration
+#ifndef PP_HEAVY
+#define PP_HEAVY 64
+#endif
+#ifndef PP_CHUNK
+#define PP_CHUNK 64
+#endif
+constexpr unsigned kHeavy = PP_HEAVY;  // out-degree >= kHeavy: expanded as kChunk-edge chunks
+constexpr unsigned kChunk = PP_CHUNK;  // edges per heavy chunk (whole warp iterations)
 constexpr unsigned kSelfChunks = 32;  // heavy vertices with more chunks are hubs (block
                                       // descriptors, one per 32 chunks)
 constexpr int kRing = 4;           // level-counter ring
@@ -47,6 +53,35 @@ constexpr bool kVrec = PP_VREC != 0;  // relabelled graphs: per-vertex {begin, d
 #define PP_PULL_REC 0
 #endif
 constexpr bool kPullRec = PP_PULL_REC != 0;  // pull: 16-byte row records instead of 32-byte heads
+#ifndef PP_DENSE
+#define PP_DENSE 1
+#endif
+// dense pull levels (single GPU, 32-bit offsets): 32-byte row records streamed into shared
+// memory by bulk copies (cp.async.bulk + mbarrier), one warp ring of kDenseR 1 KB slots
+constexpr bool kDense = PP_DENSE != 0;
+#ifndef PP_DENSE_R
+#define PP_DENSE_R 1
+#endif
+#ifndef PP_DENSE_U
+#define PP_DENSE_U 1
+#endif
+#ifndef PP_DENSE_SPEC
+#define PP_DENSE_SPEC 0
+#endif
+#ifndef PP_DENSE_MIN8
+#define PP_DENSE_MIN8 2
+#endif
+constexpr int kDenseR = kDense ? PP_DENSE_R : 0;  // ring slots (32 rows x 32 B) per warp
+constexpr int kDenseU = PP_DENSE_U;               // slots (bitmap words) processed per step
+#ifndef PP_DENSE_RB
+#define PP_DENSE_RB 0
+#endif
+#ifndef PP_DENSE_IW
+#define PP_DENSE_IW 8
+#endif
+// in-neighbour ids per dense record: 6, or 5 and the row begin (PP_DENSE_RB)
+constexpr int kDenseHead = PP_DENSE_RB ? 5 : 6;
+constexpr unsigned kDenseIW = PP_DENSE_IW;  // bitmap words per dense work item
 constexpr int kMaxRanks = 8;  // 1D row partition: ranks per multi-rank group (one node)
 constexpr int kMaxCtas = 1024;  // persistent grid size bound (per-CTA work counters)
 
@@ -59,7 +94,8 @@ struct LevelCtr {
   unsigned long long m_f;    // sum of their out-degrees (Eq. 1)
   unsigned long long m_fin;  // sum of their in-degrees (m_u update, directed graphs)
   unsigned long long nbig;   // discoveries with out-degree >= kBig (pull levels)
-  unsigned int pad0[24];
+  unsigned long long cand;   // rows the pull computed (unvisited, non-isolated)
+  unsigned int pad0[22];
   unsigned int nL;           // next frontier: light-list length
   unsigned int pad1[31];
   unsigned int nH, nB;       // next frontier: heavy-chunk count, hub block descriptors
@@ -73,6 +109,7 @@ struct LevelStat {
   int dir;
   int pad;
   long long c, m_f, m_u;
+  long long cand;  // pull: rows computed; push: frontier vertices expanded
   long long t_ns;  // %globaltimer when the level's barrier released (block 0)
 };
 
@@ -107,6 +144,7 @@ struct BfsStatus {
   int error;   // 0 or pp_status
   int levels;  // levels executed
   long long reached;
+  long long reached_nnz;      // in-degree mass of the reached vertices
   long long t_start, t_init;  // %globaltimer at kernel entry / after the init barrier
   long long xbytes;           // multi-rank: bytes this rank stored into its peers' buffers
 };
@@ -140,6 +178,9 @@ struct pp_graph_s {
   uint32_t* cidx = nullptr;
   uint32_t* isolated = nullptr;  // nwords: bit = no in- and no out-edges, or padding
   uint32_t* head = nullptr;      // 8n: first 8 in-neighbours of every row (pull heads)
+  uint32_t* drec = nullptr;      // PP_DENSE: per row {first 6 in-neighbours, caller id, in-degree}
+                                 // (32 B; nwords*32 rows, padding rows zero)
+  int64_t n_noniso = 0;          // rows not marked isolated / padding
   uint4* prec = nullptr;         // PP_PULL_REC: per row {first in-neighbour, in-degree, caller id,
                                  // row begin} (32-bit offsets only)
   // PP_GRAPH_RELABEL: internal id = rank by decreasing degree (relabel.cu)

@@ -9,6 +9,7 @@ import torch
 
 import oracle
 import synth
+from stats_defs import check_cand
 
 pytestmark = pytest.mark.gpu
 
@@ -52,6 +53,7 @@ def check(ctx, g, gT, G, s, mode, rule, toggles=0, parents=True, exp=None):
     assert np.array_equal(st["c"], t["c"])
     assert np.array_equal(st["m_f"], t["m_f"])
     assert np.array_equal(st["m_u"], t["m_u"])
+    check_cand(g, gT, ed, st, no_mask=bool(toggles & pp.PP_OPT_NO_MASKING))
     return st
 
 

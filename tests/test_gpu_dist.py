@@ -17,6 +17,7 @@ import torch
 
 import oracle
 import synth
+from stats_defs import check_cand
 
 pytestmark = pytest.mark.gpu
 pp = pytest.importorskip("paper_1804_03327_b200")
@@ -96,6 +97,7 @@ def test_team_matches_oracle(graphs, name, P):
             assert np.array_equal(st["dir"], t["dir"]), (name, P, s, mode, rule, st["dir"], t["dir"])
             assert np.array_equal(st["c"], t["c"]) and np.array_equal(st["m_f"], t["m_f"])
             assert np.array_equal(st["m_u"], t["m_u"])
+            check_cand(g, gT, exp, st)
     team.close()
 
 
