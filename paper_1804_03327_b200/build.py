@@ -31,11 +31,12 @@ def build(force=False, verbose=False):
     extra = [f"-D{k}={os.environ[k]}" for k in ("PP_BFS_BLOCK", "PP_SUM_WORDS", "PP_PULL_WORDS", "PP_PULL_KC", "PP_SOLO_EDGES", "PP_LOWLAT_EDGES", "PP_NARROW_MAX_EDGES", "PP_NARROW_MAX_DEG", "PP_VREC", "PP_INIT_VEC", "PP_STREAM_U", "PP_SSSP_G", "PP_SSSP_HEAVY") if os.environ.get(k)]
     extra += ["-DPP_IDX_NOALLOC"] if os.environ.get("PP_IDX_NOALLOC") else []
     extra += [f"-D{k}" for k in ("PP_KO_DEPTH", "PP_KO_PROBE", "PP_KO_RESID") if os.environ.get(k)]
-    extra += [f"-D{k}={os.environ[k]}" for k in ("PP_PULL_REC", "PP_FAST_NTH", "PP_PUSH_KU", "PP_STEAL",
-                                                   "PP_PULL_PF", "PP_FUSED_SYNC", "PP_LOWLAT_VREC",
-                                                   "PP_PF_ROWS", "PP_SUM_RESID", "PP_DENSE", "PP_DENSE_R",
-                                                   "PP_DENSE_U", "PP_DENSE_MIN8", "PP_CHUNK", "PP_HEAVY", "PP_RQ_EXTRA", "PP_DENSE_SPEC",
-                                                   "PP_DENSE_RB", "PP_DENSE_IW") if os.environ.get(k)]
+    extra += [f"-D{k}={os.environ[k]}" for k in ("PP_FAST_NTH", "PP_PUSH_KU", "PP_STEAL",
+                                                   "PP_PULL_PF", "PP_LOWLAT_VREC", "PP_PF_ROWS",
+                                                   "PP_SUM_RESID", "PP_DENSE", "PP_DENSE_R",
+                                                   "PP_DENSE_MIN8", "PP_DENSE_IW", "PP_SPARSE_REC",
+                                                   "PP_CHUNK", "PP_HEAVY", "PP_RQ_EXTRA", "PP_NOINLINE_PULL")
+              if os.environ.get(k)]
     odir = os.path.join(HERE, "build")
     os.makedirs(odir, exist_ok=True)
     cflags = [f for f in FLAGS if f != "-shared"]

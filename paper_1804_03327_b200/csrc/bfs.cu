@@ -45,7 +45,6 @@ struct BfsArgs {
   uint32_t* vis1;
   uint32_t* fr;  // frontier bitmap written by pull levels (push-from-bitmap)
   const uint32_t* __restrict__ head;  // first 8 in-neighbours of every row (pull), 32 B each
-  const uint4* __restrict__ prec;     // PP_PULL_REC: {first in-neighbour, deg, caller id, begin}
   const uint32_t* __restrict__ drec;  // PP_DENSE: 32-byte rows {6 in-neighbours, caller, in-degree}
   long long n_noniso;                 // rows not pre-marked visited (isolated / padding)
   uint32_t* sumv;      // visited summary: bit per 2^sum_shift vertices, isolated excluded
@@ -611,6 +610,15 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
   }
 }
 
+#ifndef PP_NOINLINE_PULL
+#define PP_NOINLINE_PULL 0
+#endif
+// PP_NOINLINE_PULL: the pull phases as called functions (code layout / register A-B only)
+#if PP_NOINLINE_PULL
+#define PP_PULL_INLINE __noinline__
+#else
+#define PP_PULL_INLINE
+#endif
 #ifndef PP_PULL_KC
 #define PP_PULL_KC 1
 #endif
@@ -919,7 +927,7 @@ struct PullCtx {
 // data is local (row i - lo), the probed in-neighbour ids are global and test the
 // replicated visited snapshot.
 template <typename Off, bool PARENTS, bool D>
-__device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
+PP_PULL_INLINE __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
                            uint32_t* __restrict__ vout, LevelCtr* out, int d, Acc& acc,
                            uint32_t* sfound, ResidualQ<Off>& rq, const uint32_t* ssum,
                            unsigned* sctr, uint32_t* fr, unsigned* gwork) {
@@ -928,6 +936,10 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
   const unsigned wb0 = D ? a.wlo : 0u;
   const uint32_t lo = D ? (uint32_t)a.lo : 0u;
   const bool no_mask = (a.toggles & PP_OPT_NO_MASKING) != 0;
+  // PP_SPARSE_REC: candidates read the dense pull's 32-byte row record (one load: 6 ids,
+  // caller id, in-degree) instead of head + offsets + caller id (three)
+  const bool usrec = !D && PP_SPARSE_REC && a.drec != nullptr;
+  const int hlen = usrec ? kDenseHead : 8;  // in-neighbour ids in the record / head
   PullCtx<Off, PARENTS, D> C{a, vin, vout, d, !(a.toggles & PP_OPT_NO_EARLYEXIT),
                              (a.toggles & PP_OPT_NO_REUSE) != 0, acc, sfound, rq, ssum,
                              a.H0, &out->work2, fr};
@@ -1046,47 +1058,6 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
         }
       }
 #endif
-#if PP_PULL_REC
-      if (!D && a.prec) {
-        // one 16-byte record per candidate: first in-neighbour, in-degree, caller id, begin;
-        // rows whose first in-neighbour misses continue from begin + 1 in the residual tiers
-        uint4 rc[kC];
-#pragma unroll
-        for (int t = 0; t < kC; ++t)
-          if (valid[t]) rc[t] = __ldg(a.prec + i[t]);
-#pragma unroll
-        for (int t = 0; t < kC; ++t) {
-          if (!valid[t]) continue;
-          const Off deg = (Off)rc[t].y;
-          rb[t] = (Off)rc[t].w;
-          e[t] = rb[t] + deg;
-          if (deg > 0 && C.hit(rc[t].x)) {
-            found[t] = true;
-            par[t] = rc[t].x;
-          }
-          p[t] = (deg > 1) ? rb[t] + 1 : e[t];
-        }
-#pragma unroll
-        for (int t = 0; t < kC; ++t) {
-          if (found[t] && fresh[t]) C.commit(i[t], par[t], e[t] - rb[t], wbase, true, rc[t].z);
-          const bool park = valid[t] && p[t] < e[t] && !(found[t] && C.early_exit) &&
-                            (fresh[t] || !found[t]);
-          const unsigned pm = __ballot_sync(kFull, park);
-          if (park) {
-            const int slot = qn + __popc(pm & lanemask_lt());
-            rq.i[slot] = fresh[t] ? i[t] : kNone - 1;
-            rq.par[slot] = (found[t] || !fresh[t]) ? (found[t] ? par[t] : 0u) : kNone;
-            rq.p[slot] = p[t];
-            rq.rem[slot] = (uint32_t)(e[t] - p[t]);
-            rq.degin[slot] = (uint32_t)(e[t] - rb[t]);
-          }
-          qn += __popc(pm);
-        }
-        __syncwarp();
-        while (qn >= 32) C.residual_batch(qn, 32, wbase, pw);
-        continue;
-      }
-#endif
       // stage: offsets and the row's head (first 8 in-neighbours = one 32-byte sector, one
       // 256-bit load from a row-contiguous array: dense items stream it), all in flight
       V8 hd[kC];
@@ -1096,10 +1067,17 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
         const uint32_t li = i[t] - lo;  // row of the CSC block (lo = 0 on one GPU)
         dpos[t] = li;
         if (valid[t]) {
-          if (!D && a.perm) dpos[t] = a.perm[i[t]];
-          rb[t] = a.coff[li];
-          e[t] = a.coff[li + 1];
-          hd[t] = ld_nc_v8(a.head + (size_t)li * 8u);
+          if (usrec) {  // one 32-byte record: 6 ids, caller id, in-degree; row-relative [0, deg)
+            hd[t] = ld_nc_v8(a.drec + (size_t)li * 8u);
+            dpos[t] = hd[t].x[6];
+            rb[t] = 0;
+            e[t] = (Off)hd[t].x[7];
+          } else {
+            if (!D && a.perm) dpos[t] = a.perm[i[t]];
+            rb[t] = a.coff[li];
+            e[t] = a.coff[li + 1];
+            hd[t] = ld_nc_v8(a.head + (size_t)li * 8u);
+          }
         }
       }
       // stage: probe the first neighbour, then the other head ids of rows that missed
@@ -1117,7 +1095,7 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
         if (valid[t] && deg > 1 && !(found[t] && C.early_exit)) {
           bool h[8];
 #pragma unroll
-          for (int q = 1; q < 8; ++q) h[q] = deg > (Off)q && C.hit(hd[t].x[q]);
+          for (int q = 1; q < 8; ++q) h[q] = q < hlen && deg > (Off)q && C.hit(hd[t].x[q]);
 #pragma unroll
           for (int q = 1; q < 8; ++q) {
             if (h[q] && !found[t]) {
@@ -1126,7 +1104,7 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
             }
           }
         }
-        p[t] = (valid[t] && deg > 8) ? rb[t] + 8 : e[t];  // the tail continues in idx
+        p[t] = (valid[t] && deg > (Off)hlen) ? rb[t] + (Off)hlen : e[t];  // the tail continues in idx
       }
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
@@ -1139,8 +1117,11 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
           const int slot = qn + __popc(pm & lanemask_lt());
           rq.i[slot] = fresh[t] ? i[t] : kNone - 1;  // visited rows (no masking) never commit
           rq.par[slot] = (found[t] || !fresh[t]) ? (found[t] ? par[t] : 0u) : kNone;
-          rq.p[slot] = p[t];
-          rq.rem[slot] = (uint32_t)(e[t] - p[t]);
+          // record: p is row-relative; the batch adds coff[i] (rows that cannot commit, i.e.
+          // visited rows of the no-masking ablation, carry no row id: made absolute here)
+          const bool rel = usrec && fresh[t];
+          rq.p[slot] = (usrec && !fresh[t]) ? a.coff[i[t] - lo] + p[t] : p[t];
+          rq.rem[slot] = (uint32_t)(e[t] - p[t]) | (rel ? kRelP : 0u);
           rq.degin[slot] = (uint32_t)(e[t] - rb[t]);
         }
         qn += __popc(pm);
@@ -1183,7 +1164,7 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
 // cp.async.bulk of a bitmap word's 32 records into a free slot (completion counted on the
 // slot's mbarrier), so kDenseR KB per warp are in flight without holding registers.  Words
 // whose rows are all visited (or isolated / padding, pre-marked) are never fetched.  A step
-// takes kDenseU landed words: lane l owns row l of each, probes the visited snapshot for the
+// takes the next landed word: lane l owns row l, probes the visited snapshot for the
 // record's first in-neighbour, then (on a miss) the other five (Alg. 2 with masking, early
 // exit and operand reuse; first hit in sorted order = min-id parent, R14); rows
 // longer than 6 that no record id decides go to the residual tiers.  The word's found bits
@@ -1224,13 +1205,32 @@ struct DenseRing {
   unsigned long long* bar;   // [kDenseR]
   uint32_t* word;            // [kDenseR]
   uint32_t* vw;              // [kDenseR]
+  unsigned* seq;             // bulk copies this warp issued (= consumed between phases)
 };
+// The calling warp's ring, from the dynamic shared memory layout (recomputed where used, so no
+// ring state stays live in registers across the level loop).  Layout: dense_ring_offset(),
+// then kBfsWarps*kDenseR slots of 1 KB, their mbarriers, words, visited words, and one
+// sequence counter per warp.
+template <typename Off>
+__device__ __forceinline__ DenseRing dense_ring(unsigned char* dyn, size_t off) {
+  const unsigned warp = threadIdx.x >> 5;
+  unsigned char* rb = dyn + off;
+  unsigned char* mb = rb + (size_t)kBfsWarps * kDenseR * 1024;
+  uint32_t* meta = reinterpret_cast<uint32_t*>(mb + (size_t)kBfsWarps * kDenseR * 8);
+  DenseRing r;
+  r.rec = reinterpret_cast<uint32_t*>(rb) + (size_t)warp * kDenseR * 256;
+  r.bar = reinterpret_cast<unsigned long long*>(mb) + (size_t)warp * kDenseR;
+  r.word = meta + (size_t)warp * kDenseR;
+  r.vw = meta + (size_t)kBfsWarps * kDenseR + (size_t)warp * kDenseR;
+  r.seq = meta + (size_t)2 * kBfsWarps * kDenseR + warp;
+  return r;
+}
 
 template <typename Off, bool PARENTS>
-__device__ void pull_dense(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
+PP_PULL_INLINE __device__ void pull_dense(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
                            uint32_t* __restrict__ vout, LevelCtr* out, int d, Acc& acc,
                            uint32_t* sfound, ResidualQ<Off>& rq, unsigned* sctr, uint32_t* fr,
-                           const DenseRing& R, unsigned& seq) {
+                           const DenseRing& R) {
   const unsigned lane = lane_id();
   PullCtx<Off, PARENTS, false> C{a, vin, vout, d, true, false, acc, sfound, rq, nullptr,
                                  a.H0, &out->work2, fr};
@@ -1244,7 +1244,8 @@ __device__ void pull_dense(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
   unsigned pk = 0, pbase = 0, pneed = 0;
   uint32_t pvw = 0xFFFFFFFFu;
   bool more = true;
-  unsigned issued = seq, cons = seq;
+  const unsigned seq0 = *R.seq;
+  unsigned issued = seq0, cons = seq0;
   // the item after the producer's is grabbed, and its visited words loaded, one item ahead
   auto grab_item = [&](uint32_t& vw_out) {
     unsigned j = 0;
@@ -1272,7 +1273,7 @@ __device__ void pull_dense(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
     return true;
   };
   auto issue = [&]() {  // fills the free slots; warp-uniform
-    while (more && issued - cons < (unsigned)kDenseR) {
+    while (kDenseR > 0 && more && issued - cons < (unsigned)kDenseR) {
       if (pneed == 0 && !next_item()) {
         more = false;
         break;
@@ -1280,7 +1281,7 @@ __device__ void pull_dense(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
       const unsigned j = __ffs(pneed) - 1;
       pneed &= pneed - 1;
       const uint32_t vwj = __shfl_sync(kFull, pvw, j);
-      const unsigned slot = issued % (unsigned)kDenseR;
+      const unsigned slot = issued % (unsigned)(kDenseR > 0 ? kDenseR : 1);
       if (lane == 0) {
         R.word[slot] = pbase + j;
         R.vw[slot] = vwj;
@@ -1291,105 +1292,79 @@ __device__ void pull_dense(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
     }
     __syncwarp();
   };
-  issue();
-  while (cons != issued) {
-    const unsigned u = min((unsigned)kDenseU, issued - cons);
-    uint4 r0[kDenseU], r1[kDenseU];
-    uint32_t w[kDenseU], vw[kDenseU];
+  // one bitmap word: lane l owns row w*32 + l, its record is {x0..x5 | x0..x4 + begin, caller, deg}
+  auto process = [&](uint32_t w, uint32_t vw, const uint4& r0, const uint4& r1) {
+    const bool cand = !((vw >> lane) & 1u);
+    acc.cand += cand ? 1u : 0u;
+    const uint32_t dg = r1.w;
+    bool found = cand && dg > 0u && C.hit(r0.x);
+    uint32_t par = r0.x;
+    // the other record ids only for rows whose first id missed (probing all six in one round
+    // measured slower: DESIGN.md §11)
+    if (cand && !found && dg > 1u) {
+      const uint32_t x[5] = {r0.y, r0.z, r0.w, r1.x, r1.y};
+      constexpr int kX = kDenseHead - 1;  // ids after the first in the record
+      bool h[kX];
 #pragma unroll
-    for (int t = 0; t < kDenseU; ++t) {
-      if ((unsigned)t < u) {
-        const unsigned q = cons + t, slot = q % (unsigned)kDenseR;
-        if (!mbar_try(&R.bar[slot], (q / (unsigned)kDenseR) & 1u)) {
-          const unsigned long long t0 = global_timer_ns();
-          while (!mbar_try(&R.bar[slot], (q / (unsigned)kDenseR) & 1u))
-            if (global_timer_ns() - t0 > kWatchdogNs) __trap();  // a lost copy: fail, never hang
+      for (int q = 0; q < kX; ++q) h[q] = dg > (uint32_t)(q + 1) && C.hit(x[q]);
+#pragma unroll
+      for (int q = kX - 1; q >= 0; --q)
+        if (h[q]) {
+          found = true;
+          par = x[q];
         }
-        w[t] = R.word[slot];
-        vw[t] = R.vw[slot];
-        const uint4* rp = reinterpret_cast<const uint4*>(R.rec + slot * 256u) + 2 * lane;
-        r0[t] = rp[0];
-        r1[t] = rp[1];
-      } else {
-        w[t] = 0;
-        vw[t] = 0xFFFFFFFFu;
-        r0[t] = make_uint4(0, 0, 0, 0);
-        r1[t] = make_uint4(0, 0, 0, 0);
-      }
     }
-    cons += u;
-    __syncwarp();  // every lane has its records: the slots may be refilled
+    const uint32_t fb = __ballot_sync(kFull, found);
+    if (lane == 0) {
+      vout[w] = vw | fb;
+      fr[w] = fb;
+    }
+    const uint32_t i = w * 32u + lane;
+    if (found) {
+      a.depth[r1.z] = d + 1;
+      if (PARENTS) a.parent[i] = par;
+      const Off odg = a.symmetric ? (Off)dg : (Off)(a.off[i + 1] - a.off[i]);
+      acc.c += 1;
+      acc.mf += (unsigned long long)odg;
+      acc.mfin += (unsigned long long)dg;
+      acc.big += odg >= (Off)kBig ? 1u : 0u;
+    }
+    // rows longer than the record that no record id decided: the residual tiers
+    const bool park = cand && !found && dg > (uint32_t)kDenseHead;
+    const unsigned pm = __ballot_sync(kFull, park);
+    if (park) {
+      const int slot = qn + __popc(pm & lanemask_lt());
+      rq.i[slot] = i;
+      rq.par[slot] = kNone;
+      rq.p[slot] = (Off)kDenseHead;  // relative: the batch adds coff[i] (one round trip per
+      rq.rem[slot] = (dg - (uint32_t)kDenseHead) | kRelP;  // batch, not per step)
+      rq.degin[slot] = dg;
+    }
+    qn += __popc(pm);
+    __syncwarp();
+    while (qn >= 32) C.residual_batch(qn, 32, 0u, 0u);
+  };
+  {
     issue();
-    bool cand[kDenseU], found[kDenseU];
-    uint32_t par[kDenseU];
-#pragma unroll
-    for (int t = 0; t < kDenseU; ++t) {
-      cand[t] = !((vw[t] >> lane) & 1u);
-      acc.cand += cand[t] ? 1u : 0u;
-      found[t] = cand[t] && r1[t].w > 0u && C.hit(r0[t].x);
-      par[t] = r0[t].x;
-    }
-#pragma unroll
-    for (int t = 0; t < kDenseU; ++t) {
-      const uint32_t dg = r1[t].w;
-      // PP_DENSE_SPEC: the other five ids are probed in the same round as the first (more
-      // probes, one dependent round less); else only for rows whose first id missed
-      if (cand[t] && (PP_DENSE_SPEC || !found[t]) && dg > 1u) {
-        const uint32_t x[5] = {r0[t].y, r0[t].z, r0[t].w, r1[t].x, r1[t].y};
-        constexpr int kX = kDenseHead - 1;  // ids after the first in the record
-        bool h[kX];
-#pragma unroll
-        for (int q = 0; q < kX; ++q) h[q] = dg > (uint32_t)(q + 1) && C.hit(x[q]);
-        const bool hit0 = found[t];  // the first id decides alone when it hits
-#pragma unroll
-        for (int q = kX - 1; q >= 0; --q)
-          if (h[q] && !hit0) {
-            found[t] = true;
-            par[t] = x[q];
-          }
+    while (cons != issued) {
+      const unsigned slot = cons % (unsigned)kDenseR;
+      const unsigned par = (cons / (unsigned)kDenseR) & 1u;
+      if (!mbar_try(&R.bar[slot], par)) {
+        const unsigned long long t0 = global_timer_ns();
+        while (!mbar_try(&R.bar[slot], par))
+          if (global_timer_ns() - t0 > kWatchdogNs) __trap();  // a lost copy: fail, never hang
       }
-    }
-#pragma unroll
-    for (int t = 0; t < kDenseU; ++t) {
-      const uint32_t fb = __ballot_sync(kFull, found[t]);
-      if ((unsigned)t < u && lane == 0) {
-        vout[w[t]] = vw[t] | fb;
-        fr[w[t]] = fb;
-      }
-      const uint32_t i = w[t] * 32u + lane;
-      const uint32_t dg = r1[t].w;
-      if (found[t]) {
-        a.depth[r1[t].z] = d + 1;
-        if (PARENTS) a.parent[i] = par[t];
-        const Off odg = a.symmetric ? (Off)dg : (Off)(a.off[i + 1] - a.off[i]);
-        acc.c += 1;
-        acc.mf += (unsigned long long)odg;
-        acc.mfin += (unsigned long long)dg;
-        acc.big += odg >= (Off)kBig ? 1u : 0u;
-      }
-      // rows longer than the record that no record id decided: the residual tiers
-      const bool park = cand[t] && !found[t] && dg > (uint32_t)kDenseHead;
-      const unsigned pm = __ballot_sync(kFull, park);
-      if (park) {
-        const int slot = qn + __popc(pm & lanemask_lt());
-        rq.i[slot] = i;
-        rq.par[slot] = kNone;
-        if (PP_DENSE_RB) {  // the record carries the row begin
-          rq.p[slot] = (Off)r1[t].y + (Off)kDenseHead;
-          rq.rem[slot] = dg - (uint32_t)kDenseHead;
-        } else {  // relative: the batch adds coff[i] (one round trip per batch, not per step)
-          rq.p[slot] = (Off)kDenseHead;
-          rq.rem[slot] = (dg - (uint32_t)kDenseHead) | kRelP;
-        }
-        rq.degin[slot] = dg;
-      }
-      qn += __popc(pm);
-      __syncwarp();
-      while (qn >= 32) C.residual_batch(qn, 32, 0u, 0u);
+      const uint32_t w = R.word[slot], vw = R.vw[slot];
+      const uint4* rp = reinterpret_cast<const uint4*>(R.rec + slot * 256u) + 2 * lane;
+      const uint4 r0 = rp[0], r1 = rp[1];
+      ++cons;
+      __syncwarp();  // every lane has its records: the slot may be refilled
+      issue();
+      process(w, vw, r0, r1);
     }
   }
   if (qn > 0) C.residual_batch(qn, qn, 0u, 0u);
-  seq = issued;
+  if (lane == 0) *R.seq = issued;
   __syncwarp();
 }
 
@@ -1399,7 +1374,7 @@ __device__ void pull_dense(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
 // chunk whose atomicOr on v' flips the bit (the item owning the row has closed); the
 // min-id parent is the atomicMin of the chunks' first hits (R14).
 template <typename Off, bool PARENTS>
-__device__ void pull_hub_chunks(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
+PP_PULL_INLINE __device__ void pull_hub_chunks(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
                                 uint32_t* __restrict__ vout, LevelCtr* out, unsigned nch, int d,
                                 Acc& acc, ResidualQ<Off>& rq) {
   const unsigned lane = lane_id();
@@ -1644,7 +1619,7 @@ __host__ __device__ constexpr size_t dense_ring_offset() {
 }
 template <typename Off, bool D = false>
 __host__ __device__ constexpr size_t dyn_smem_bytes() {  // D (multi-rank): no dense rings
-  return (kDenseR && !D) ? dense_ring_offset<Off>() + (size_t)kBfsWarps * kDenseR * (1024 + 8 + 4 + 4)
+  return (kDenseR && !D) ? dense_ring_offset<Off>() + (size_t)kBfsWarps * (kDenseR * (1024 + 8 + 4 + 4) + 4)
                          : sizeof(ResidualQ<Off>) * kBfsWarps + sizeof(uint32_t) * kSumWordsMax;
 }
 
@@ -1658,22 +1633,17 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
   ResidualQ<Off>* rqs = reinterpret_cast<ResidualQ<Off>*>(dyn_smem);
   uint32_t* ssum = reinterpret_cast<uint32_t*>(dyn_smem + sizeof(ResidualQ<Off>) * kBfsWarps);
   const unsigned warp = threadIdx.x >> 5;
-  DenseRing ring{nullptr, nullptr, nullptr, nullptr};
-  unsigned dseq = 0;  // this warp's bulk copies issued (= consumed between levels)
   if constexpr (!D && kDenseR > 0) {
-    unsigned char* rb = dyn_smem + dense_ring_offset<Off>();
-    ring.rec = reinterpret_cast<uint32_t*>(rb) + (size_t)warp * kDenseR * 256;
-    unsigned char* mb = rb + (size_t)kBfsWarps * kDenseR * 1024;
-    ring.bar = reinterpret_cast<unsigned long long*>(mb) + (size_t)warp * kDenseR;
-    uint32_t* meta = reinterpret_cast<uint32_t*>(mb + (size_t)kBfsWarps * kDenseR * 8);
-    ring.word = meta + (size_t)warp * kDenseR;
-    ring.vw = meta + (size_t)kBfsWarps * kDenseR + (size_t)warp * kDenseR;
-    if (a.drec && lane_id() == 0) {
-      for (int r = 0; r < kDenseR; ++r) mbar_init(&ring.bar[r], 1u);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (a.drec) {
+      const DenseRing ring = dense_ring<Off>(dyn_smem, dense_ring_offset<Off>());
+      if (lane_id() == 0) {
+        for (int r = 0; r < kDenseR; ++r) mbar_init(&ring.bar[r], 1u);
+        *ring.seq = 0u;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      }
+      __syncwarp();
     }
-    __syncwarp();
   }
   const unsigned cta = cta_of(a);
   const unsigned long long gtid = (unsigned long long)cta * blockDim.x + threadIdx.x;
@@ -1836,13 +1806,14 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
         __syncthreads();
       }
       bool dense = false;
-      if constexpr (!D && kDenseR > 0)
+      if constexpr (!D && kDense)
         dense = a.drec != nullptr && a.toggles == 0u && !a.narrow &&
                 (a.n_noniso - reached) * 8 >= a.n_noniso * (long long)PP_DENSE_MIN8;
       if (dense) {
-        if constexpr (!D && kDenseR > 0)
+        if constexpr (!D && kDense)
           pull_dense<Off, PARENTS>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp],
-                                   &sh.work, frout, ring, dseq);
+                                   &sh.work, frout,
+                                   dense_ring<Off>(dyn_smem, dense_ring_offset<Off>()));
       } else {
         pull_phase<Off, PARENTS, D>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp],
                                     ssum, &sh.work, frout, a.gwork + (size_t)(d & (kRing - 1)) * kMaxCtas);
@@ -2092,7 +2063,6 @@ static cudaError_t launch_off(pp_graph g, uint32_t source, int mode, int rule, d
   a.fr = g->fr;
   a.sumv = g->sumv;
   a.head = g->head;
-  a.prec = g->prec;
   a.drec = g->drec;
   a.n_noniso = g->n_noniso;
   a.sum_shift = g->sum_shift;

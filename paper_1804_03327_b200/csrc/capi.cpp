@@ -81,7 +81,7 @@ void free_graph(pp_graph g) {
                   g->sbits[0], g->sbits[1], g->sbits[2], g->sbits[3], g->sblock, g->hubq, g->scount,
                   g->dtmp[0], g->dtmp[1], g->dbg, g->perm, g->rank, g->pint, g->vrec,
                   g->rbits[0], g->rbits[1], g->rbits[2], g->rbits[3],
-                  g->odeg, g->xbuf, g->dargs, g->gwork, g->prec, g->drec};
+                  g->odeg, g->xbuf, g->dargs, g->gwork, g->drec};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (g->status_host) cudaFreeHost(g->status_host);
@@ -611,8 +611,10 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t row_lo, int64_t row_hi,
     }
   }
   if ((s = dalloc(&g->isolated, g->nwords, &bytes, "isolated")) != PP_OK) return s;
-  if ((s = dalloc(&g->head, (size_t)n * 8, &bytes, "row heads")) != PP_OK) return s;
-  if (kPullRec && !g->off64 && (s = dalloc(&g->prec, (size_t)n, &bytes, "row records")) != PP_OK) return s;
+  // pull row data: the 32-byte dense records (32-bit offsets), which the sparse pull reads too
+  // (PP_SPARSE_REC), else the 8-id row heads
+  if (!(kDense && !g->off64 && PP_SPARSE_REC) &&
+      (s = dalloc(&g->head, (size_t)n * 8, &bytes, "row heads")) != PP_OK) return s;
   if (kDense && !g->off64) {
     const size_t words = (size_t)g->nwords * 32 * 8;  // 32 B per row incl. padding rows
     if ((s = dalloc(&g->drec, words, &bytes, "dense pull records")) != PP_OK) return s;

@@ -45,7 +45,7 @@ __global__ void k_drec(const int64_t* __restrict__ coff, const uint32_t* __restr
     r0.z = d > 2 ? cidx[b + 2] : 0xFFFFFFFFu;
     r0.w = d > 3 ? cidx[b + 3] : 0xFFFFFFFFu;
     r1.x = d > 4 ? cidx[b + 4] : 0xFFFFFFFFu;
-    r1.y = PP_DENSE_RB ? (uint32_t)b : (d > 5 ? cidx[b + 5] : 0xFFFFFFFFu);
+    r1.y = d > 5 ? cidx[b + 5] : 0xFFFFFFFFu;
     r1.z = perm ? perm[v] : (uint32_t)v;
     r1.w = (uint32_t)d;
     reinterpret_cast<uint4*>(drec)[2 * v] = r0;
@@ -72,19 +72,6 @@ __global__ void k_head(const int64_t* __restrict__ coff, const uint32_t* __restr
     h1.w = d > 7 ? cidx[b + 7] : 0xFFFFFFFFu;
     reinterpret_cast<uint4*>(head)[2 * v] = h0;
     reinterpret_cast<uint4*>(head)[2 * v + 1] = h1;
-  }
-}
-
-// PP_PULL_REC: one 16-byte record per row {first in-neighbour (0xFFFFFFFF if none), in-degree,
-// caller id, row begin} — everything a pull candidate needs when its first in-neighbour is
-// already visited (79-100% of the candidates at C2's heavy levels), in one load.
-__global__ void k_prec(const int64_t* __restrict__ coff, const uint32_t* __restrict__ cidx,
-                       const uint32_t* __restrict__ perm, int64_t n, uint4* __restrict__ prec) {
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = coff[v], d = coff[v + 1] - b;
-    prec[v] = make_uint4(d > 0 ? cidx[b] : 0xFFFFFFFFu, (uint32_t)d, perm ? perm[v] : (uint32_t)v,
-                         (uint32_t)b);
   }
 }
 
@@ -185,12 +172,8 @@ cudaError_t launch_graph_prepare(pp_graph g, const int64_t* d_off64, const int64
     *launches += 1;
     k_vrec<<<blocks, kBlock, 0, st>>>(d_off64, g->perm, g->n, g->vrec);
   }
-  *launches += 4;
-  k_head<<<blocks, kBlock, 0, st>>>(d_coff64, g->cidx, g->n, g->head);
-  if (g->prec) {
-    *launches += 1;
-    k_prec<<<blocks, kBlock, 0, st>>>(d_coff64, g->cidx, g->perm, g->n, g->prec);
-  }
+  *launches += g->head ? 4 : 3;
+  if (g->head) k_head<<<blocks, kBlock, 0, st>>>(d_coff64, g->cidx, g->n, g->head);
   if (g->drec) {
     *launches += 1;
     k_drec<<<blocks, kBlock, 0, st>>>(d_coff64, g->cidx, g->perm, g->n, g->drec);

@@ -49,10 +49,6 @@ constexpr bool kInitVec = PP_INIT_VEC != 0;  // BFS init: 16-byte depth stores
 #define PP_VREC 1
 #endif
 constexpr bool kVrec = PP_VREC != 0;  // relabelled graphs: per-vertex {begin, deg, caller id}
-#ifndef PP_PULL_REC
-#define PP_PULL_REC 0
-#endif
-constexpr bool kPullRec = PP_PULL_REC != 0;  // pull: 16-byte row records instead of 32-byte heads
 #ifndef PP_DENSE
 #define PP_DENSE 1
 #endif
@@ -62,25 +58,17 @@ constexpr bool kDense = PP_DENSE != 0;
 #ifndef PP_DENSE_R
 #define PP_DENSE_R 1
 #endif
-#ifndef PP_DENSE_U
-#define PP_DENSE_U 1
-#endif
-#ifndef PP_DENSE_SPEC
-#define PP_DENSE_SPEC 0
-#endif
 #ifndef PP_DENSE_MIN8
 #define PP_DENSE_MIN8 2
 #endif
-constexpr int kDenseR = kDense ? PP_DENSE_R : 0;  // ring slots (32 rows x 32 B) per warp
-constexpr int kDenseU = PP_DENSE_U;               // slots (bitmap words) processed per step
-#ifndef PP_DENSE_RB
-#define PP_DENSE_RB 0
+#ifndef PP_SPARSE_REC
+#define PP_SPARSE_REC 1
 #endif
+constexpr int kDenseR = kDense ? PP_DENSE_R : 0;  // ring slots (32 rows x 32 B) per warp
 #ifndef PP_DENSE_IW
 #define PP_DENSE_IW 8
 #endif
-// in-neighbour ids per dense record: 6, or 5 and the row begin (PP_DENSE_RB)
-constexpr int kDenseHead = PP_DENSE_RB ? 5 : 6;
+constexpr int kDenseHead = 6;  // in-neighbour ids per dense record
 constexpr unsigned kDenseIW = PP_DENSE_IW;  // bitmap words per dense work item
 constexpr int kMaxRanks = 8;  // 1D row partition: ranks per multi-rank group (one node)
 constexpr int kMaxCtas = 1024;  // persistent grid size bound (per-CTA work counters)
@@ -181,8 +169,6 @@ struct pp_graph_s {
   uint32_t* drec = nullptr;      // PP_DENSE: per row {first 6 in-neighbours, caller id, in-degree}
                                  // (32 B; nwords*32 rows, padding rows zero)
   int64_t n_noniso = 0;          // rows not marked isolated / padding
-  uint4* prec = nullptr;         // PP_PULL_REC: per row {first in-neighbour, in-degree, caller id,
-                                 // row begin} (32-bit offsets only)
   // PP_GRAPH_RELABEL: internal id = rank by decreasing degree (relabel.cu)
   uint32_t* perm = nullptr;  // internal -> caller id (nullptr: ids are the caller's)
   uint32_t* rank = nullptr;  // caller -> internal id
