@@ -35,7 +35,7 @@ def build(force=False, verbose=False):
                                                    "PP_PULL_PF", "PP_LOWLAT_VREC", "PP_PF_ROWS",
                                                    "PP_SUM_RESID", "PP_DENSE", "PP_DENSE_R",
                                                    "PP_DENSE_MIN8", "PP_DENSE_IW", "PP_SPARSE_REC",
-                                                   "PP_CHUNK", "PP_HEAVY", "PP_RQ_EXTRA", "PP_NOINLINE_PULL")
+                                                   "PP_CHUNK", "PP_HEAVY", "PP_RQ_EXTRA")
               if os.environ.get(k)]
     odir = os.path.join(HERE, "build")
     os.makedirs(odir, exist_ok=True)

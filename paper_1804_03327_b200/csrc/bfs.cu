@@ -610,15 +610,6 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
   }
 }
 
-#ifndef PP_NOINLINE_PULL
-#define PP_NOINLINE_PULL 0
-#endif
-// PP_NOINLINE_PULL: the pull phases as called functions (code layout / register A-B only)
-#if PP_NOINLINE_PULL
-#define PP_PULL_INLINE __noinline__
-#else
-#define PP_PULL_INLINE
-#endif
 #ifndef PP_PULL_KC
 #define PP_PULL_KC 1
 #endif
@@ -926,8 +917,8 @@ struct PullCtx {
 // Multi-rank (D): the items cover the owned words [wlo, wlo + wcnt) only; the rows' CSC
 // data is local (row i - lo), the probed in-neighbour ids are global and test the
 // replicated visited snapshot.
-template <typename Off, bool PARENTS, bool D>
-PP_PULL_INLINE __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
+template <typename Off, bool PARENTS, bool D, bool ABL>
+__device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
                            uint32_t* __restrict__ vout, LevelCtr* out, int d, Acc& acc,
                            uint32_t* sfound, ResidualQ<Off>& rq, const uint32_t* ssum,
                            unsigned* sctr, uint32_t* fr, unsigned* gwork) {
@@ -935,13 +926,14 @@ PP_PULL_INLINE __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t*
   const unsigned nitems = (D ? a.wcnt : a.nwords) / kPW;
   const unsigned wb0 = D ? a.wlo : 0u;
   const uint32_t lo = D ? (uint32_t)a.lo : 0u;
-  const bool no_mask = (a.toggles & PP_OPT_NO_MASKING) != 0;
+  // ABL: the Table-2 ablation kernel; the default kernel compiles the toggles out
+  const bool no_mask = ABL && (a.toggles & PP_OPT_NO_MASKING) != 0;
   // PP_SPARSE_REC: candidates read the dense pull's 32-byte row record (one load: 6 ids,
   // caller id, in-degree) instead of head + offsets + caller id (three)
   const bool usrec = !D && PP_SPARSE_REC && a.drec != nullptr;
   const int hlen = usrec ? kDenseHead : 8;  // in-neighbour ids in the record / head
-  PullCtx<Off, PARENTS, D> C{a, vin, vout, d, !(a.toggles & PP_OPT_NO_EARLYEXIT),
-                             (a.toggles & PP_OPT_NO_REUSE) != 0, acc, sfound, rq, ssum,
+  PullCtx<Off, PARENTS, D> C{a, vin, vout, d, !ABL || !(a.toggles & PP_OPT_NO_EARLYEXIT),
+                             ABL && (a.toggles & PP_OPT_NO_REUSE) != 0, acc, sfound, rq, ssum,
                              a.H0, &out->work2, fr};
   int qn = 0;
   unsigned wbase = 0;
@@ -1227,7 +1219,7 @@ __device__ __forceinline__ DenseRing dense_ring(unsigned char* dyn, size_t off) 
 }
 
 template <typename Off, bool PARENTS>
-PP_PULL_INLINE __device__ void pull_dense(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
+__device__ void pull_dense(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
                            uint32_t* __restrict__ vout, LevelCtr* out, int d, Acc& acc,
                            uint32_t* sfound, ResidualQ<Off>& rq, unsigned* sctr, uint32_t* fr,
                            const DenseRing& R) {
@@ -1374,7 +1366,7 @@ PP_PULL_INLINE __device__ void pull_dense(const BfsArgs<Off>& a, const uint32_t*
 // chunk whose atomicOr on v' flips the bit (the item owning the row has closed); the
 // min-id parent is the atomicMin of the chunks' first hits (R14).
 template <typename Off, bool PARENTS>
-PP_PULL_INLINE __device__ void pull_hub_chunks(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
+__device__ void pull_hub_chunks(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
                                 uint32_t* __restrict__ vout, LevelCtr* out, unsigned nch, int d,
                                 Acc& acc, ResidualQ<Off>& rq) {
   const unsigned lane = lane_id();
@@ -1626,7 +1618,7 @@ __host__ __device__ constexpr size_t dyn_smem_bytes() {  // D (multi-rank): no d
 // The BFS loop (Algorithm 1) run by the CTAs of one rank.  D = multi-rank (1D
 // row partition): the same push / pull / convert phases over the rank's block, plus the
 // exchange after every level and a merge of the peers' discoveries into the visited bitmap.
-template <typename Off, bool PARENTS, bool D>
+template <typename Off, bool PARENTS, bool D, bool ABL = false>
 __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
   __shared__ BfsShared<Off> sh;
   extern __shared__ __align__(16) unsigned char dyn_smem[];
@@ -1807,7 +1799,7 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
       }
       bool dense = false;
       if constexpr (!D && kDense)
-        dense = a.drec != nullptr && a.toggles == 0u && !a.narrow &&
+        dense = !ABL && a.drec != nullptr && !a.narrow &&
                 (a.n_noniso - reached) * 8 >= a.n_noniso * (long long)PP_DENSE_MIN8;
       if (dense) {
         if constexpr (!D && kDense)
@@ -1815,10 +1807,10 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
                                    &sh.work, frout,
                                    dense_ring<Off>(dyn_smem, dense_ring_offset<Off>()));
       } else {
-        pull_phase<Off, PARENTS, D>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp],
+        pull_phase<Off, PARENTS, D, ABL>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp],
                                     ssum, &sh.work, frout, a.gwork + (size_t)(d & (kRing - 1)) * kMaxCtas);
       }
-      if (!D && (a.toggles & PP_OPT_NO_EARLYEXIT)) {  // ablation arms: long rows grid-wide
+      if (!D && ABL && (a.toggles & PP_OPT_NO_EARLYEXIT)) {  // ablation arms: long rows grid-wide
         if (!level_barrier(a.narrow, a.bar, a.status, epoch, (unsigned)a.ncta)) return;
         const unsigned nch = ld_relaxed_u32(&out->work2);
         if (nch) pull_hub_chunks<Off, PARENTS>(a, vis, vis_other, out, nch, d, acc, rqs[warp]);
@@ -1942,9 +1934,9 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
 }
 
 // One GPU: the whole grid runs one BFS; the arguments are a kernel parameter.
-template <typename Off, bool PARENTS>
+template <typename Off, bool PARENTS, bool ABL>
 __global__ void __launch_bounds__(kBfsBlock, 1) bfs_persistent(BfsArgs<Off> a) {
-  bfs_body<Off, PARENTS, false>(a);
+  bfs_body<Off, PARENTS, false, ABL>(a);
 }
 
 // Multi-rank: `all` holds one argument block per rank of this launch, rank r running on the
@@ -1986,9 +1978,15 @@ static int coop_grid(const void* fn, size_t smem) {
   return g;
 }
 
-template <typename Off, bool PARENTS>
+template <typename Off, bool PARENTS, bool ABL = false>
 static int grid_for() {
-  return coop_grid((const void*)bfs_persistent<Off, PARENTS>, dyn_smem_bytes<Off>());
+  return coop_grid((const void*)bfs_persistent<Off, PARENTS, ABL>, dyn_smem_bytes<Off>());
+}
+// the default kernel (toggles compiled out) or the ablation kernel
+template <typename Off, bool PARENTS>
+static const void* bfs_kernel(bool abl) {
+  return abl ? (const void*)bfs_persistent<Off, PARENTS, true>
+             : (const void*)bfs_persistent<Off, PARENTS, false>;
 }
 
 int bfs_grid_size(pp_graph g, bool parents) {
@@ -1998,12 +1996,13 @@ int bfs_grid_size(pp_graph g, bool parents) {
 
 template <typename Off, bool PARENTS>
 static cudaError_t launch_t(pp_graph g, BfsArgs<Off> args) {
-  const int grid = grid_for<Off, PARENTS>();
+  const bool abl = args.toggles != 0u;
+  const int grid = abl ? grid_for<Off, PARENTS, true>() : grid_for<Off, PARENTS, false>();
   args.cta_base = 0;
   args.ncta = grid;
   void* params[] = {(void*)&args};
   g->ctx->launches += 1;
-  return cudaLaunchCooperativeKernel((const void*)bfs_persistent<Off, PARENTS>, dim3(grid),
+  return cudaLaunchCooperativeKernel(bfs_kernel<Off, PARENTS>(abl), dim3(grid),
                                      dim3(kBfsBlock), params, dyn_smem_bytes<Off>(),
                                      g->ctx->stream);
 }
@@ -2015,7 +2014,8 @@ template <typename Off, bool PARENTS>
 static cudaError_t launch_narrow(pp_graph g, BfsArgs<Off> args) {
   args.cta_base = 0;
   args.ncta = kNarrowCtas;
-  (void)grid_for<Off, PARENTS>();  // sets the dynamic shared memory attribute
+  const bool abl = args.toggles != 0u;
+  (void)(abl ? grid_for<Off, PARENTS, true>() : grid_for<Off, PARENTS, false>());  // smem attribute
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(kNarrowCtas);
   cfg.blockDim = dim3(kBfsBlock);
@@ -2029,7 +2029,8 @@ static cudaError_t launch_narrow(pp_graph g, BfsArgs<Off> args) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   g->ctx->launches += 1;
-  return cudaLaunchKernelEx(&cfg, bfs_persistent<Off, PARENTS>, args);
+  void* params[] = {(void*)&args};
+  return cudaLaunchKernelExC(&cfg, bfs_kernel<Off, PARENTS>(abl), params);
 }
 
 // PP_NARROW unset or 0: never; 1: always (tests of the hand-over on any graph);

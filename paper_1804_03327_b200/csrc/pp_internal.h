@@ -68,7 +68,8 @@ constexpr int kDenseR = kDense ? PP_DENSE_R : 0;  // ring slots (32 rows x 32 B)
 #ifndef PP_DENSE_IW
 #define PP_DENSE_IW 8
 #endif
-constexpr int kDenseHead = 6;  // in-neighbour ids per dense record
+constexpr int kDenseHead = 6;  // in-neighbour ids per row record (a 5-id record with the row
+                               // begin instead of the sixth id measured equal)
 constexpr unsigned kDenseIW = PP_DENSE_IW;  // bitmap words per dense work item
 constexpr int kMaxRanks = 8;  // 1D row partition: ranks per multi-rank group (one node)
 constexpr int kMaxCtas = 1024;  // persistent grid size bound (per-CTA work counters)
