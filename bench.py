@@ -161,7 +161,10 @@ def byte_models(torch, gd, depth, dirs, n, off_bytes, per_level=False):
       s8d_sector  the same with every scattered access rounded to the 32-byte sectors it touches
                   (distinct sectors; sorted streams rounded up): the realistic HBM floor
       design      this design's own traffic (no candidate list: each pull scans the visited
-                  bitmap for zero bits; pushes read 16-byte frontier entries)
+                  bitmap for zero bits and reads one 32-byte row record per candidate -- or,
+                  on a dense level, the records of every 32-row word holding a candidate --
+                  plus the ids past the record's six; pushes read 16-byte frontier entries;
+                  DESIGN.md §6)
     S = sum over candidates of the ids read = first-hit index + 1, or the degree on a miss."""
     off, idx, rows, deg, noniso = gd
     O = 2 * off_bytes
@@ -209,7 +212,14 @@ def byte_models(torch, gd, depth, dirs, n, off_bytes, per_level=False):
                                   _sectors_unique(torch, offs) +
                                   _sectors_runs(torch, off[cv], scanned[cv]) + depth_sec +
                                   seq(4 * Fn) + seq(4 * Cs) + seq(nb8) + seq(2 * nb8))
-            tot["design"] += 2 * nb8 + C * O + 4 * S + 4 * Fn
+            # records (32 B) instead of offsets + ids; dense levels (candidates >= 1/4 of the
+            # non-isolated rows: bfs.cu PP_DENSE_MIN8 = 2) stream whole 32-row words
+            n_noniso = int(noniso.sum())
+            dense = C * 8 >= n_noniso * 2
+            words = int(torch.unique(cv // 32).numel()) if dense else 0
+            rec = 32 * 32 * words if dense else 32 * C
+            tail = int(torch.clamp(scanned[cv] - 6, min=0).sum())
+            tot["design"] += 3 * nb8 + rec + 4 * tail + 4 * Fn
             if k < L and dirs[k] == 0:  # pull -> push: bitmap -> list
                 tot["s8d"] += nb8 + 4 * Fn
                 tot["s8d_sector"] += seq(nb8) + seq(4 * Fn)
@@ -450,7 +460,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong" if partitioned else "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic",
-            "config": dict(workload_config(args, g, world, args.mode), relabel=relabel),
+            "config": workload_config(args, g, world, args.mode),  # identical to the reference arm's
+            "layout": {"relabel": relabel,
+                       "note": "degree-ordered internal ids (upload-time; depth is in caller ids)"},
             "roofline": {"bound": "hbm", "achieved": a8, "peak": peak * (world if partitioned else 1),
                          "unit": "GB/s",
                          "frac": a8 / (peak * (world if partitioned else 1)) if a8 else None,

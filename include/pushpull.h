@@ -294,7 +294,10 @@ pp_status pp_bfs_team(const pp_graph* graphs, int32_t nranks, int64_t source,
  *   csc_off/csc_idx/csc_w: the same matrix by columns (rows of A^T, in-edges);
  *   source in [0, n); alpha >= 0 the switch threshold on nnz(f)/n;
  *   dist[n] fp32 output: 0 at the source, +inf where unreachable.
- * Stream-ordered on the ctx stream; synchronises it once per iteration (frontier size).
+ * Stream-ordered on the ctx stream: three prologue kernels, then the whole iteration loop in
+ * ONE persistent cooperative kernel (frontier size and the push -> pull switch decided on the
+ * device); synchronises twice: after reading off[0] / off[n] of both sides (argument check)
+ * and at the end (error flags, stats) -- never per iteration.
  * Errors: PP_ERR_ARG (NULL / n <= 0 / alpha < 0), PP_ERR_RANGE (source), PP_ERR_GRAPH
  * (a negative or NaN weight), PP_ERR_CUDA / PP_ERR_OOM. */
 typedef struct {

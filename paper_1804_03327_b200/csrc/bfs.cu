@@ -117,17 +117,6 @@ constexpr unsigned long long kWatchdogNs = 4000000000ull;  // 4 s per barrier wa
 // CTA's writes.  Bit 63 is the abort flag (watchdog), which releases every waiter.
 constexpr unsigned long long kAbortBit = 1ull << 63;
 
-__device__ __forceinline__ unsigned long long atom_add_release_u64(unsigned long long* p,
-                                                                   unsigned long long v) {
-  unsigned long long old;
-  asm volatile("atom.add.release.gpu.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
-  return old;
-}
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
 
 __device__ __forceinline__ bool grid_barrier(GridBarrier* b, BfsStatus* st, unsigned& epoch,
                                              unsigned ncta) {

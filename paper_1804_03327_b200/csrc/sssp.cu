@@ -12,11 +12,17 @@
 #include <math.h>
 #include <stdint.h>
 
-#include "pp_internal.h"
+#include <map>
+#include <mutex>
+
+#include "pp_device.cuh"
 
 namespace {
 
-constexpr int kT = 256;                 // threads per CTA
+using namespace pp;
+
+constexpr int kT = 256;                 // threads per CTA (prologue kernels)
+constexpr int kLoopT = 1024;            // threads per CTA of the persistent loop
 constexpr unsigned kInfBits = 0x7f800000u;
 
 __global__ void k_sssp_init(int64_t n, int64_t s, float* __restrict__ d, float* __restrict__ t,
@@ -70,14 +76,20 @@ __device__ __forceinline__ void relax(uint32_t v, float nd, const float* __restr
 constexpr int64_t kChunk = 2048;        // heavy rows / out-lists are cut into chunks of this
                                         // many edges, one warp each (no serial hub tail)
 
+// The iteration loop runs in ONE persistent cooperative kernel (k_sssp_loop): the phases
+// below are grid-stride device functions separated by a software grid barrier, the frontier
+// size is read on the device after each barrier and the push -> pull switch (R29) is decided
+// on the device, so a whole SSSP is one launch after the prologue with no host round trip per
+// iteration (as bfs_persistent does for BFS).
+
 // Column-based step (push, Alg. 3 shape P:370): a kG-lane group per active vertex u scatters
 // d(u) + A(u, v) into t(v); a vertex with more than kHeavyDeg out-edges is cut into kChunk-edge
-// chunk descriptors {u, chunk} for k_sssp_push_heavy.
-__global__ void k_sssp_push(const uint32_t* __restrict__ f, unsigned nf, const int64_t* __restrict__ off,
-                            const uint32_t* __restrict__ idx, const float* __restrict__ w,
-                            const float* __restrict__ d, float* __restrict__ t,
-                            uint32_t* __restrict__ next, unsigned* __restrict__ cnt,
-                            uint2* __restrict__ chunks) {
+// chunk descriptors {u, chunk} for push_heavy.
+__device__ void push_light(const uint32_t* __restrict__ f, unsigned nf, const int64_t* __restrict__ off,
+                           const uint32_t* __restrict__ idx, const float* __restrict__ w,
+                           const float* __restrict__ d, float* __restrict__ t,
+                           uint32_t* __restrict__ next, unsigned* __restrict__ ncnt,
+                           uint2* __restrict__ chunks, unsigned* __restrict__ ccnt) {
   const unsigned lane = threadIdx.x & (kG - 1);
   const unsigned gpb = blockDim.x / kG;
   for (unsigned k = blockIdx.x * gpb + threadIdx.x / kG; k < nf; k += gridDim.x * gpb) {
@@ -86,22 +98,21 @@ __global__ void k_sssp_push(const uint32_t* __restrict__ f, unsigned nf, const i
     if (e - b > kHeavyDeg) {
       const unsigned nch = (unsigned)((e - b + kChunk - 1) / kChunk);
       unsigned base = 0;
-      if (lane == 0) base = atomicAdd(cnt + 2, nch);
+      if (lane == 0) base = atomicAdd(ccnt, nch);
       base = __shfl_sync(group_mask(), base, 0, kG);
       for (unsigned c = lane; c < nch; c += kG) chunks[base + c] = make_uint2(u, c);
       continue;
     }
     const float du = d[u];
-    for (int64_t j = b + lane; j < e; j += kG) relax(__ldg(idx + j), du + __ldg(w + j), d, t, next, cnt);
+    for (int64_t j = b + lane; j < e; j += kG) relax(__ldg(idx + j), du + __ldg(w + j), d, t, next, ncnt);
   }
 }
 
 // Heavy out-lists of this step: one warp per kChunk-edge chunk.
-__global__ void k_sssp_push_heavy(const uint2* __restrict__ chunks, const int64_t* __restrict__ off,
-                                  const uint32_t* __restrict__ idx, const float* __restrict__ w,
-                                  const float* __restrict__ d, float* __restrict__ t,
-                                  uint32_t* __restrict__ next, unsigned* __restrict__ cnt) {
-  const unsigned nc = cnt[2];
+__device__ void push_heavy(const uint2* __restrict__ chunks, unsigned nc, const int64_t* __restrict__ off,
+                           const uint32_t* __restrict__ idx, const float* __restrict__ w,
+                           const float* __restrict__ d, float* __restrict__ t,
+                           uint32_t* __restrict__ next, unsigned* __restrict__ ncnt) {
   const unsigned lane = threadIdx.x & 31;
   const unsigned nw = gridDim.x * (blockDim.x >> 5);
   for (unsigned k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < nc; k += nw) {
@@ -109,16 +120,16 @@ __global__ void k_sssp_push_heavy(const uint2* __restrict__ chunks, const int64_
     const float du = d[c.x];
     const int64_t b = off[c.x] + (int64_t)c.y * kChunk;
     const int64_t e = min(off[c.x + 1], b + kChunk);
-    for (int64_t j = b + lane; j < e; j += 32) relax(__ldg(idx + j), du + __ldg(w + j), d, t, next, cnt);
+    for (int64_t j = b + lane; j < e; j += 32) relax(__ldg(idx + j), du + __ldg(w + j), d, t, next, ncnt);
   }
 }
 
 // Row-based step (pull, Alg. 2 shape P:320 without mask / early exit): a kG-lane group per
 // row j of A^T reduces min_i d(i) + A(i, j) over the in-edges (operand reuse: all of d).
-// Rows longer than kHeavyDeg are left to k_sssp_pull_heavy / k_sssp_pull_finish.
-__global__ void k_sssp_pull(int64_t n, const int64_t* __restrict__ coff, const uint32_t* __restrict__ cidx,
-                            const float* __restrict__ cw, const float* __restrict__ d,
-                            float* __restrict__ t, uint32_t* __restrict__ next, unsigned* __restrict__ cnt) {
+// Rows longer than kHeavyDeg are left to pull_heavy / pull_finish.
+__device__ void pull_light(int64_t n, const int64_t* __restrict__ coff, const uint32_t* __restrict__ cidx,
+                           const float* __restrict__ cw, const float* __restrict__ d,
+                           float* __restrict__ t, uint32_t* __restrict__ next, unsigned* __restrict__ ncnt) {
   const unsigned lane = threadIdx.x & (kG - 1);
   const unsigned gm = group_mask();
   const int64_t gpb = blockDim.x / kG;
@@ -131,17 +142,17 @@ __global__ void k_sssp_pull(int64_t n, const int64_t* __restrict__ coff, const u
     for (int o = kG / 2; o; o >>= 1) m = fminf(m, __shfl_xor_sync(gm, m, o));
     if (lane == 0 && m < d[j]) {
       t[j] = m;
-      next[atomicAdd(cnt, 1u)] = (uint32_t)j;
+      next[atomicAdd(ncnt, 1u)] = (uint32_t)j;
     }
   }
 }
 
 // Heavy rows: one warp per kChunk-edge chunk (descriptors built once per call), partial min
 // folded into cand(j) with atomicMin on the fp32 bits.
-__global__ void k_sssp_pull_heavy(const uint2* __restrict__ chunks, unsigned nc,
-                                  const int64_t* __restrict__ coff, const uint32_t* __restrict__ cidx,
-                                  const float* __restrict__ cw, const float* __restrict__ d,
-                                  float* __restrict__ cand) {
+__device__ void pull_heavy(const uint2* __restrict__ chunks, unsigned nc,
+                           const int64_t* __restrict__ coff, const uint32_t* __restrict__ cidx,
+                           const float* __restrict__ cw, const float* __restrict__ d,
+                           float* __restrict__ cand) {
   const unsigned lane = threadIdx.x & 31;
   const unsigned nw = gridDim.x * (blockDim.x >> 5);
   for (unsigned k = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); k < nc; k += nw) {
@@ -164,16 +175,16 @@ __global__ void k_sssp_pull_heavy(const uint2* __restrict__ chunks, unsigned nc,
 }
 
 // Heavy rows: t(j) = cand(j) where it improves d(j); cand reset to +inf for the next step.
-__global__ void k_sssp_pull_finish(const uint32_t* __restrict__ hrows, unsigned nh, const float* __restrict__ d,
-                                   float* __restrict__ t, float* __restrict__ cand,
-                                   uint32_t* __restrict__ next, unsigned* __restrict__ cnt) {
+__device__ void pull_finish(const uint32_t* __restrict__ hrows, unsigned nh, const float* __restrict__ d,
+                            float* __restrict__ t, float* __restrict__ cand,
+                            uint32_t* __restrict__ next, unsigned* __restrict__ ncnt) {
   for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < nh; k += gridDim.x * blockDim.x) {
     const uint32_t j = hrows[k];
     const float m = cand[j];
     cand[j] = __int_as_float(kInfBits);
     if (m < d[j]) {
       t[j] = m;
-      next[atomicAdd(cnt, 1u)] = j;
+      next[atomicAdd(ncnt, 1u)] = j;
     }
   }
 }
@@ -194,13 +205,109 @@ __global__ void k_sssp_heavy_rows(int64_t n, const int64_t* __restrict__ coff, u
   }
 }
 
-// d_{k+1} = t on the changed set (t == d elsewhere).
-__global__ void k_sssp_commit(const uint32_t* __restrict__ list, const unsigned* __restrict__ cnt,
-                              const float* __restrict__ t, float* __restrict__ d) {
-  const unsigned nf = *cnt;
-  for (unsigned k = blockIdx.x * blockDim.x + threadIdx.x; k < nf; k += gridDim.x * blockDim.x) {
-    const uint32_t v = list[k];
-    d[v] = t[v];
+// Device control block of the persistent loop (in the workspace, zeroed before the launch).
+struct SsspCtl {
+  unsigned long long bar;        // grid barrier: monotone arrivals, bit 63 = abort (watchdog)
+  unsigned pad[30];
+  unsigned cnt[3][4];            // per iteration mod 3: [0] next-frontier length, [1] push chunks
+  long long it, push_it, pull_it, sw;  // stats, written by block 0 at the end
+  int error;                     // PP_ERR_TIMEOUT if a barrier wait timed out
+};
+
+constexpr unsigned long long kSsspAbort = 1ull << 63;
+constexpr unsigned long long kSsspWatchdogNs = 4000000000ull;
+
+__device__ __forceinline__ bool sssp_barrier(SsspCtl* c, unsigned& epoch) {
+  __shared__ int s_ok;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ++epoch;
+    const unsigned long long target = (unsigned long long)epoch * gridDim.x;
+    unsigned long long v = atom_add_release_u64(&c->bar, 1ull) + 1ull;
+    if (v < target) {
+      const unsigned long long t0 = global_timer_ns();
+      while ((v = ld_acquire_u64(&c->bar)) < target) {
+        __nanosleep(32);
+        if (global_timer_ns() - t0 > kSsspWatchdogNs) {
+          atomicExch(&c->error, (int)PP_ERR_TIMEOUT);
+          atomicOr(&c->bar, kSsspAbort);
+          v = kSsspAbort;
+          break;
+        }
+      }
+    }
+    __threadfence();
+    s_ok = (v & kSsspAbort) ? 0 : 1;
+  }
+  __syncthreads();
+  return s_ok != 0;
+}
+
+struct SsspArgs {
+  int64_t n;
+  double alpha;
+  const int64_t *off, *coff;
+  const uint32_t *idx, *cidx;
+  const float *w, *cw;
+  float *d, *t, *cand;
+  uint32_t *la, *lb, *hrows;
+  uint2 *pch, *hch;
+  const unsigned* flags;  // prologue counters: [1] bad weight, [3] heavy rows, [4] their chunks
+  SsspCtl* ctl;
+};
+
+// The whole 2-phase traversal in one cooperative launch: per iteration the step's
+// phase(s), a grid barrier, the commit d = t on the changed list, a grid barrier; the next
+// frontier's length decides termination and the single push -> pull switch identically in
+// every CTA (R28, R29).
+__global__ void __launch_bounds__(kLoopT, 2) k_sssp_loop(SsspArgs a) {
+  SsspCtl* c = a.ctl;
+  if (a.flags[1]) return;  // a negative or NaN weight: the host reports PP_ERR_GRAPH
+  const unsigned nh = a.flags[3], nhc = a.flags[4];
+  unsigned epoch = 0;
+  long long it = 0, push_it = 0, pull_it = 0, sw = -1;
+  int dir = 0;
+  unsigned nf = 1;
+  uint32_t *f = a.la, *nx = a.lb;
+  const unsigned gtid = blockIdx.x * blockDim.x + threadIdx.x, gsize = gridDim.x * blockDim.x;
+  while (nf > 0) {
+    if (dir == 0 && (double)nf / (double)a.n > a.alpha) {  // the one switch (R29)
+      dir = 1;
+      sw = it;
+    }
+    unsigned* cc = c->cnt[it % 3];
+    // the counters of iteration it+1 were last read in iteration it-2: two barriers ago
+    if (blockIdx.x == 0 && threadIdx.x < 4) c->cnt[(it + 1) % 3][threadIdx.x] = 0u;
+    if (dir == 0) {
+      push_light(f, nf, a.off, a.idx, a.w, a.d, a.t, nx, &cc[0], a.pch, &cc[1]);
+      if (!sssp_barrier(c, epoch)) return;
+      push_heavy(a.pch, ld_relaxed_u32(&cc[1]), a.off, a.idx, a.w, a.d, a.t, nx, &cc[0]);
+      ++push_it;
+    } else {
+      pull_light(a.n, a.coff, a.cidx, a.cw, a.d, a.t, nx, &cc[0]);
+      if (nhc) pull_heavy(a.hch, nhc, a.coff, a.cidx, a.cw, a.d, a.cand);
+      if (!sssp_barrier(c, epoch)) return;
+      if (nh) pull_finish(a.hrows, nh, a.d, a.t, a.cand, nx, &cc[0]);
+      ++pull_it;
+    }
+    if (!sssp_barrier(c, epoch)) return;
+    const unsigned nn = ld_relaxed_u32(&cc[0]);
+    for (unsigned k = gtid; k < nn; k += gsize) {  // d_{k+1} = t on the changed set
+      const uint32_t v = nx[k];
+      a.d[v] = a.t[v];
+    }
+    if (!sssp_barrier(c, epoch)) return;
+    nf = nn;
+    uint32_t* tmp = f;
+    f = nx;
+    nx = tmp;
+    ++it;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    c->it = it;
+    c->push_it = push_it;
+    c->pull_it = pull_it;
+    c->sw = sw;
   }
 }
 
@@ -249,10 +356,9 @@ extern "C" pp_status pp_sssp(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* 
   float* cand = nullptr;
   const int64_t nch_max = nnz / kHeavyDeg + 1;  // ceil(deg/kChunk) <= deg/kHeavyDeg for heavy rows
   unsigned* cnt = nullptr;
+  SsspCtl* ctl = nullptr;
   unsigned h[5] = {0, 0, 0, 0, 0};
-  int64_t it = 0, push_it = 0, pull_it = 0, sw = -1;
-  int dir = 0;  // 0 push, 1 pull
-  unsigned nf = 1;
+  SsspCtl hc;
   SS_CK(cudaSetDevice(ctx->device), "pp_sssp: cudaSetDevice");
   {  // structural check of the caller's arrays: off[0] = 0 and off[n] = nnz on both sides
     int64_t ends[4] = {-1, -1, -1, -1};
@@ -272,7 +378,7 @@ extern "C" pp_status pp_sssp(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* 
   {  // workspace cached in the context (grown on demand, freed by pp_ctx_destroy): no
      // per-call allocation and no change to any process-wide allocator state
     const size_t need = sizeof(float) * n * 2 + sizeof(uint32_t) * n * 3 +
-                        sizeof(uint2) * (size_t)nch_max * 2 + 256 * 9;
+                        sizeof(uint2) * (size_t)nch_max * 2 + 256 * 9 + sizeof(SsspCtl) + 256;
     if (ctx->sssp_ws_bytes < need) {
       if (ctx->sssp_ws) cudaFree(ctx->sssp_ws);
       ctx->sssp_ws = nullptr;
@@ -294,6 +400,7 @@ extern "C" pp_status pp_sssp(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* 
     pch = (uint2*)carve(sizeof(uint2) * nch_max);
     hch = (uint2*)carve(sizeof(uint2) * nch_max);
     cnt = (unsigned*)carve(sizeof(unsigned) * 8);
+    ctl = (SsspCtl*)carve(sizeof(SsspCtl));
   }
   k_sssp_init<<<grid_for(n, kT, cap), kT, 0, s>>>(n, source, dist, t, la, cnt);
   ctx->launches++;
@@ -304,48 +411,47 @@ extern "C" pp_status pp_sssp(pp_ctx ctx, int64_t n, int64_t nnz, const int64_t* 
   }
   k_sssp_heavy_rows<<<grid_for(n, kT, cap), kT, 0, s>>>(n, csc_off, hrows, hch, cand, cnt);
   ctx->launches++;
+  SS_CK(cudaMemsetAsync(ctl, 0, sizeof(SsspCtl), s), "pp_sssp: reset control block");
+  {  // the iteration loop: one persistent cooperative launch, then one synchronisation
+    static std::mutex mu;
+    static std::map<int, int> grid_cache;  // per device: co-resident CTAs of k_sssp_loop
+    int grid = 0;
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      auto itg = grid_cache.find(ctx->device);
+      if (itg == grid_cache.end()) {
+        int per = 0;
+        SS_CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_sssp_loop, kLoopT, 0),
+              "pp_sssp: occupancy");
+        grid_cache[ctx->device] = ctx->num_sms * (per > 0 ? per : 1);
+      }
+      grid = grid_cache[ctx->device];
+    }
+    SsspArgs args{n, alpha, csr_off, csc_off, csr_idx, csc_idx, csr_w, csc_w, dist, t, cand,
+                  la, lb, hrows, pch, hch, cnt, ctl};
+    void* params[] = {(void*)&args};
+    SS_CK(cudaLaunchCooperativeKernel((const void*)k_sssp_loop, dim3(grid), dim3(kLoopT), params, 0, s),
+          "pp_sssp: persistent loop");
+    ctx->launches++;
+  }
   SS_CK(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, s), "pp_sssp: read flags");
-  SS_CK(cudaStreamSynchronize(s), "pp_sssp: init");
+  SS_CK(cudaMemcpyAsync(&hc, ctl, sizeof(SsspCtl), cudaMemcpyDeviceToHost, s), "pp_sssp: read stats");
+  SS_CK(cudaStreamSynchronize(s), "pp_sssp: run");
   if (h[1]) {
     set_error("pp_sssp: negative or NaN edge weight (SPEC S:342)");
     st = PP_ERR_GRAPH;
     goto out;
   }
-  while (nf > 0) {
-    if (dir == 0 && (double)nf / (double)n > alpha) {  // the one switch (R29)
-      dir = 1;
-      sw = it;
-    }
-    SS_CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * 3, s), "pp_sssp: reset counters");
-    if (dir == 0) {
-      k_sssp_push<<<grid_for(nf, kT / kG, cap), kT, 0, s>>>(la, nf, csr_off, csr_idx, csr_w, dist, t, lb, cnt, pch);
-      k_sssp_push_heavy<<<cap, kT, 0, s>>>(pch, csr_off, csr_idx, csr_w, dist, t, lb, cnt);
-      push_it++;
-    } else {
-      k_sssp_pull<<<cap, kT, 0, s>>>(n, csc_off, csc_idx, csc_w, dist, t, lb, cnt);
-      if (h[3]) {
-        k_sssp_pull_heavy<<<cap, kT, 0, s>>>(hch, h[4], csc_off, csc_idx, csc_w, dist, cand);
-        k_sssp_pull_finish<<<grid_for(h[3], kT, cap), kT, 0, s>>>(hrows, h[3], dist, t, cand, lb, cnt);
-        ctx->launches += 2;
-      }
-      pull_it++;
-    }
-    k_sssp_commit<<<cap, kT, 0, s>>>(lb, cnt, t, dist);
-    ctx->launches += 3;
-    SS_CK(cudaGetLastError(), "pp_sssp: launch");
-    SS_CK(cudaMemcpyAsync(h, cnt, sizeof(unsigned), cudaMemcpyDeviceToHost, s), "pp_sssp: read count");
-    SS_CK(cudaStreamSynchronize(s), "pp_sssp: step");
-    nf = h[0];
-    uint32_t* tmp = la;
-    la = lb;
-    lb = tmp;
-    it++;
+  if (hc.error) {
+    set_error("pp_sssp: a grid barrier timed out (watchdog)");
+    st = (pp_status)hc.error;
+    goto out;
   }
   if (stats) {
-    stats->iterations = it;
-    stats->push_iterations = push_it;
-    stats->pull_iterations = pull_it;
-    stats->switch_iteration = sw;
+    stats->iterations = hc.it;
+    stats->push_iterations = hc.push_it;
+    stats->pull_iterations = hc.pull_it;
+    stats->switch_iteration = hc.sw;
   }
 out:
   return st;
