@@ -32,9 +32,9 @@ def build(force=False, verbose=False):
     extra += ["-DPP_IDX_NOALLOC"] if os.environ.get("PP_IDX_NOALLOC") else []
     extra += [f"-D{k}" for k in ("PP_KO_DEPTH", "PP_KO_PROBE", "PP_KO_RESID") if os.environ.get(k)]
     extra += [f"-D{k}={os.environ[k]}" for k in ("PP_FAST_NTH", "PP_PUSH_KU", "PP_STEAL",
-                                                   "PP_PULL_PF", "PP_LOWLAT_VREC", "PP_PF_ROWS",
+                                                   "PP_LOWLAT_VREC", "PP_PF_ROWS",
                                                    "PP_SUM_RESID", "PP_DENSE", "PP_DENSE_R",
-                                                   "PP_DENSE_MIN8", "PP_DENSE_IW", "PP_SPARSE_REC",
+                                                   "PP_DENSE_MIN8", "PP_DENSE_IW",
                                                    "PP_CHUNK", "PP_HEAVY", "PP_RQ_EXTRA")
               if os.environ.get(k)]
     odir = os.path.join(HERE, "build")

@@ -44,7 +44,6 @@ struct BfsArgs {
   uint32_t* vis0;
   uint32_t* vis1;
   uint32_t* fr;  // frontier bitmap written by pull levels (push-from-bitmap)
-  const uint32_t* __restrict__ head;  // first 8 in-neighbours of every row (pull), 32 B each
   const uint32_t* __restrict__ drec;  // PP_DENSE: 32-byte rows {6 in-neighbours, caller, in-degree}
   long long n_noniso;                 // rows not pre-marked visited (isolated / padding)
   uint32_t* sumv;      // visited summary: bit per 2^sum_shift vertices, isolated excluded
@@ -605,9 +604,6 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
 #ifndef PP_SUM_RESID
 #define PP_SUM_RESID 0  // with PP_SUM_WORDS > 0: the summary serves the residual tiers only
 #endif
-#ifndef PP_PULL_PF
-#define PP_PULL_PF 0  // 1: L2 prefetch of the next round's row head / offsets / caller id
-#endif
 #ifndef PP_STEAL
 #define PP_STEAL 0    // > 0: per-CTA item counters in global memory; a warp whose CTA ran out
                       // of items claims items of up to PP_STEAL other CTAs (tail balance)
@@ -770,7 +766,7 @@ struct PullCtx {
       uint32_t rem = q.rem[slot];
       if (rem & kRelP) {  // dense pull: p is relative to the row's begin
         rem &= ~kRelP;
-        p += a.coff[i];
+        p += a.coff[D ? i - (uint32_t)a.lo : i];
       }
       e = p + (Off)rem;
       degin = q.degin[slot];
@@ -917,10 +913,6 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
   const uint32_t lo = D ? (uint32_t)a.lo : 0u;
   // ABL: the Table-2 ablation kernel; the default kernel compiles the toggles out
   const bool no_mask = ABL && (a.toggles & PP_OPT_NO_MASKING) != 0;
-  // PP_SPARSE_REC: candidates read the dense pull's 32-byte row record (one load: 6 ids,
-  // caller id, in-degree) instead of head + offsets + caller id (three)
-  const bool usrec = !D && PP_SPARSE_REC && a.drec != nullptr;
-  const int hlen = usrec ? kDenseHead : 8;  // in-neighbour ids in the record / head
   PullCtx<Off, PARENTS, D> C{a, vin, vout, d, !ABL || !(a.toggles & PP_OPT_NO_EARLYEXIT),
                              ABL && (a.toggles & PP_OPT_NO_REUSE) != 0, acc, sfound, rq, ssum,
                              a.H0, &out->work2, fr};
@@ -1024,41 +1016,20 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
         par[t] = kNone;
         rb[t] = e[t] = 0;
       }
-#if PP_PULL_PF
-      {  // the next round's candidate rows: their head / offsets / caller-id lines into L2
-        const unsigned k2 = base + 32u * kC + lane;
-        const unsigned j2 = warp_owner(incl, k2);
-        const uint32_t m2 = __shfl_sync(kFull, cand, j2);
-        const unsigned x2 = __shfl_sync(kFull, excl, j2);
-        if (k2 < tot) {
-          const uint32_t i2 = wbase * 32u + j2 * 32u + nth_set_bit(m2, k2 - x2);
-          const uint32_t l2 = i2 - lo;
-          prefetch_l2(a.head + (size_t)l2 * 8u);
-          prefetch_l2(a.coff + l2);
-          if (!D && a.perm) prefetch_l2(a.perm + i2);
-        }
-      }
-#endif
-      // stage: offsets and the row's head (first 8 in-neighbours = one 32-byte sector, one
-      // 256-bit load from a row-contiguous array: dense items stream it), all in flight
+      // stage: the row's 32-byte record {first 6 in-neighbours, caller id (multi-rank: block
+      // slot), in-degree}: one 256-bit load from a row-contiguous array (an ELL head in front of
+      // the CSR tail); positions are row-relative [0, deg) until a parked row needs its begin
       V8 hd[kC];
-      uint32_t dpos[kC];  // caller id of the row (relabelled graph: loaded with the head)
+      uint32_t dpos[kC];  // where the row's depth goes
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
         const uint32_t li = i[t] - lo;  // row of the CSC block (lo = 0 on one GPU)
         dpos[t] = li;
         if (valid[t]) {
-          if (usrec) {  // one 32-byte record: 6 ids, caller id, in-degree; row-relative [0, deg)
-            hd[t] = ld_nc_v8(a.drec + (size_t)li * 8u);
-            dpos[t] = hd[t].x[6];
-            rb[t] = 0;
-            e[t] = (Off)hd[t].x[7];
-          } else {
-            if (!D && a.perm) dpos[t] = a.perm[i[t]];
-            rb[t] = a.coff[li];
-            e[t] = a.coff[li + 1];
-            hd[t] = ld_nc_v8(a.head + (size_t)li * 8u);
-          }
+          hd[t] = ld_nc_v8(a.drec + (size_t)li * 8u);
+          dpos[t] = hd[t].x[6];
+          rb[t] = 0;
+          e[t] = (Off)hd[t].x[7];
         }
       }
       // stage: probe the first neighbour, then the other head ids of rows that missed
@@ -1074,18 +1045,18 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
       for (int t = 0; t < kC; ++t) {
         const Off deg = e[t] - rb[t];
         if (valid[t] && deg > 1 && !(found[t] && C.early_exit)) {
-          bool h[8];
+          bool h[kDenseHead];
 #pragma unroll
-          for (int q = 1; q < 8; ++q) h[q] = q < hlen && deg > (Off)q && C.hit(hd[t].x[q]);
+          for (int q = 1; q < kDenseHead; ++q) h[q] = deg > (Off)q && C.hit(hd[t].x[q]);
 #pragma unroll
-          for (int q = 1; q < 8; ++q) {
+          for (int q = 1; q < kDenseHead; ++q) {
             if (h[q] && !found[t]) {
               found[t] = true;
               par[t] = hd[t].x[q];
             }
           }
         }
-        p[t] = (valid[t] && deg > (Off)hlen) ? rb[t] + (Off)hlen : e[t];  // the tail continues in idx
+        p[t] = (valid[t] && deg > (Off)kDenseHead) ? (Off)kDenseHead : e[t];  // tail continues in idx
       }
 #pragma unroll
       for (int t = 0; t < kC; ++t) {
@@ -1098,11 +1069,10 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
           const int slot = qn + __popc(pm & lanemask_lt());
           rq.i[slot] = fresh[t] ? i[t] : kNone - 1;  // visited rows (no masking) never commit
           rq.par[slot] = (found[t] || !fresh[t]) ? (found[t] ? par[t] : 0u) : kNone;
-          // record: p is row-relative; the batch adds coff[i] (rows that cannot commit, i.e.
+          // p is row-relative: the batch adds the row begin (rows that cannot commit, i.e.
           // visited rows of the no-masking ablation, carry no row id: made absolute here)
-          const bool rel = usrec && fresh[t];
-          rq.p[slot] = (usrec && !fresh[t]) ? a.coff[i[t] - lo] + p[t] : p[t];
-          rq.rem[slot] = (uint32_t)(e[t] - p[t]) | (rel ? kRelP : 0u);
+          rq.p[slot] = fresh[t] ? p[t] : a.coff[i[t] - lo] + p[t];
+          rq.rem[slot] = (uint32_t)(e[t] - p[t]) | (fresh[t] ? kRelP : 0u);
           rq.degin[slot] = (uint32_t)(e[t] - rb[t]);
         }
         qn += __popc(pm);
@@ -2052,7 +2022,6 @@ static cudaError_t launch_off(pp_graph g, uint32_t source, int mode, int rule, d
   a.vis1 = g->vis[1];
   a.fr = g->fr;
   a.sumv = g->sumv;
-  a.head = g->head;
   a.drec = g->drec;
   a.n_noniso = g->n_noniso;
   a.sum_shift = g->sum_shift;
@@ -2143,11 +2112,11 @@ static cudaError_t launch_ranks_t(pp_graph* gs, int P, uint32_t source, int mode
     a.coff = (const Off*)g->coff;
     a.cidx = g->cidx;
     a.symmetric = g->symmetric ? 1 : 0;
+    a.drec = g->drec;
     a.isolated = g->isolated;
     a.vis0 = g->vis[0];
     a.vis1 = g->vis[1];
     a.fr = g->xfr[0];
-    a.head = g->head;
     a.sumv = nullptr;
     a.sum_shift = 3;
     a.sum_words = 0;

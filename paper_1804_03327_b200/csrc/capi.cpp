@@ -75,7 +75,7 @@ void free_graph(pp_graph g) {
     if (g->ipc_base[q]) cudaIpcCloseMemHandle(g->ipc_base[q]);
   const bool alias = g->dist ? false : g->symmetric;  // multi-rank: coff/off are distinct
   void* ptrs[] = {g->off, g->idx, alias ? nullptr : g->coff,
-                  (alias || g->cidx == g->idx) ? nullptr : (void*)g->cidx, g->isolated, g->head,
+                  (alias || g->cidx == g->idx) ? nullptr : (void*)g->cidx, g->isolated,
                   g->vis[0], g->vis[1], g->fr, g->sumv,
                   g->L[0], g->L[1], g->H[0], g->H[1], g->ctr, g->stats, g->bar,
                   g->sbits[0], g->sbits[1], g->sbits[2], g->sbits[3], g->sblock, g->hubq, g->scount,
@@ -293,8 +293,13 @@ pp_status upload_block(pp_ctx ctx, int64_t n, int64_t row_lo, int64_t row_hi, in
       PP_CK(cudaStreamSynchronize(st), "sync");
     }
   }
-  if ((s = dalloc(&g->head, (size_t)std::max<int64_t>(len, 1) * 8, &bytes, "row heads")) != PP_OK) return s;
-  PP_CK(launch_head(g, d_coff, g->cidx, len), "row heads");
+  {  // pull row records of the block's rows (ids global, caller id = block slot), padded to the
+     // owned words
+    const size_t words = (size_t)std::max<int64_t>(g->chunk_words, 1) * 32 * 8;
+    if ((s = dalloc(&g->drec, words, &bytes, "pull row records")) != PP_OK) return s;
+    PP_CK(cudaMemsetAsync(g->drec, 0, words * 4, st), "memset row records");
+    PP_CK(launch_drec(g, d_coff, g->cidx, len), "row records");
+  }
   if ((s = dalloc(&g->isolated, g->nwords, &bytes, "isolated")) != PP_OK) return s;
   PP_CK(cudaMemsetAsync(g->isolated, 0, sizeof(uint32_t) * g->nwords, st), "memset");
   if (!symmetric && (s = dalloc(&g->odeg, (size_t)std::max<int64_t>(len, 1), &bytes, "out-degrees")) != PP_OK)
@@ -611,11 +616,9 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t row_lo, int64_t row_hi,
     }
   }
   if ((s = dalloc(&g->isolated, g->nwords, &bytes, "isolated")) != PP_OK) return s;
-  // pull row data: the 32-byte dense records (32-bit offsets), which the sparse pull reads too
-  // (PP_SPARSE_REC), else the 8-id row heads
-  if (!(kDense && !g->off64 && PP_SPARSE_REC) &&
-      (s = dalloc(&g->head, (size_t)n * 8, &bytes, "row heads")) != PP_OK) return s;
-  if (kDense && !g->off64) {
+  // pull row data: one 32-byte record per row {first 6 in-neighbours, caller id, in-degree},
+  // read by the sparse pull per candidate and streamed by the dense pull per bitmap word
+  {
     const size_t words = (size_t)g->nwords * 32 * 8;  // 32 B per row incl. padding rows
     if ((s = dalloc(&g->drec, words, &bytes, "dense pull records")) != PP_OK) return s;
     PP_CK(cudaMemsetAsync(g->drec, 0, words * 4, st), "memset dense records");
@@ -627,6 +630,9 @@ pp_status pp_graph_upload(pp_ctx ctx, int64_t n, int64_t row_lo, int64_t row_hi,
   g->hcap = (int64_t)std::max(g->scount_host[0], g->scount_host[1]);
   g->max_out_deg = (int64_t)g->scount_host[2];
   g->n_noniso = (int64_t)g->nwords * 32 - (int64_t)g->scount_host[4];
+  if (g->scount_host[3] >= (1ull << 31))  // residual queue: 31-bit remaining lengths
+    PP_FAIL(PP_ERR_UNSUPPORTED, "pp_graph_upload: a row of A^T has %llu >= 2^31 entries",
+            (unsigned long long)g->scount_host[3]);
 
   // BFS / mxv working set
   for (int k = 0; k < 2; ++k) {

@@ -31,8 +31,10 @@ __global__ void k_isolated(const int64_t* __restrict__ off, const int64_t* __res
   if (cnt) atomicAdd(niso, cnt);
 }
 
-// PP_DENSE: the dense pull's row record {in-neighbours 0..5 (0xFFFFFFFF-padded), caller id,
-// in-degree}, 32 bytes, so one 1 KB bulk copy brings a bitmap word's 32 rows.  Rows >= n
+// Pull row record {in-neighbours 0..5 (0xFFFFFFFF-padded), caller id (perm == nullptr: the row
+// itself, i.e. the block slot of a multi-rank block), in-degree}, 32 bytes: the sparse pull's
+// one load per candidate (an ELL head in front of the CSR tail); one 1 KB bulk copy brings a
+// bitmap word's 32 rows to the dense pull.  Rows >= n
 // (padding of the last words) stay zero (in-degree 0; they are pre-marked visited anyway).
 __global__ void k_drec(const int64_t* __restrict__ coff, const uint32_t* __restrict__ cidx,
                        const uint32_t* __restrict__ perm, int64_t n, uint32_t* __restrict__ drec) {
@@ -50,28 +52,6 @@ __global__ void k_drec(const int64_t* __restrict__ coff, const uint32_t* __restr
     r1.w = (uint32_t)d;
     reinterpret_cast<uint4*>(drec)[2 * v] = r0;
     reinterpret_cast<uint4*>(drec)[2 * v + 1] = r1;
-  }
-}
-
-// Pull-side row heads: the first 8 in-neighbours of every row (CSC), 0xFFFFFFFF-padded,
-// 32 bytes per vertex.  A row-contiguous sector per vertex lets the pull decide most rows
-// without a scattered access into the id array (ELL head + CSR tail).
-__global__ void k_head(const int64_t* __restrict__ coff, const uint32_t* __restrict__ cidx,
-                       int64_t n, uint32_t* __restrict__ head) {
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = coff[v], d = coff[v + 1] - b;
-    uint4 h0, h1;
-    h0.x = d > 0 ? cidx[b] : 0xFFFFFFFFu;
-    h0.y = d > 1 ? cidx[b + 1] : 0xFFFFFFFFu;
-    h0.z = d > 2 ? cidx[b + 2] : 0xFFFFFFFFu;
-    h0.w = d > 3 ? cidx[b + 3] : 0xFFFFFFFFu;
-    h1.x = d > 4 ? cidx[b + 4] : 0xFFFFFFFFu;
-    h1.y = d > 5 ? cidx[b + 5] : 0xFFFFFFFFu;
-    h1.z = d > 6 ? cidx[b + 6] : 0xFFFFFFFFu;
-    h1.w = d > 7 ? cidx[b + 7] : 0xFFFFFFFFu;
-    reinterpret_cast<uint4*>(head)[2 * v] = h0;
-    reinterpret_cast<uint4*>(head)[2 * v + 1] = h1;
   }
 }
 
@@ -125,9 +105,9 @@ cudaError_t launch_off_narrow(pp_graph g, const int64_t* in, void* out, int64_t 
   else k_off_narrow<uint32_t><<<blocks, kBlock, 0, g->ctx->stream>>>(in, (uint32_t*)out, m);
   return cudaGetLastError();
 }
-cudaError_t launch_head(pp_graph g, const int64_t* coff, const uint32_t* cidx, int64_t rows) {
+cudaError_t launch_drec(pp_graph g, const int64_t* coff, const uint32_t* cidx, int64_t rows) {
   g->ctx->launches += 1;
-  k_head<<<g->ctx->num_sms * 8, kBlock, 0, g->ctx->stream>>>(coff, cidx, rows, g->head);
+  k_drec<<<g->ctx->num_sms * 8, kBlock, 0, g->ctx->stream>>>(coff, cidx, nullptr, rows, g->drec);
   return cudaGetLastError();
 }
 cudaError_t launch_hcap(pp_graph g, const int64_t* off, int64_t rows, unsigned long long* d_cap,
@@ -172,8 +152,7 @@ cudaError_t launch_graph_prepare(pp_graph g, const int64_t* d_off64, const int64
     *launches += 1;
     k_vrec<<<blocks, kBlock, 0, st>>>(d_off64, g->perm, g->n, g->vrec);
   }
-  *launches += g->head ? 4 : 3;
-  if (g->head) k_head<<<blocks, kBlock, 0, st>>>(d_coff64, g->cidx, g->n, g->head);
+  *launches += 3;
   if (g->drec) {
     *launches += 1;
     k_drec<<<blocks, kBlock, 0, st>>>(d_coff64, g->cidx, g->perm, g->n, g->drec);

@@ -61,9 +61,6 @@ constexpr bool kDense = PP_DENSE != 0;
 #ifndef PP_DENSE_MIN8
 #define PP_DENSE_MIN8 2
 #endif
-#ifndef PP_SPARSE_REC
-#define PP_SPARSE_REC 1
-#endif
 constexpr int kDenseR = kDense ? PP_DENSE_R : 0;  // ring slots (32 rows x 32 B) per warp
 #ifndef PP_DENSE_IW
 #define PP_DENSE_IW 8
@@ -166,7 +163,6 @@ struct pp_graph_s {
   void* coff = nullptr;  // CSC (in-neighbours); aliases off when symmetric
   uint32_t* cidx = nullptr;
   uint32_t* isolated = nullptr;  // nwords: bit = no in- and no out-edges, or padding
-  uint32_t* head = nullptr;      // 8n: first 8 in-neighbours of every row (pull heads)
   uint32_t* drec = nullptr;      // PP_DENSE: per row {first 6 in-neighbours, caller id, in-degree}
                                  // (32 B; nwords*32 rows, padding rows zero)
   int64_t n_noniso = 0;          // rows not marked isolated / padding
@@ -247,7 +243,7 @@ cudaError_t launch_graph_prepare(pp_graph g, const int64_t* d_off64, const int64
 cudaError_t launch_graph_validate(pp_graph g, const int64_t* d_off64, const uint32_t* d_idx,
                                   unsigned long long* d_bad, uint64_t* launches, int64_t rows = -1);
 cudaError_t launch_off_narrow(pp_graph g, const int64_t* in, void* out, int64_t m);
-cudaError_t launch_head(pp_graph g, const int64_t* coff, const uint32_t* cidx, int64_t rows);
+cudaError_t launch_drec(pp_graph g, const int64_t* coff, const uint32_t* cidx, int64_t rows);
 cudaError_t launch_hcap(pp_graph g, const int64_t* off, int64_t rows, unsigned long long* d_cap,
                         unsigned long long* d_max);
 int bfs_grid_size(pp_graph g, bool parents);
