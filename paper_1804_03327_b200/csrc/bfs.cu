@@ -356,7 +356,7 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
                                             const uint32_t (&u)[kU], const uint32_t (&w)[kU],
                                             uint32_t* vis, int newdepth, uint4* Lout,
                                             uint2* Hout, LevelCtr* out, Acc& acc, bool lowlat,
-                                            uint32_t* frout) {
+                                            uint32_t* frout, bool& xfull) {
   uint32_t cur[kU];
   bool disc[kU];
   Off sb[kU], se[kU];
@@ -423,16 +423,33 @@ __device__ __forceinline__ void push_visit4(const BfsArgs<Off>& a, const bool (&
   for (int t = 0; t < kU; ++t) any = any || disc[t];
   if (!__any_sync(kFull, any)) return;
   if (D) {
+    // the id list the exchange sends instead of the bitmap slice when it is shorter: slots are
+    // reserved with ONE atomic per warp step (a per-discovery atomic on one counter serialised
+    // in one L2 slice: C5's big push level took 4.7 ms instead of 0.4)
+    unsigned dm[kU], ndisc = 0;
 #pragma unroll
     for (int t = 0; t < kU; ++t) {
+      dm[t] = __ballot_sync(kFull, disc[t]);
+      ndisc += __popc(dm[t]);
+    }
+    // once this warp has seen the list overflow the slice, it stops counting (nX only has to
+    // be exact below wcnt: the exchange sends the list only then)
+    unsigned xbase = a.wcnt;
+    if (!xfull) {
+      if (lane_id() == 0) xbase = atomicAdd(&out->nX, ndisc);
+      xbase = __shfl_sync(kFull, xbase, 0);
+      xfull = xbase + ndisc >= a.wcnt;
+    }
+#pragma unroll
+    for (int t = 0; t < kU; ++t) {
+      const unsigned slot = xbase + __popc(dm[t] & lanemask_lt());
+      xbase += __popc(dm[t]);
       if (!disc[t]) continue;
       const uint32_t r = w[t] - (uint32_t)a.lo;  // local row of the owned target
       const Off degin = a.coff[r + 1] - a.coff[r];
       const Off dg = a.symmetric ? degin : (Off)a.odeg[r];
       a.depth[r] = newdepth;
       atomicOr(&frout[w[t] >> 5], 1u << (w[t] & 31u));
-      // the id list the exchange sends instead of the bitmap slice when it is shorter
-      const unsigned slot = atomicAdd(&out->nX, 1u);
       if (slot < a.wcnt) a.xown[slot] = w[t];
       acc.c += 1;
       acc.mf += (unsigned long long)dg;
@@ -484,7 +501,7 @@ template <typename Off, bool PARENTS, bool D>
 __device__ __forceinline__ void push_round(const BfsArgs<Off>& a, uint32_t v, Off b, unsigned deg,
                                            uint4* Lout, uint2* Hout, LevelCtr* out,
                                            uint32_t* vis, int newdepth, Acc& acc, bool lowlat,
-                                           uint32_t* frout) {
+                                           uint32_t* frout, bool& xfull) {
   const unsigned lane = lane_id();
   const unsigned incl = warp_incl_scan(deg);
   const unsigned excl = incl - deg;
@@ -503,7 +520,7 @@ __device__ __forceinline__ void push_round(const BfsArgs<Off>& a, uint32_t v, Of
       w[t] = valid[t] ? a.idx[bj + (Off)(e - xj)] : 0u;
     }
     push_visit4<Off, PARENTS, D>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat,
-                                 frout);
+                                 frout, xfull);
   }
 }
 
@@ -527,6 +544,7 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
                            unsigned* sctr, bool lowlat, uint32_t* frout) {
   const unsigned lane = lane_id();
   const unsigned NW = nwarps(a);
+  bool xfull = false;  // multi-rank: this warp saw the level's id list overflow its slice
   unsigned R = 32;
   while (R > 1 && (nL + R / 2 - 1) / (R / 2) <= NW) R >>= 1;
   const unsigned nRounds = fr ? a.nwords / kPW : (nL + R - 1) / R;
@@ -557,7 +575,7 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
           w[t] = valid[t] ? a.idx[p] : 0u;
         }
         push_visit4<Off, PARENTS, D>(a, valid, u, w, vis, newdepth, Lout, Hout, out, acc, lowlat,
-                                     frout);
+                                     frout, xfull);
       }
     } else if (!fr) {
       const unsigned i = (item - nHC) * R + lane;
@@ -570,7 +588,8 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
         deg = le.y;
         b = light_begin<Off>(le);
       }
-      push_round<Off, PARENTS, D>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc, lowlat, frout);
+      push_round<Off, PARENTS, D>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc, lowlat, frout,
+                                  xfull);
     } else {
       const unsigned wbase = (item - nHC) * kPW;
       const uint32_t fw = lane < kPW ? fr[wbase + lane] : 0u;
@@ -592,12 +611,15 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
           deg = (unsigned)(a.off[v + 1] - b);
         }
         push_round<Off, PARENTS, D>(a, v, b, deg, Lout, Hout, out, vis, newdepth, acc, lowlat,
-                                    frout);
+                                    frout, xfull);
       }
     }
   }
 }
 
+#ifndef PP_DENSE_DIST
+#define PP_DENSE_DIST 0  // dense pull on multi-rank blocks: measured slower (their rows are not
+#endif                   // degree-ordered: the first record id rarely decides)
 #ifndef PP_PULL_KC
 #define PP_PULL_KC 1
 #endif
@@ -1177,16 +1199,20 @@ __device__ __forceinline__ DenseRing dense_ring(unsigned char* dyn, size_t off) 
   return r;
 }
 
-template <typename Off, bool PARENTS>
+template <typename Off, bool PARENTS, bool D>
 __device__ void pull_dense(const BfsArgs<Off>& a, const uint32_t* __restrict__ vin,
                            uint32_t* __restrict__ vout, LevelCtr* out, int d, Acc& acc,
                            uint32_t* sfound, ResidualQ<Off>& rq, unsigned* sctr, uint32_t* fr,
                            const DenseRing& R) {
   const unsigned lane = lane_id();
-  PullCtx<Off, PARENTS, false> C{a, vin, vout, d, true, false, acc, sfound, rq, nullptr,
-                                 a.H0, &out->work2, fr};
+  PullCtx<Off, PARENTS, D> C{a, vin, vout, d, true, false, acc, sfound, rq, nullptr,
+                             a.H0, &out->work2, fr};
   int qn = 0;
-  const unsigned nitems = a.nwords / kDenseIW;
+  // multi-rank (D): the items cover the owned words [wlo, wlo + wcnt), whose records are the
+  // block's (row i - lo); one GPU: all words, wlo = lo = 0
+  const unsigned wb0 = D ? a.wlo : 0u;
+  const uint32_t lo = D ? (uint32_t)a.lo : 0u;
+  const unsigned nitems = (D ? a.wcnt : a.nwords) / kDenseIW;
   const unsigned G = (unsigned)a.ncta;
   const unsigned cta = cta_of(a);
   const unsigned K = nitems > cta ? (nitems - cta + G - 1) / G : 0u;
@@ -1202,7 +1228,7 @@ __device__ void pull_dense(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
     unsigned j = 0;
     if (lane == 0) j = atomicAdd(sctr, 1u);
     j = __shfl_sync(kFull, j, 0);
-    vw_out = (j < K && lane < kDenseIW) ? vin[(cta + j * G) * kDenseIW + lane] : 0xFFFFFFFFu;
+    vw_out = (j < K && lane < kDenseIW) ? vin[wb0 + (cta + j * G) * kDenseIW + lane] : 0xFFFFFFFFu;
     return j;
   };
   uint32_t nvw;
@@ -1211,7 +1237,7 @@ __device__ void pull_dense(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
     while (pneed == 0) {
       if (nk >= K) return false;
       pk = nk;
-      pbase = (cta + pk * G) * kDenseIW;
+      pbase = wb0 + (cta + pk * G) * kDenseIW;
       pvw = nvw;
       nk = grab_item(nvw);
       const bool need = pvw != 0xFFFFFFFFu;
@@ -1237,7 +1263,7 @@ __device__ void pull_dense(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
         R.word[slot] = pbase + j;
         R.vw[slot] = vwj;
         mbar_arrive_tx(&R.bar[slot], 1024u);
-        bulk_g2s(R.rec + slot * 256u, a.drec + (size_t)(pbase + j) * 256u, 1024u, &R.bar[slot]);
+        bulk_g2s(R.rec + slot * 256u, a.drec + (size_t)(pbase + j - wb0) * 256u, 1024u, &R.bar[slot]);
       }
       ++issued;
     }
@@ -1272,9 +1298,10 @@ __device__ void pull_dense(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
     }
     const uint32_t i = w * 32u + lane;
     if (found) {
-      a.depth[r1.z] = d + 1;
-      if (PARENTS) a.parent[i] = par;
-      const Off odg = a.symmetric ? (Off)dg : (Off)(a.off[i + 1] - a.off[i]);
+      a.depth[r1.z] = d + 1;  // caller id (multi-rank: the block slot i - lo)
+      if (PARENTS) a.parent[i - lo] = par;
+      const Off odg = a.symmetric ? (Off)dg
+                                  : (D ? (Off)a.odeg[i - lo] : (Off)(a.off[i + 1] - a.off[i]));
       acc.c += 1;
       acc.mf += (unsigned long long)odg;
       acc.mfin += (unsigned long long)dg;
@@ -1569,9 +1596,10 @@ __host__ __device__ constexpr size_t dense_ring_offset() {
   return (sizeof(ResidualQ<Off>) * kBfsWarps + sizeof(uint32_t) * kSumWordsMax + 127) & ~(size_t)127;
 }
 template <typename Off, bool D = false>
-__host__ __device__ constexpr size_t dyn_smem_bytes() {  // D (multi-rank): no dense rings
-  return (kDenseR && !D) ? dense_ring_offset<Off>() + (size_t)kBfsWarps * (kDenseR * (1024 + 8 + 4 + 4) + 4)
-                         : sizeof(ResidualQ<Off>) * kBfsWarps + sizeof(uint32_t) * kSumWordsMax;
+__host__ __device__ constexpr size_t dyn_smem_bytes() {  // multi-rank: rings only with PP_DENSE_DIST
+  return (kDenseR && (!D || PP_DENSE_DIST))
+             ? dense_ring_offset<Off>() + (size_t)kBfsWarps * (kDenseR * (1024 + 8 + 4 + 4) + 4)
+             : sizeof(ResidualQ<Off>) * kBfsWarps + sizeof(uint32_t) * kSumWordsMax;
 }
 
 // The BFS loop (Algorithm 1) run by the CTAs of one rank.  D = multi-rank (1D
@@ -1584,7 +1612,7 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
   ResidualQ<Off>* rqs = reinterpret_cast<ResidualQ<Off>*>(dyn_smem);
   uint32_t* ssum = reinterpret_cast<uint32_t*>(dyn_smem + sizeof(ResidualQ<Off>) * kBfsWarps);
   const unsigned warp = threadIdx.x >> 5;
-  if constexpr (!D && kDenseR > 0) {
+  if constexpr (kDenseR > 0 && (!D || PP_DENSE_DIST)) {
     if (a.drec) {
       const DenseRing ring = dense_ring<Off>(dyn_smem, dense_ring_offset<Off>());
       if (lane_id() == 0) {
@@ -1757,12 +1785,12 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
         __syncthreads();
       }
       bool dense = false;
-      if constexpr (!D && kDense)
+      if constexpr (kDense && (!D || PP_DENSE_DIST))
         dense = !ABL && a.drec != nullptr && !a.narrow &&
                 (a.n_noniso - reached) * 8 >= a.n_noniso * (long long)PP_DENSE_MIN8;
       if (dense) {
-        if constexpr (!D && kDense)
-          pull_dense<Off, PARENTS>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp],
+        if constexpr (kDense)
+          pull_dense<Off, PARENTS, D>(a, vis, vis_other, out, d, acc, sh.sfound[warp], rqs[warp],
                                    &sh.work, frout,
                                    dense_ring<Off>(dyn_smem, dense_ring_offset<Off>()));
       } else {
@@ -2113,6 +2141,7 @@ static cudaError_t launch_ranks_t(pp_graph* gs, int P, uint32_t source, int mode
     a.cidx = g->cidx;
     a.symmetric = g->symmetric ? 1 : 0;
     a.drec = g->drec;
+    a.n_noniso = g->n_noniso;  // all ranks' (dense-pull decision)
     a.isolated = g->isolated;
     a.vis0 = g->vis[0];
     a.vis1 = g->vis[1];

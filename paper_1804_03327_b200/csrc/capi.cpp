@@ -128,7 +128,8 @@ struct BootRec {
   cudaIpcMemHandle_t h;  // 64 bytes: the rank's exchange buffer
   int64_t n, lo, hi, nnz;
   int32_t rank, nranks, off64, symmetric;
-  char pad[16];
+  int64_t noniso;  // the block's non-isolated rows (dense-pull decision needs the global sum)
+  char pad[8];
 };
 static_assert(sizeof(BootRec) == 128, "BootRec layout");
 
@@ -140,6 +141,7 @@ pp_status make_record(pp_graph g, BootRec* me) {
   me->lo = g->row_lo;
   me->hi = g->row_hi;
   me->nnz = g->nnz;
+  me->noniso = g->n_noniso_block;
   me->rank = g->me;
   me->nranks = g->nranks;
   me->off64 = g->off64 ? 1 : 0;
@@ -152,7 +154,7 @@ pp_status make_record(pp_graph g, BootRec* me) {
 pp_status attach_records(pp_graph g, const BootRec* all) {
   const int P = g->nranks;
   const XLayout L = xlayout(g->nwords);
-  int64_t in_total = 0;
+  int64_t in_total = 0, noniso = 0;
   for (int q = 0; q < P; ++q) {
     const BootRec& r = all[q];
     int64_t lo, hi, cw;
@@ -163,6 +165,7 @@ pp_status attach_records(pp_graph g, const BootRec* all) {
               "rows [%lld, %lld), offsets %s, %s)", q, (long long)r.n, (long long)r.lo,
               (long long)r.hi, r.off64 ? "64-bit" : "32-bit", r.symmetric ? "symmetric" : "directed");
     in_total += r.nnz;
+    noniso += r.noniso;
   }
   for (int q = 0; q < P; ++q) {
     if (q == g->me || g->ipc_base[q]) continue;
@@ -172,6 +175,7 @@ pp_status attach_records(pp_graph g, const BootRec* all) {
     set_peer(g, q, (char*)base, L);
   }
   g->in_total = in_total;
+  g->n_noniso = noniso;
   g->attached = true;
   return PP_OK;
 }
@@ -304,6 +308,7 @@ pp_status upload_block(pp_ctx ctx, int64_t n, int64_t row_lo, int64_t row_hi, in
   PP_CK(cudaMemsetAsync(g->isolated, 0, sizeof(uint32_t) * g->nwords, st), "memset");
   if (!symmetric && (s = dalloc(&g->odeg, (size_t)std::max<int64_t>(len, 1), &bytes, "out-degrees")) != PP_OK)
     return s;
+  PP_CK(cudaMemsetAsync(g->scount + 5, 0, sizeof(unsigned long long), st), "memset");
   PP_CK(launch_block_prepare(g, d_off, d_coff, len), "block prepare");
   // push structure: transpose of the CSC block (global rows u, owned targets)
   {
@@ -322,10 +327,12 @@ pp_status upload_block(pp_ctx ctx, int64_t n, int64_t row_lo, int64_t row_hi, in
     PP_CK(launch_off_narrow(g, poff64, g->off, n + 1), "narrow push offsets");
     PP_CK(cudaMemsetAsync(g->scount, 0, 4 * sizeof(unsigned long long), st), "memset");
     PP_CK(launch_hcap(g, poff64, n, g->scount, g->scount + 2), "chunk capacity");
-    PP_CK(cudaMemcpyAsync(g->scount_host, g->scount, 32, cudaMemcpyDeviceToHost, st), "copy");
+    PP_CK(cudaMemcpyAsync(g->scount_host, g->scount, 48, cudaMemcpyDeviceToHost, st), "copy");
     PP_CK(cudaStreamSynchronize(st), "sync");
     g->hcap = (int64_t)g->scount_host[0];
     g->max_out_deg = (int64_t)g->scount_host[2];
+    g->n_noniso_block = g->chunk_words * 32 - (int64_t)g->scount_host[5];
+    g->n_noniso = g->n_noniso_block;  // the global count after the bootstrap / team setup
     cudaFree(poff64);
     g->dtmp[1] = nullptr;
   }
@@ -1037,11 +1044,15 @@ pp_status pp_bfs_team(const pp_graph* graphs, int32_t nranks, int64_t source,
   const bool want_parents = o.want_parents && parent;
   // the peers' exchange buffers are on this device: map them directly
   const XLayout L = xlayout(g0->nwords);
-  int64_t in_total = 0;
-  for (int r = 0; r < nranks; ++r) in_total += graphs[r]->nnz;
+  int64_t in_total = 0, noniso = 0;
+  for (int r = 0; r < nranks; ++r) {
+    in_total += graphs[r]->nnz;
+    noniso += graphs[r]->n_noniso_block;
+  }
   for (int r = 0; r < nranks; ++r) {
     for (int q = 0; q < nranks; ++q) set_peer(graphs[r], q, (char*)graphs[q]->xbuf, L);
     graphs[r]->in_total = in_total;
+    graphs[r]->n_noniso = noniso;
   }
   PP_CK(cudaSetDevice(g0->ctx->device), "cudaSetDevice");
   cudaStream_t st = g0->ctx->stream;

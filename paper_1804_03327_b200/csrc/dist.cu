@@ -175,7 +175,9 @@ __global__ void k_fill_push(const int64_t* __restrict__ coff, const uint32_t* __
 // isolated / padding bits of the owned words: local row >= rows (past the block or n), or no
 // in- and no out-edges
 __global__ void k_iso_block(const int64_t* __restrict__ off, const int64_t* __restrict__ coff,
-                            int64_t rows, uint32_t wlo, uint32_t cw, uint32_t* __restrict__ iso) {
+                            int64_t rows, uint32_t wlo, uint32_t cw, uint32_t* __restrict__ iso,
+                            unsigned long long* __restrict__ niso) {
+  unsigned long long cnt = 0;
   for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < cw; w += gridDim.x * blockDim.x) {
     uint32_t bits = 0;
     for (int b = 0; b < 32; ++b) {
@@ -185,7 +187,9 @@ __global__ void k_iso_block(const int64_t* __restrict__ off, const int64_t* __re
       bits |= (isolated ? 1u : 0u) << b;
     }
     iso[wlo + w] = bits;
+    cnt += (unsigned long long)__popc(bits);
   }
+  if (cnt) atomicAdd(niso, cnt);
 }
 
 __global__ void k_odeg(const int64_t* __restrict__ off, int64_t rows, uint32_t* __restrict__ od) {
@@ -258,7 +262,7 @@ cudaError_t launch_block_prepare(pp_graph g, const int64_t* d_off64, const int64
   g->ctx->launches += 1;
   k_iso_block<<<blocks, kBlock, 0, st>>>(d_off64, d_coff64, rows,
                                          (uint32_t)(g->me * g->chunk_words),
-                                         (uint32_t)g->chunk_words, g->isolated);
+                                         (uint32_t)g->chunk_words, g->isolated, g->scount + 5);
   if (g->odeg) {
     g->ctx->launches += 1;
     k_odeg<<<blocks, kBlock, 0, st>>>(d_off64, rows, g->odeg);

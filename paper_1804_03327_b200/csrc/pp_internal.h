@@ -165,7 +165,8 @@ struct pp_graph_s {
   uint32_t* isolated = nullptr;  // nwords: bit = no in- and no out-edges, or padding
   uint32_t* drec = nullptr;      // PP_DENSE: per row {first 6 in-neighbours, caller id, in-degree}
                                  // (32 B; nwords*32 rows, padding rows zero)
-  int64_t n_noniso = 0;          // rows not marked isolated / padding
+  int64_t n_noniso = 0;          // rows not marked isolated / padding (multi-rank: all ranks')
+  int64_t n_noniso_block = 0;    // multi-rank: this block's
   // PP_GRAPH_RELABEL: internal id = rank by decreasing degree (relabel.cu)
   uint32_t* perm = nullptr;  // internal -> caller id (nullptr: ids are the caller's)
   uint32_t* rank = nullptr;  // caller -> internal id
