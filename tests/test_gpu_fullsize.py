@@ -74,3 +74,24 @@ def test_c5_single_gpu_and_teams(ctx):
         team.close()
         del Gs, ds
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("cfg", ["RGG24", "K21"])
+def test_paper_shaped_graphs_bit_exact(ctx, cfg):
+    """The paper's Table-3 shapes at full size (rgg_n_24: 16.8M vertices, 265M edges and
+    ~2,000-3,000 levels; kron_g500-logn21: s21 ef48), relabelled as bench.py uploads: one
+    source, depths bit-exact vs O1, the direction trace vs O4, min-id parents Graph500-valid
+    (O5) -- the high-diameter push path and the dense pull path at scale."""
+    g = synth.make(cfg)
+    G = pp.Graph.from_csr(ctx, g, relabel=True)
+    d = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    p = torch.empty(g.n, dtype=torch.int32, device="cuda")
+    s = int(synth.sources(g, 1, seed=2)[0])
+    st = pp.bfs(G, s, d, p, stats_capacity=70000)
+    exp, L = oracle.bfs(g, s)
+    dd = d.cpu().numpy()
+    assert np.array_equal(dd, exp), cfg
+    t = oracle.trace(g, g, exp)
+    assert st["levels"] == L and np.array_equal(st["dir"][:L], t["dir"])
+    oracle.validate_graph500(g, s, dd, p.cpu().numpy())
+    G.close()
