@@ -291,8 +291,8 @@ __device__ __forceinline__ void append_frontier(bool valid, uint32_t v, Off deg,
 #endif
 constexpr int kU = PP_PUSH_KU;  // edges (push) in flight per lane
 #ifndef PP_LOWLAT_VREC
-#define PP_LOWLAT_VREC 0  // measured neutral; doubles the spills
-#endif
+#define PP_LOWLAT_VREC 1  // round 2b: C4 7.41 -> 7.35 us per level, C2 equal; with
+#endif                    // kU = 2 and the smaller kernel it costs 60 B of spills, not 670
 #ifndef PP_PF_ROWS
 #define PP_PF_ROWS 0  // measured neutral
 #endif
