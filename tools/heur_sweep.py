@@ -7,13 +7,13 @@ sys.path.insert(0, ".")
 import synth
 import paper_1804_03327_b200 as pp
 
-cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
+cfg = sys.argv[1] if len(sys.argv) > 1 and not sys.argv[1].startswith("no") else "C2"
 g = synth.make(cfg)
 ctx = pp.Context(0)
-G = pp.Graph.from_csr(ctx, g)
+G = pp.Graph.from_csr(ctx, g, relabel="norelabel" not in sys.argv)  # bench layout
 depth = torch.empty(g.n, dtype=torch.int32, device="cuda")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-srcs = synth.sources(g, 16, seed=2)
+srcs = synth.sources(g, 32, seed=2)
 
 
 def run(heur, alpha, beta):
