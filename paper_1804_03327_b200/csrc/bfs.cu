@@ -115,6 +115,9 @@ constexpr unsigned long long kWatchdogNs = 4000000000ull;  // 4 s per barrier wa
 // a gpu-scope fence afterwards invalidates this SM's L1 so post-barrier loads see every
 // CTA's writes.  Bit 63 is the abort flag (watchdog), which releases every waiter.
 constexpr unsigned long long kAbortBit = 1ull << 63;
+#ifndef PP_BAR_ACQREL
+#define PP_BAR_ACQREL 0
+#endif
 
 
 __device__ __forceinline__ bool grid_barrier(GridBarrier* b, BfsStatus* st, unsigned& epoch,
@@ -125,7 +128,15 @@ __device__ __forceinline__ bool grid_barrier(GridBarrier* b, BfsStatus* st, unsi
     ++epoch;
     const unsigned long long target = (unsigned long long)epoch * ncta;
     unsigned long long* cnt = reinterpret_cast<unsigned long long*>(&b->count);
+#if PP_BAR_ACQREL
+    // arrival with acquire-release semantics (the last arriver acquires too) and acquire
+    // polling: no trailing fence
+    unsigned long long v;
+    asm volatile("atom.add.acq_rel.gpu.u64 %0, [%1], 1;" : "=l"(v) : "l"(cnt) : "memory");
+    v += 1ull;
+#else
     unsigned long long v = atom_add_release_u64(cnt, 1ull) + 1ull;
+#endif
     if (v < target) {
       unsigned long long t0 = global_timer_ns();
       while ((v = ld_acquire_u64(cnt)) < target) {
@@ -138,7 +149,7 @@ __device__ __forceinline__ bool grid_barrier(GridBarrier* b, BfsStatus* st, unsi
         }
       }
     }
-    __threadfence();
+    if (!PP_BAR_ACQREL) __threadfence();
     s_ok = (v & kAbortBit) ? 0 : 1;
   }
   __syncthreads();
@@ -172,8 +183,15 @@ struct Acc {
 __device__ __forceinline__ void flush_acc(Acc& acc, LevelCtr* out,
                                           unsigned long long (*red)[5]) {
   const unsigned warp = threadIdx.x >> 5;
-  unsigned long long c = warp_sum(acc.c), mf = warp_sum(acc.mf), mfin = warp_sum(acc.mfin),
-                     big = warp_sum(acc.big), cd = warp_sum(acc.cand);
+  unsigned long long c = 0, mf = 0, mfin = 0, big = 0, cd = 0;
+  // a warp with nothing to report (most warps of a small level) skips its 25 shuffles
+  if (__any_sync(kFull, (acc.c | acc.mf | acc.mfin | acc.big | acc.cand) != 0ull)) {
+    c = warp_sum(acc.c);
+    mf = warp_sum(acc.mf);
+    mfin = warp_sum(acc.mfin);
+    big = warp_sum(acc.big);
+    cd = warp_sum(acc.cand);
+  }
   if (lane_id() == 0) {
     red[warp][0] = c;
     red[warp][1] = mf;
@@ -213,6 +231,14 @@ __device__ __forceinline__ unsigned cta_grab(const BfsArgs<Off>& a, unsigned* sc
   if (lane_id() == 0) j = atomicAdd(sctr, 1u);
   j = __shfl_sync(kFull, j, 0);
   return cta_of(a) + j * (unsigned)a.ncta;
+}
+// A phase's FIRST grab is static: warp w takes the CTA's item w, and the shared counter starts
+// at kBfsWarps (set by read_level), so the 32 warps do not serialise on one shared-memory
+// atomic at the start of every level (~1 us on a small level).
+__device__ __forceinline__ unsigned first_j() { return threadIdx.x >> 5; }
+template <typename Off>
+__device__ __forceinline__ unsigned cta_first(const BfsArgs<Off>& a) {
+  return cta_of(a) + first_j() * (unsigned)a.ncta;
 }
 template <typename Off>
 __device__ __forceinline__ unsigned nwarps(const BfsArgs<Off>& a) { return (unsigned)a.ncta * kBfsWarps; }
@@ -550,7 +576,7 @@ __device__ void push_phase(const BfsArgs<Off>& a, const uint4* Lin, unsigned nL,
   const unsigned nRounds = fr ? a.nwords / kPW : (nL + R - 1) / R;
   const unsigned nHC = nH + 32u * nB;  // chunk items: descriptors, then 32 per hub block
   const unsigned total = nHC + nRounds;
-  for (unsigned item = cta_grab(a, sctr); item < total; item = cta_grab(a, sctr)) {
+  for (unsigned item = cta_first(a); item < total; item = cta_grab(a, sctr)) {
     if (item < nHC) {
       bool valid[kU];
       uint32_t u[kU], w[kU];
@@ -990,7 +1016,12 @@ __device__ void pull_phase(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
     vw_next = (k != ~0u && lane < pwn) ? vin[w0n + lane] : 0xFFFFFFFFu;
 #else
   (void)gwork;
+  bool first = true;  // the first grab is static (first_j)
   auto grab = [&]() {
+    if (first) {
+      first = false;
+      return first_j();
+    }
     unsigned j = 0;
     if (lane == 0) j = atomicAdd(sctr, 1u);
     return __shfl_sync(kFull, j, 0);
@@ -1224,10 +1255,14 @@ __device__ void pull_dense(const BfsArgs<Off>& a, const uint32_t* __restrict__ v
   const unsigned seq0 = *R.seq;
   unsigned issued = seq0, cons = seq0;
   // the item after the producer's is grabbed, and its visited words loaded, one item ahead
+  bool first = true;  // the first grab is static (first_j)
   auto grab_item = [&](uint32_t& vw_out) {
-    unsigned j = 0;
-    if (lane == 0) j = atomicAdd(sctr, 1u);
-    j = __shfl_sync(kFull, j, 0);
+    unsigned j = first_j();
+    if (!first) {
+      if (lane == 0) j = atomicAdd(sctr, 1u);
+      j = __shfl_sync(kFull, j, 0);
+    }
+    first = false;
     vw_out = (j < K && lane < kDenseIW) ? vin[wb0 + (cta + j * G) * kDenseIW + lane] : 0xFFFFFFFFu;
     return j;
   };
@@ -1405,7 +1440,7 @@ __device__ void convert_phase(const BfsArgs<Off>& a, const uint32_t* vnew, const
                               uint4* Lout, uint2* Hout, LevelCtr* out, unsigned* sctr) {
   const unsigned lane = lane_id();
   const unsigned nchunks = a.nwords / 32u;
-  for (unsigned item = cta_grab(a, sctr); item < nchunks; item = cta_grab(a, sctr)) {
+  for (unsigned item = cta_first(a); item < nchunks; item = cta_grab(a, sctr)) {
     const unsigned w = item * 32u + lane;
     uint32_t diff = vold ? (vnew[w] & ~vold[w]) : vnew[w];  // multi-rank: vnew = frontier
     while (__ballot_sync(kFull, diff != 0u)) {
@@ -1461,7 +1496,7 @@ __device__ __forceinline__ void read_level(const LevelCtr* out, BfsShared<Off>& 
     sh.lvl[5] = (long long)ld_relaxed_u64(&out->nbig);
     sh.lvl[6] = (long long)ld_relaxed_u32(&out->nB);
     sh.lvl[7] = (long long)ld_relaxed_u64(&out->cand);
-    sh.work = 0u;
+    sh.work = (unsigned)kBfsWarps;  // item j < kBfsWarps is warp j's static first grab
   }
   __syncthreads();
 }
@@ -1674,7 +1709,7 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
     m_u = r.m_u;
     reached = r.reached;
     mf_last = r.mf_last;
-    if (threadIdx.x == 0) sh.work = 0u;
+    if (threadIdx.x == 0) sh.work = (unsigned)kBfsWarps;
     __syncthreads();
   } else {
   // ---- Alg. 1 lines 2-4: d <- 1, f <- e_s, v <- 0 (depth 0 = unvisited) ----
@@ -1806,7 +1841,13 @@ __device__ __forceinline__ void bfs_body(const BfsArgs<Off>& a) {
     if (a.dbg && threadIdx.x == 0 && d - 1 < a.dbg_levels)
       a.dbg[(size_t)(d - 1) * a.ncta + cta] = (long long)global_timer_ns() - t_lvl;
     flush_acc(acc, out, sh.red);
+    // debug phases (pp_bfs_debug_phases): plane 1 = every warp of the CTA done (counters
+    // flushed), plane 2 = the grid barrier released; ns from the level's loop top
+    const bool dbgp = a.dbg && threadIdx.x == 0 && d - 1 < a.dbg_levels;
+    const size_t dplane = (size_t)a.dbg_levels * (size_t)a.ncta, dslot = (size_t)(d - 1) * a.ncta + cta;
+    if (dbgp) a.dbg[dplane + dslot] = (long long)global_timer_ns() - t_lvl;
     if (!level_barrier(a.narrow, a.bar, a.status, epoch, (unsigned)a.ncta)) return;
+    if (dbgp) a.dbg[2 * dplane + dslot] = (long long)global_timer_ns() - t_lvl;
     read_level(out, sh);
     if (D && !exchange<Off>(a, sh, frout, d, epoch, (d == 1) ? indeg_s_own : 0, gtid, gsize,
                             dir == 0, out))
