@@ -72,34 +72,10 @@ constexpr int kMaxRanks = 8;  // 1D row partition: ranks per multi-rank group (o
 constexpr int kMaxCtas = 1024;  // persistent grid size bound (per-CTA work counters)
 
 // Per-level counters, written with atomics during a level, read after the grid barrier.
-// PP_CTR_SPREAD (default): every per-CTA flushed counter (c, m_f, m_fin, nbig, cand) has its
-// own 128-byte L2 line, as do the per-warp light-list appends (nL) and the heavy-chunk appends /
-// work counters: same-line atomics serialise in one L2 slice (148 CTAs x 5 counters on one
-// line before).  Otherwise the five flushed counters share one line.
-#ifndef PP_CTR_SPREAD
-#define PP_CTR_SPREAD 0
-#endif
-#if PP_CTR_SPREAD
-struct LevelCtr {
-  unsigned long long c;      // vertices discovered by the level
-  unsigned long long pc[15];
-  unsigned long long m_f;    // sum of their out-degrees (Eq. 1)
-  unsigned long long pm[15];
-  unsigned long long m_fin;  // sum of their in-degrees (m_u update, directed graphs)
-  unsigned long long pi[15];
-  unsigned long long nbig;   // discoveries with out-degree >= kBig (pull levels)
-  unsigned long long pb[15];
-  unsigned long long cand;   // rows the pull computed (unvisited, non-isolated)
-  unsigned long long pd[15];
-  unsigned int nL;           // next frontier: light-list length
-  unsigned int pad1[31];
-  unsigned int nH, nB;       // next frontier: heavy-chunk count, hub block descriptors
-  unsigned int work, work2;  // dynamic work counters (phase, convert phase)
-  unsigned int nX;           // multi-rank push: discoveries appended to the rank's id list
-  unsigned int pad2[27];
-};
-static_assert(sizeof(LevelCtr) == 7 * 128, "LevelCtr layout");
-#else
+// The three atomic populations sit on separate 128-byte L2 lines: the per-CTA counter flush
+// (c, m_f, m_fin, nbig, cand), the per-warp light-list appends (nL), and the heavy-chunk
+// appends / work counters — same-line atomics serialise in one L2 slice.  (Each flushed
+// counter on its own line measured equal: DESIGN.md §11b.)
 struct LevelCtr {
   unsigned long long c;      // vertices discovered by the level
   unsigned long long m_f;    // sum of their out-degrees (Eq. 1)
@@ -115,7 +91,7 @@ struct LevelCtr {
   unsigned int pad2[27];
 };
 static_assert(sizeof(LevelCtr) == 384, "LevelCtr layout");
-#endif
+
 
 struct LevelStat {
   int dir;

@@ -223,7 +223,11 @@ __device__ __forceinline__ bool sssp_barrier(SsspCtl* c, unsigned& epoch) {
   if (threadIdx.x == 0) {
     ++epoch;
     const unsigned long long target = (unsigned long long)epoch * gridDim.x;
-    unsigned long long v = atom_add_release_u64(&c->bar, 1ull) + 1ull;
+    // acq_rel arrival (the last arriver acquires too), acquire polling, no trailing fence:
+    // the same protocol as bfs.cu's grid barrier
+    unsigned long long v;
+    asm volatile("atom.add.acq_rel.gpu.u64 %0, [%1], 1;" : "=l"(v) : "l"(&c->bar) : "memory");
+    v += 1ull;
     if (v < target) {
       const unsigned long long t0 = global_timer_ns();
       while ((v = ld_acquire_u64(&c->bar)) < target) {
@@ -236,7 +240,6 @@ __device__ __forceinline__ bool sssp_barrier(SsspCtl* c, unsigned& epoch) {
         }
       }
     }
-    __threadfence();
     s_ok = (v & kSsspAbort) ? 0 : 1;
   }
   __syncthreads();
