@@ -35,7 +35,7 @@ def build(force=False, verbose=False):
                                                    "PP_LOWLAT_VREC", "PP_PF_ROWS",
                                                    "PP_SUM_RESID", "PP_DENSE", "PP_DENSE_R",
                                                    "PP_DENSE_MIN8", "PP_DENSE_IW",
-                                                   "PP_CHUNK", "PP_HEAVY", "PP_RQ_EXTRA", "PP_DENSE_DIST", "PP_BAR_ACQREL")
+                                                   "PP_CHUNK", "PP_HEAVY", "PP_RQ_EXTRA", "PP_DENSE_DIST", "PP_BAR_ACQREL", "PP_BAR_SLEEP")
               if os.environ.get(k)]
     odir = os.path.join(HERE, "build")
     os.makedirs(odir, exist_ok=True)

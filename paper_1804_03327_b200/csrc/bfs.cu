@@ -117,6 +117,9 @@ constexpr unsigned long long kWatchdogNs = 4000000000ull;  // 4 s per barrier wa
 // release-arrival + fence.sc form is PP_BAR_ACQREL=0).  Bit 63 is the abort flag (watchdog),
 // which releases every waiter.
 constexpr unsigned long long kAbortBit = 1ull << 63;
+#ifndef PP_BAR_SLEEP
+#define PP_BAR_SLEEP 16  // ns of back-off between barrier polls
+#endif
 #ifndef PP_BAR_ACQREL
 #define PP_BAR_ACQREL 1  // measured: C4 7.09 -> 6.63 us per level, C2 +3%
 #endif
@@ -142,7 +145,7 @@ __device__ __forceinline__ bool grid_barrier(GridBarrier* b, BfsStatus* st, unsi
     if (v < target) {
       unsigned long long t0 = global_timer_ns();
       while ((v = ld_acquire_u64(cnt)) < target) {
-        __nanosleep(16);
+        if (PP_BAR_SLEEP) __nanosleep(PP_BAR_SLEEP);
         if (global_timer_ns() - t0 > kWatchdogNs) {
           atomicExch(&st->error, (int)PP_ERR_TIMEOUT);
           atomicOr(cnt, kAbortBit);
